@@ -1,0 +1,563 @@
+"""-m "not gpu" pins of the CPU oracle against what the paper and the mathematics fix.
+
+Each test names the passage it pins.  Nothing here reuses oracle code for the
+expected value: closed forms are evaluated independently, dense references come
+from tests/helpers.py (numpy), brute force enumerates small cases, and golden
+values come from tests/golden/ (each file cites its source).
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+import helpers as H
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def path_graph(gen, n, d=None):
+    return gen.from_edges(n, [(i, i + 1) for i in range(n - 1)], d=d)
+
+
+# ----------------------------------------------------------------- core sparse
+def test_spmv_inf_norm_spec_examples(oracle_mod, gen_mod):
+    g = gold("spec_examples.json")
+    p = path_graph(gen_mod, 4)
+    assert np.array_equal(oracle_mod.spmv(p.rp, p.ci, p.val, np.ones(4)), g["spmv_path4_ones"])
+    assert np.array_equal(oracle_mod.spmv(p.rp, p.ci, p.val, np.arange(4.0)), g["spmv_path4_ramp"])
+    assert oracle_mod.inf_norm(p.rp, p.ci, p.val) == g["inf_norm_path4"]
+    q = gen_mod.grid2d(3)
+    A = H.dense(q.rp, q.ci, q.val)
+    assert oracle_mod.inf_norm(q.rp, q.ci, q.val) == np.abs(A).sum(1).max()
+    # 5-pt Dirichlet operator (with d): still 8; 7-pt scaled by h: 12 h
+    h0 = oracle_mod.Hierarchy(q.rp, q.ci, q.val, q.d, 1, 2, coarsest_size=100)
+    assert h0.level_info(0)["lambda1"] == 8.0
+    r = gen_mod.grid3d(3)
+    h1 = oracle_mod.Hierarchy(r.rp, r.ci, r.val, r.d, 1, 2, coarsest_size=100)
+    assert h1.level_info(0)["lambda1"] == pytest.approx(12.0 / 4.0, rel=1e-15)
+    rng = np.random.default_rng(0)
+    rg = gen_mod.random_graph(50, 4, seed=1, weighted=True)
+    x = rng.standard_normal(50)
+    assert np.allclose(oracle_mod.spmv(rg.rp, rg.ci, rg.val, x), H.dense(rg.rp, rg.ci, rg.val) @ x, rtol=1e-14)
+
+
+# ----------------------------------------------------------------- E_m, kappa
+def test_Em_closed_forms(oracle_mod):
+    """P:167 (2 kappa delta^m / ((kappa-1)(a^2-1))) and P:177 (delta^m (kappa-1)/2) agree with the oracle."""
+    for kappa in (2.0, 9.0, 10.0, 100.0):
+        delta = (np.sqrt(kappa) - 1) / (np.sqrt(kappa) + 1)
+        a = (kappa + 1) / (kappa - 1)
+        for m in range(0, 8):
+            e167 = 2 * kappa * delta ** m / ((kappa - 1) * (a * a - 1))
+            e177 = delta ** m * (kappa - 1) / 2
+            assert oracle_mod.Em(m, kappa) == pytest.approx(e167, rel=1e-13)
+            assert oracle_mod.Em(m, kappa) == pytest.approx(e177, rel=1e-13)
+    assert oracle_mod.Em(3, 9.0) == 0.5  # delta(9) = 1/2 exactly
+    assert oracle_mod.Em(0, 10.0) == pytest.approx(4.5)
+
+
+def test_golden_coefficients_and_kappa_rule(oracle_mod):
+    g = gold("poly_coeffs.json")
+    for row in g["rows"]:
+        k = row["kappa"]
+        a, b = oracle_mod.poly_coeffs(1.0, k, 4)
+        assert b[0] == pytest.approx(row["beta0"], rel=1e-14)
+        assert a[1] == pytest.approx(row["alpha1"], rel=1e-14)
+        assert b[1] == pytest.approx(row["beta1"], rel=1e-14)
+        assert a[2] == pytest.approx(row["alpha2"], rel=1e-14) and a[3] == a[2] and a[4] == a[2]
+        assert b[2] == pytest.approx(row["beta2"], rel=1e-14) and b[4] == b[2]
+        for m in (2, 3, 4):
+            assert oracle_mod.Em(m, k) == pytest.approx(row[f"E{m}"], rel=1e-12)
+        # beta scales as 1/lambda1
+        a8, b8 = oracle_mod.poly_coeffs(8.0, k, 4)
+        assert np.allclose(b8 * 8.0, b, rtol=1e-15) and np.array_equal(a8, a)
+    assert oracle_mod.kappa_rule(1) == pytest.approx(g["kappa_star"]["1"], rel=1e-15)
+    assert oracle_mod.kappa_rule(2) == pytest.approx(g["kappa_star"]["2"], rel=1e-15)
+    for m in (3, 4, 5):
+        assert oracle_mod.kappa_rule(m) == 10.0  # P:327 lambda0 = lambda1/10 whenever E_m(10) < 1
+    # R1: E_m(kappa*) = 1/2 exactly for the rule's m
+    assert oracle_mod.Em(2, oracle_mod.kappa_rule(2)) == pytest.approx(0.5, abs=1e-15)
+    t = np.sqrt(oracle_mod.kappa_rule(2))
+    assert t ** 3 - 3 * t ** 2 + 2 * t - 2 == pytest.approx(0.0, abs=1e-13)
+
+
+# ----------------------------------------------------------------- smoother
+def _diag_q(oracle_mod, xs, l1, kappa, m):
+    n = len(xs)
+    rp = np.arange(n + 1)
+    ci = np.arange(n)
+    a, b = oracle_mod.poly_coeffs(l1, kappa, m)
+    return oracle_mod.smooth(rp, ci, xs, m, a, b, np.ones(n), np.zeros(n))
+
+
+@pytest.mark.parametrize("kappa", [9.0, 10.0, 6.3573556258858871, 30.0])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5])
+def test_smoother_is_best_uniform_approximation(oracle_mod, kappa, m):
+    """S(1, 0) on diag(x) = q_m(x): equals an independent Remez best approximation to 1/x on
+    [lambda1/kappa, lambda1], max|1 - x q_m| = E_m, lambda1 an
+    alternation point, and the Chebyshev closed form."""
+    l1 = 8.0
+    l0 = l1 / kappa
+    xs = np.linspace(l0, l1, 4001)
+    q = _diag_q(oracle_mod, xs, l1, kappa, m)
+    qr, Estar = H.remez_inv(l0, l1, m)
+    assert np.max(np.abs(q - qr(xs))) <= 1e-7 * np.max(np.abs(q))
+    r = 1 - xs * q
+    Em = (np.sqrt(kappa) - 1) ** m / (np.sqrt(kappa) + 1) ** m * (kappa - 1) / 2
+    assert np.max(np.abs(r)) == pytest.approx(Em, rel=1e-12)
+    assert r[-1] == pytest.approx((-1) ** (m + 1) * Em, rel=1e-12)  # value at lambda1
+    assert Estar * l1 == pytest.approx(Em, rel=1e-7)
+    assert np.max(np.abs(r - H.cheb_closed_form_r(xs, l0, l1, m))) < 1e-13 * max(1, Em)
+    # (1 - r)/x is a polynomial of degree m: interpolate on m+1 nodes, predict elsewhere
+    nodes = np.linspace(l0, l1, m + 1)
+    qn = _diag_q(oracle_mod, nodes, l1, kappa, m)
+    coef = np.polyfit(nodes, qn, m)
+    assert np.max(np.abs(np.polyval(coef, xs) - q)) < 1e-9 * np.max(np.abs(q))
+    # r(0) = 1: q finite at 0 (x=0 row gives S(1,0)=q(0), and 1 - 0*q = 1 trivially); check continuity
+    q0 = _diag_q(oracle_mod, np.array([1e-300]), l1, kappa, m)
+    assert np.isfinite(q0).all()
+
+
+def test_smoother_matrix_function(oracle_mod, gen_mod):
+    """S(f, x0) = x0 + q_m(A)(f - A x0) with q_m(A) from a dense eigendecomposition."""
+    rng = np.random.default_rng(5)
+    p = gen_mod.random_graph(40, 5, seed=7, weighted=True)
+    A = H.A0_dense(p)
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 1, 3, coarsest_size=1000)
+    l1 = np.abs(A).sum(1).max()
+    assert hier.level_info(0)["lambda1"] == pytest.approx(l1, rel=1e-15)
+    kappa = hier.level_info(0)["kappa"]
+    qf = H.q_closed_form(l1 / kappa, l1, 3)
+    R = H.matfun_sym(A, qf)
+    f = rng.standard_normal(40)
+    x0 = rng.standard_normal(40)
+    x = hier.smooth(0, f, x0)
+    ref = x0 + R @ (f - A @ x0)
+    assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+    # exact solution is a fixed point
+    xs = np.linalg.solve(A, f)
+    assert np.allclose(hier.smooth(0, f, xs), xs, rtol=1e-12, atol=1e-12)
+
+
+# ----------------------------------------------------------------- matching
+def _random_pass_graph(rng, n, deg, maxw):
+    e = {(min(a, b), max(a, b)) for a, b in rng.integers(0, n, (int(n * deg / 2), 2)) if a != b}
+    e = sorted(e)
+    w = rng.integers(1, maxw + 1, len(e))
+    rows = [a for a, b in e] + [b for a, b in e]
+    cols = [b for a, b in e] + [a for a, b in e]
+    ww = list(w) + list(w)
+    M = sp.csr_matrix((np.array(ww, dtype=np.int64), (rows, cols)), shape=(n, n))
+    M.sort_indices()
+    return M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data.astype(np.int64), e, w
+
+
+def test_handshake_equals_edge_greedy(oracle_mod):
+    """A1: the parallel handshake and the sequential edge-greedy rule give the same matching."""
+    rng = np.random.default_rng(11)
+    for trial in range(120):
+        n = int(rng.integers(2, 300))
+        rp, ci, w, _, _ = _random_pass_graph(rng, n, rng.uniform(0.5, 8), int(rng.integers(1, 4)))
+        m0, _ = oracle_mod.match(rp, ci, w, seed=trial, level=trial % 3, pass_=trial % 4, rule=0)
+        m1, rounds = oracle_mod.match(rp, ci, w, seed=trial, level=trial % 3, pass_=trial % 4, rule=1)
+        assert np.array_equal(m0, m1)
+        # matching invariants: symmetric, along edges, maximal
+        for v in range(n):
+            u = m0[v]
+            if u >= 0:
+                assert m0[u] == v and u in ci[rp[v]:rp[v + 1]]
+            else:
+                assert all(m0[x] >= 0 for x in ci[rp[v]:rp[v + 1]])
+
+
+def test_matching_brute_force_unique(oracle_mod):
+    """Brute force on <= 10-vertex graphs with the test's own key function (docs/keys.md): the
+    unique matching M in which every non-M edge touches a larger-key M edge is the oracle's."""
+    rng = np.random.default_rng(3)
+    for trial in range(40):
+        n = int(rng.integers(3, 11))
+        rp, ci, w, e, ew = _random_pass_graph(rng, n, 3.0, 2)
+        if len(e) == 0 or len(e) > 14:
+            continue
+        keys = [H.edge_key(ew[k], a, b, 7, 1, 2) for k, (a, b) in enumerate(e)]
+        keys = [(int(w_), h_, lo_, hi_) for (w_, h_, lo_, hi_) in keys]
+        # the oracle's hash equals the test's independent SplitMix64 implementation
+        assert all(oracle_mod.edge_hash(7, 1, 2, int(a), int(b)) == keys[k][1] for k, (a, b) in enumerate(e))
+        sols = []
+        for mask in range(1 << len(e)):
+            M = [k for k in range(len(e)) if mask >> k & 1]
+            verts = [v for k in M for v in e[k]]
+            if len(verts) != len(set(verts)):
+                continue
+            ok = True
+            for k in range(len(e)):
+                if k in M:
+                    continue
+                if not any(set(e[k]) & set(e[j]) and keys[j] > keys[k] for j in M):
+                    ok = False
+                    break
+            if ok:
+                sols.append(M)
+        assert len(sols) == 1
+        mate, _ = oracle_mod.match(rp, ci, w, seed=7, level=1, pass_=2, rule=0)
+        got = sorted((v, int(mate[v])) for v in range(n) if mate[v] > v)
+        assert got == sorted((int(e[k][0]), int(e[k][1])) for k in sols[0])
+
+
+def _check_partition(rp, ci, agg, nc):
+    n = len(agg)
+    assert agg.min() >= 0 and agg.max() == nc - 1 and len(np.unique(agg)) == nc
+    G = sp.csr_matrix((np.ones(len(ci)), ci, rp), shape=(n, n))
+    import scipy.sparse.csgraph as csg
+    for I in range(nc):
+        mem = np.flatnonzero(agg == I)
+        ncomp, _ = csg.connected_components(G[mem][:, mem], directed=False)
+        assert ncomp == 1  # P:70 "all subgraphs ... non empty and connected"
+    # numbering: ids increase with the aggregate's leader (min vertex of its pair <= min member ... monotone)
+    first = np.array([np.flatnonzero(agg == I).min() for I in range(nc)])
+    return first
+
+
+def test_aggregate_pass_invariants(oracle_mod):
+    rng = np.random.default_rng(21)
+    for trial in range(40):
+        n = int(rng.integers(2, 200))
+        rp, ci, w, _, _ = _random_pass_graph(rng, n, rng.uniform(1, 6), 2)
+        agg0, nc0 = oracle_mod.aggregate_pass(rp, ci, w, seed=trial, rule=0)
+        agg1, nc1 = oracle_mod.aggregate_pass(rp, ci, w, seed=trial, rule=1)
+        assert nc0 == nc1 and np.array_equal(agg0, agg1)
+        _check_partition(rp, ci, agg0, nc0)
+        mate, _ = oracle_mod.match(rp, ci, w, seed=trial)
+        # every matched pair shares an aggregate; every aggregate has exactly one leader pair or is an isolated singleton
+        for v in range(n):
+            if mate[v] >= 0:
+                assert agg0[v] == agg0[mate[v]]
+        for I in range(nc0):
+            mem = np.flatnonzero(agg0 == I)
+            pairs = [v for v in mem if mate[v] > v]
+            iso = [v for v in mem if rp[v + 1] == rp[v]]
+            assert (len(pairs) == 1 and not iso) or (len(mem) == 1 and len(iso) == 1)
+        # A4: ids are the rank of the leader (pair min) in increasing vertex order
+        leaders = [min(np.flatnonzero(agg0 == I)[[mate[v] >= 0 or rp[v + 1] == rp[v] for v in np.flatnonzero(agg0 == I)]]) for I in range(nc0)]
+        assert leaders == sorted(leaders)
+
+
+# ----------------------------------------------------------------- Galerkin
+def test_galerkin_dense_and_invariants(oracle_mod, gen_mod):
+    """A_H = P^T A P as entry sums; for d = 0 a weighted graph Laplacian with
+    zero row sums and negative off-diagonals; 1^T A_H 1 = 1^T A 1; nnz(A_H) <= nnz(A)."""
+    rng = np.random.default_rng(2)
+    for trial in range(20):
+        n = int(rng.integers(5, 200))
+        p = gen_mod.random_graph(n, 5, seed=trial, weighted=True, dirichlet=bool(trial % 2))
+        A = H.A0_dense(p)
+        agg = rng.integers(0, max(1, n // 4), n).astype(np.int32)
+        _, agg = np.unique(agg, return_inverse=True)
+        agg = agg.astype(np.int32)
+        nc = int(agg.max()) + 1
+        Asp = sp.csr_matrix(A)
+        Asp.sort_indices()
+        rp, ci, v = oracle_mod.quotient(Asp.indptr, Asp.indices, Asp.data, None, agg, nc, drop_diag=False)
+        AH = H.dense(rp, ci, v, nc)
+        P = H.P_dense(agg, nc)
+        assert np.allclose(AH, P.T @ A @ P, rtol=1e-13, atol=1e-13)
+        assert np.allclose(AH, AH.T, rtol=1e-14, atol=1e-14)
+        assert len(ci) <= Asp.nnz
+        assert AH.sum() == pytest.approx(A.sum(), rel=1e-12)
+        off = AH - np.diag(np.diag(AH))
+        assert (off[np.abs(off) > 0] < 0).all()
+        if p.d is None:
+            assert np.allclose(AH.sum(1), 0.0, atol=1e-12)
+        # pass-graph quotient: multiplicities = number of fine edges joining I, J; no self loops
+        W = (np.abs(A - np.diag(np.diag(A))) > 0).astype(np.int64)
+        Wsp = sp.csr_matrix(W)
+        Wsp.sort_indices()
+        qrp, qci, qw = oracle_mod.quotient(Wsp.indptr, Wsp.indices, None, Wsp.data, agg, nc, drop_diag=True)
+        WH = H.dense(qrp, qci, qw.astype(float), nc)
+        ref = P.T @ W @ P
+        np.fill_diagonal(ref, 0)
+        assert np.array_equal(WH, ref)
+    g = gold("spec_examples.json")
+    p4 = path_graph(gen_mod, 4)
+    rp, ci, v = oracle_mod.quotient(p4.rp, p4.ci, p4.val, None, np.array([0, 0, 1, 1], np.int32), 2, False)
+    assert np.array_equal(H.dense(rp, ci, v, 2), g["galerkin_path4_pairs"])
+
+
+def _hier_check(oracle_mod, p, hier, exact):
+    A = sp.csr_matrix((p.val, p.ci, p.rp), shape=(p.n, p.n))
+    if p.d is not None:
+        A = A + sp.diags(p.d)
+    A = sp.csr_matrix(A)
+    for l in range(hier.nlev):
+        rp, ci, v = hier.level_csr(l)
+        Al = sp.csr_matrix((v, ci, rp), shape=(len(rp) - 1,) * 2)
+        diff = abs(Al - A)
+        tol = 0.0 if exact else 1e-12 * abs(A).max()
+        assert diff.max() <= tol
+        info = hier.level_info(l)
+        assert info["lambda1"] == pytest.approx(np.abs(A).sum(1).max(), rel=1e-15)
+        if l < hier.nlev - 1:
+            agg = hier.level_agg(l)
+            nc = info["nc"]
+            _check_partition(rp, ci, agg, nc)
+            P = sp.csr_matrix((np.ones(len(agg)), (np.arange(len(agg)), agg)), shape=(len(agg), nc))
+            A = sp.csr_matrix(P.T @ A @ P)
+            A.sum_duplicates()
+
+
+def test_hierarchy_C1_exact(oracle_mod, gen_mod):
+    """Every level of the C1 hierarchy is exactly P^T A P of the one above (integer-valued)."""
+    p = gen_mod.problem("C1")
+    hier = oracle_mod.setup_problem(p)
+    assert hier.nlev >= 3  # A6: coarsest 100 keeps the inner FCG recursion exercised
+    _hier_check(oracle_mod, p, hier, exact=True)
+    hier2 = oracle_mod.setup_problem(p, rule=1)
+    for l in range(hier.nlev - 1):
+        assert np.array_equal(hier.level_agg(l), hier2.level_agg(l))  # A1 on a real hierarchy
+    hier3 = oracle_mod.setup_problem(p)
+    for l in range(hier.nlev):  # determinism
+        assert all(np.array_equal(a, b) for a, b in zip(hier.level_csr(l), hier3.level_csr(l)))
+
+
+def test_hierarchy_3d_and_singular(oracle_mod, gen_mod):
+    p = gen_mod.grid3d(10)
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 3, 3, coarsest_size=20)
+    _hier_check(oracle_mod, p, hier, exact=False)
+    q = gen_mod.rgg(3000, seed=1)
+    hs = oracle_mod.Hierarchy(q.rp, q.ci, q.val, None, 2, 2, coarsest_size=30)
+    assert hs.singular
+    _hier_check(oracle_mod, q, hs, exact=True)
+    for l in range(hs.nlev):
+        rp, ci, v = hs.level_csr(l)
+        rs = np.add.reduceat(v, rp[:-1]) if len(rp) > 1 else []
+        assert np.allclose(rs, 0.0, atol=1e-12)  # A_H 1 = 0
+
+
+# ----------------------------------------------------------------- coarsest
+def test_coarse_solve(oracle_mod, gen_mod):
+    rng = np.random.default_rng(4)
+    p = gen_mod.random_graph(60, 4, seed=3, weighted=True)
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 1, 2, coarsest_size=100)
+    assert hier.nlev == 1
+    A = H.A0_dense(p)
+    b = rng.standard_normal(60)
+    x = hier.coarse_solve(b)
+    assert np.linalg.norm(A @ x - b) <= 1e-12 * np.linalg.norm(b)
+    q = gen_mod.random_graph(60, 4, seed=4, weighted=True, dirichlet=False)
+    hs = oracle_mod.Hierarchy(q.rp, q.ci, q.val, None, 1, 2, coarsest_size=100)
+    As = H.A0_dense(q)
+    x = hs.coarse_solve(b)
+    assert abs(x.mean()) < 1e-13
+    assert np.allclose(x, H.pinv_sym(As) @ b, rtol=1e-10, atol=1e-12)
+    # S:64 example: path-2, b = (1,-1) -> (0.5,-0.5)
+    p2 = path_graph(gen_mod, 2)
+    h2 = oracle_mod.Hierarchy(p2.rp, p2.ci, p2.val, None, 1, 2, coarsest_size=10)
+    assert np.allclose(h2.coarse_solve(np.array([1.0, -1.0])), [0.5, -0.5], atol=1e-15)
+
+
+# ----------------------------------------------------------------- two-level / k-cycle
+def _seed_for_pairs(gen_mod):
+    """A seed whose level-0/pass-0 keys make {0,1},{2,3} the matching of path-4."""
+    for s in range(100):
+        k = [H.edge_key(1, a, a + 1, s, 0, 0) for a in range(3)]
+        if k[1] < max(k[0], k[2]):
+            return s
+    raise AssertionError
+
+
+def test_golden_W1(oracle_mod, gen_mod):
+    g = gold("w1_path4.json")
+    p = path_graph(gen_mod, 4, d=[1, 0, 0, 0])
+    seed = _seed_for_pairs(gen_mod)
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 1, g["m"], coarsest_size=2, seed=seed)
+    assert hier.nlev == 2
+    assert list(hier.level_agg(0)) == g["aggregates"]
+    info = hier.level_info(0)
+    assert info["lambda1"] == g["lambda1"] and info["kappa"] == g["kappa"]
+    a, b = hier.level_coeffs(0)
+    assert np.allclose(a, g["alpha"], rtol=1e-15) and np.allclose(b, g["beta"], rtol=1e-15)
+    rp, ci, v = hier.level_csr(1)
+    assert np.array_equal(H.dense(rp, ci, v, 2), g["A_H"])
+    e0 = np.array([1.0, 0, 0, 0])
+    assert np.allclose(hier.smooth(0, e0, np.zeros(4)), g["q3_A_e0"], rtol=1e-14, atol=1e-15)
+    Be0 = hier.precond(e0, nu=2)
+    assert np.allclose(Be0, g["B_e0"], rtol=1e-14, atol=1e-15)
+    A = np.array(g["A"], float)
+    B = np.column_stack([hier.precond(np.eye(4)[j]) for j in range(4)])
+    assert np.allclose(np.sort(np.linalg.eigvals(B @ A).real), g["eig_BA"], atol=1e-12)
+
+
+@pytest.mark.parametrize("singular", [False, True])
+@pytest.mark.parametrize("m", [2, 3, 4])
+def test_two_level_dense_formula(oracle_mod, gen_mod, singular, m):
+    """B(r) equals Rbar + (I-RA) P A_H^+ P^T (I-AR) with R = q_m(A) from the closed form;
+    B symmetric; eig(BA) in (0, 1] when E_m < 1."""
+    rng = np.random.default_rng(m + 10 * singular)
+    p = gen_mod.random_graph(120, 5, seed=m, weighted=True, dirichlet=not singular)
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, m, coarsest_size=60)
+    assert hier.nlev == 2
+    A = H.A0_dense(p)
+    l1 = hier.level_info(0)["lambda1"]
+    kappa = hier.level_info(0)["kappa"]
+    R = H.matfun_sym(A, H.q_closed_form(l1 / kappa, l1, m))
+    agg = hier.level_agg(0)
+    P = H.P_dense(agg, hier.level_info(0)["nc"])
+    AH = P.T @ A @ P
+    AHi = H.pinv_sym(AH) if singular else np.linalg.inv(AH)
+    B = H.two_level_B(A, P, R, AHi)
+    Bo = np.column_stack([hier.precond(np.eye(120)[j]) for j in range(120)])
+    assert np.linalg.norm(Bo - B) <= 1e-10 * np.linalg.norm(B)
+    r = rng.standard_normal(120)
+    assert np.linalg.norm(hier.precond(r) - B @ r) <= 1e-10 * np.linalg.norm(B @ r)
+    assert np.allclose(Bo, Bo.T, atol=1e-10 * np.abs(Bo).max())
+    ev = np.linalg.eigvals(Bo @ A).real
+    if singular:
+        ev = np.sort(ev)[1:]  # drop the kernel
+    assert ev.min() > 0 and ev.max() <= 1 + 1e-10
+
+
+def test_kcycle_partial_pins(oracle_mod, gen_mod):
+    """Multilevel k-cycle: positive homogeneity B(cr) = cB(r); the linear V-cycle switch is
+    symmetric and equals the dense recursion B_l = Rbar + (I-RA)P B_{l+1} P^T (I-AR)."""
+    p = gen_mod.grid2d(18)
+    hk = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=10)
+    assert hk.nlev >= 3
+    rng = np.random.default_rng(9)
+    r = rng.standard_normal(p.n)
+    z = hk.precond(r)
+    assert np.allclose(hk.precond(3.5 * r), 3.5 * z, rtol=1e-13, atol=1e-13)
+    hv = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=10, cycle=1)
+    s = rng.standard_normal(p.n)
+    assert (hv.precond(r) @ s) == pytest.approx(r @ hv.precond(s), rel=1e-10)
+    # dense recursion
+    mats = []
+    for l in range(hv.nlev):
+        rp, ci, v = hv.level_csr(l)
+        mats.append(H.dense(rp, ci, v))
+    Bl = np.linalg.inv(mats[-1])
+    for l in range(hv.nlev - 2, -1, -1):
+        A = mats[l]
+        l1 = hv.level_info(l)["lambda1"]
+        kap = hv.level_info(l)["kappa"]
+        R = H.matfun_sym(A, H.q_closed_form(l1 / kap, l1, 3))
+        P = H.P_dense(hv.level_agg(l), hv.level_info(l)["nc"])
+        Bl = H.two_level_B(A, P, R, Bl)
+    assert np.linalg.norm(hv.precond(r) - Bl @ r) <= 1e-10 * np.linalg.norm(Bl @ r)
+    # two levels: k-cycle == two-level B (no inner FCG runs)
+    h2 = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=200)
+    h2v = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=200, cycle=1)
+    assert h2.nlev == 2 and np.allclose(h2.precond(r), h2v.precond(r), rtol=0, atol=0)
+
+
+def test_fcg_equals_pcg_and_exact_precond(oracle_mod, gen_mod):
+    """FCG == PCG when B is linear SPD and restart >= max_iter; FCG with B = A^{-1}
+    converges in one iteration."""
+    p = gen_mod.grid2d(20)
+    hv = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=10, cycle=1, restart=1000)
+    A = H.A0_dense(p)
+    b = gen_mod.rhs(p.n, 1)
+    res = hv.solve(b, tol=1e-10)
+    x, k, _ = H.pcg(A, b, lambda r: hv.precond(r), 1e-10, 500)
+    assert res["status"] == 0 and res["iters"] == k
+    assert np.linalg.norm(res["x"] - x) <= 1e-8 * np.linalg.norm(x)
+    h1 = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=1000)
+    assert h1.nlev == 1
+    r1 = h1.solve(b, tol=1e-10)
+    assert r1["iters"] == 1 and r1["relres"] < 1e-12
+
+
+def test_full_solve_C1(oracle_mod, gen_mod):
+    """relres <= tol on the recursive and the true residual; error vs a sparse direct solve within
+    tol * sqrt(cond(A)) in the A-norm (SURVEY 8(c) pins, 'Full solve')."""
+    p = gen_mod.problem("C1")
+    hier = oracle_mod.setup_problem(p)
+    b = gen_mod.rhs(p.n, 0)
+    res = hier.solve(b, tol=1e-8, nu=2)
+    assert res["status"] == 0 and res["relres"] <= 1e-8 and res["true_relres"] <= 1.5e-8
+    assert 8 <= res["iters"] <= 30
+    A = sp.csr_matrix((p.val, p.ci, p.rp), shape=(p.n, p.n)) + sp.diags(p.d)
+    xs = spla.spsolve(sp.csc_matrix(A), b)
+    e = res["x"] - xs
+    cond = 8.0 / (2 * (1 - np.cos(np.pi / 65)))  # 5-pt Dirichlet spectrum
+    assert np.sqrt(e @ (A @ e)) <= 1e-8 * np.sqrt(cond) * np.sqrt(xs @ (A @ xs))
+
+
+def test_singular_solve(oracle_mod, gen_mod):
+    q = gen_mod.rgg(4000, seed=2)
+    hier = oracle_mod.Hierarchy(q.rp, q.ci, q.val, None, 3, 3, coarsest_size=50)
+    b = gen_mod.rhs(q.n, 0)
+    res = hier.solve(b, tol=1e-8)
+    assert res["status"] == 0 and res["true_relres"] <= 2e-8
+
+
+def test_error_codes(oracle_mod, gen_mod):
+    p = path_graph(gen_mod, 5)
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.Hierarchy(p.rp, p.ci, p.val, None, 0, 2)
+    assert e.value.code == -1
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.Hierarchy(p.rp, p.ci, p.val, None, 1, 2, kappa=10.0)  # A9: E_2(10) >= 1
+    assert e.value.code == -1
+    bad = p.val.copy()
+    bad[1] = 0.5  # positive off-diagonal
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.Hierarchy(p.rp, p.ci, bad, None, 1, 2)
+    assert e.value.code == -2
+    asym = p.val.copy()
+    asym[1] = -2.0
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.Hierarchy(p.rp, p.ci, asym, None, 1, 2)
+    assert e.value.code == -2
+    # diagonal-only matrix above coarsest size: coarsening stagnates
+    n = 200
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.Hierarchy(np.zeros(n + 1, np.int64), np.zeros(0, np.int32), np.zeros(0), np.ones(n), 1, 2, coarsest_size=10)
+    assert e.value.code == -7
+
+
+def test_missing_diagonal_inserted(oracle_mod, gen_mod):
+    p = gen_mod.random_graph(30, 4, seed=5, weighted=True)
+    keep = p.ci != np.repeat(np.arange(p.n), np.diff(p.rp))
+    rp = np.concatenate([[0], np.cumsum(np.add.reduceat(keep.astype(np.int64), p.rp[:-1]))])
+    h_full = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 1, 2, coarsest_size=10)
+    h_nod = oracle_mod.Hierarchy(rp, p.ci[keep], p.val[keep], p.d, 1, 2, coarsest_size=10)
+    for l in range(h_full.nlev):
+        a, b = h_full.level_csr(l), h_nod.level_csr(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.allclose(a[2], b[2], rtol=1e-15)
+
+
+def test_decoupled_aggregation(oracle_mod, gen_mod):
+    """A20: with nparts = P no aggregate crosses a row block; coarse blocks stay contiguous."""
+    p = gen_mod.grid2d(40)
+    for P in (2, 3, 4):
+        hier = oracle_mod.setup_problem(gen_mod.problem("C1", size=40), nparts=P, gather_rows=100)
+        n = p.n
+        blk = np.zeros(n, np.int64)
+        for b in range(P):
+            blk[b * n // P:(b + 1) * n // P] = b
+        for l in range(hier.nlev - 1):
+            info = hier.level_info(l)
+            agg = hier.level_agg(l)
+            if info["nparts"] > 1:
+                for I in range(info["nc"]):
+                    assert len(np.unique(blk[agg == I])) == 1
+                cblk = np.zeros(info["nc"], np.int64)
+                cblk[agg] = blk
+                assert np.all(np.diff(cblk) >= 0)
+                blk = cblk
+            else:
+                blk = np.zeros(info["nc"], np.int64)
+        res = hier.solve(gen_mod.rhs(n, 0), tol=1e-8)
+        assert res["status"] == 0
+    h1 = oracle_mod.setup_problem(gen_mod.problem("C1", size=40), nparts=1)
+    h1b = oracle_mod.setup_problem(gen_mod.problem("C1", size=40))
+    assert np.array_equal(h1.level_agg(0), h1b.level_agg(0))
