@@ -1,0 +1,138 @@
+// amg_internal.h -- internal declarations of libamg_b200.so (host launchers of the sm_100a
+// kernels in k_setup.cu / k_solve.cu, used by driver.cu).  Not part of the ABI (include/amg.h).
+// Shares nothing with oracle/ (the CPU oracle is test infrastructure only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace amg {
+
+constexpr int kMaxDeg = 16;      // poly_degree m <= kMaxDeg
+constexpr int kMaxLevels = 48;
+constexpr int kMaxWin = 16;      // restart window / inner nu <= kMaxWin
+constexpr int kBlock = 256;      // threads per block of the tile / vector kernels
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define CK(call) ::amg::cuda_check((call), #call, __FILE__, __LINE__)
+
+// ---------------------------------------------------------------- device views
+struct Csr {           // A_l: int32 row_ptr / col, fp64 values; arrays padded by >= 4 elements
+    int n = 0;
+    int64_t nnz = 0;
+    int* rp = nullptr;
+    int* ci = nullptr;
+    double* v = nullptr;
+};
+
+struct Tiles {         // row tiles of the SpMV-class kernels: tile t = rows [row[t], row[t+1])
+    int ntiles = 0;
+    int cap = 0;       // shared-memory entry capacity; tiles with more nnz (single long rows) use the long path
+    int grid = 0;      // resident grid used by the grid-stride launch
+    int* row = nullptr;
+};
+
+struct DotScratch {    // deterministic two-stage reductions (per-block partials + last-block sum)
+    double* partials = nullptr;  // [kMaxWin+2][max grid]
+    unsigned* ticket = nullptr;  // zero-initialised counter, reset by the last block
+};
+
+// ---------------------------------------------------------------- setup launchers (k_setup.cu)
+// Allocation helpers use cudaMallocAsync on `s`.
+template <class T>
+T* dalloc(size_t n, cudaStream_t s) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), s);
+    if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); throw Error(-5, "device out of memory"); }
+    CK(e);
+    return static_cast<T*>(p);
+}
+void dfree(void* p, cudaStream_t s);
+
+// validation of the user CSR (reading A17).  Returns bit flags (0 = valid).
+int validate_input(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s);
+// A_0 = L + diag(d) with inserted missing diagonals; returns a fresh Csr.
+Csr form_A0(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s);
+// lambda_1 = max_i sum_j |a_ij|  (exact: per-row sums in CSR order, max by ordered-int atomicMax)
+double inf_norm(const Csr& A, cudaStream_t s);
+// true if some d_i != 0
+bool any_nonzero(int n, const double* d, cudaStream_t s);
+
+struct PassGraph {     // matching pass graph G_t: CSR with integer multiplicities, no diagonal
+    int n = 0;
+    int64_t nnz = 0;
+    int* rp = nullptr;
+    int* ci = nullptr;
+    uint32_t* w = nullptr;
+};
+PassGraph pass_graph0(const Csr& A, cudaStream_t s);
+void free_graph(PassGraph& g, cudaStream_t s);
+// one aggregation pass: handshake matching + attach + leader numbering.  agg_t[v] in [0, *nc).
+int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* rounds, cudaStream_t s);
+// G_{t+1} = quotient of G_t under agg_t (multiplicities summed, self-loops dropped)
+PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStream_t s);
+// agg[i] = agg_t[agg[i]]
+void compose(int n, int* agg, const int* agg_t, cudaStream_t s);
+// A_H = P^T A P as entry sums in (row, CSR position) order per coarse entry (bit-exact with a
+// sequential left-to-right summation).
+Csr galerkin(const Csr& A, const int* agg, int nc, cudaStream_t s);
+// perm = vertices sorted stably by aggregate, aptr[I] = first position of aggregate I
+void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s);
+// row tiles for the SpMV-class kernels
+Tiles build_tiles(const Csr& A, int grid_per_sm, cudaStream_t s);
+// dense (pseudo-)inverse of the coarsest operator, row-major n x n
+double* coarse_inverse(const Csr& A, bool singular, double shift, cudaStream_t s);
+void free_csr(Csr& A, cudaStream_t s);
+
+// ---------------------------------------------------------------- solve launchers (k_solve.cu)
+// Count of kernels launched through these launchers (for the gpu_launches report).
+extern long long g_launches;
+
+// SpMV-class fused kernels (one pass over A_l):
+//  smooth: out_i = alpha*cg*xg_i + (1-alpha)*prev_i + beta*(f_i - cg*(A xg)_i),
+//          prev_i = xprev ? xprev_i : cp*f_i          (three-term recurrence step)
+void launch_smooth(const Csr& A, const Tiles& T, const double* xg, double cg, const double* f, const double* xprev,
+                   double cp, double alpha, double beta, double* out, cudaStream_t s);
+//  resid: out = f - A xg; optional dot r.r into dots[0]
+void launch_resid(const Csr& A, const Tiles& T, const double* xg, const double* f, double* out, double* dot_rr,
+                  const DotScratch& ds, cudaStream_t s);
+//  spmv with dots: q = A d; *dot_dq = d.q, *dot_dr = d.rho
+void launch_spmv_dots(const Csr& A, const Tiles& T, const double* d, const double* rho, double* q, double* dot_dq,
+                      double* dot_dr, const DotScratch& ds, cudaStream_t s);
+
+// restriction rH[I] = sum_{t in [aptr[I], aptr[I+1])} r[perm[t]]  (sequential per aggregate)
+void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, double* rH, cudaStream_t s);
+// prolongation + axpy: x[i] += eH[agg[i]]
+void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s);
+// dense coarse apply e = M r (M row-major n x n)
+void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_t s);
+// c[j] = z . Q_j for j < w  (Q_j = Q[j], pointers in a device array)
+void launch_multidot(int n, const double* z, const double* const* Q, int w, double* c, const DotScratch& ds,
+                     cudaStream_t s);
+// d = z - sum_{j<w} (c[j]/dq[j]) D_j
+void launch_direction(int n, const double* z, const double* const* D, const double* c, const double* dq, int w,
+                      double* d, cudaStream_t s);
+// FCG update: alpha = dr/dq (alpha = 0 if dq == 0 and inner);  x (+)= alpha d;  r -= alpha q (if r);
+// optional rr = r.r; outer: breakdown flag if !(dq > 0).
+void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
+                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s);
+// v -= mean(v) (two kernels: sum then subtract); tmp = one device double
+void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cudaStream_t s);
+// y = x (device copy kernel)
+void launch_copy(int n, const double* x, double* y, cudaStream_t s);
+// dot = x.y (deterministic)
+void launch_dot(int n, const double* x, const double* y, double* out, const DotScratch& ds, cudaStream_t s);
+// grid size used by the vector kernels
+int vector_grid();
+void init_device_props();
+
+}  // namespace amg

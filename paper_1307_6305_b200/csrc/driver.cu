@@ -1,0 +1,800 @@
+// driver.cu -- host driver and C ABI of libamg_b200.so (include/amg.h).
+//
+// Builds the hierarchy with the setup kernels (k_setup.cu) and runs the solve schedule with the
+// solve kernels (k_solve.cu).  The k-cycle recursion (SURVEY.md
+// 8(c) O6-O8) is a static schedule of kernel launches with all FCG scalars resident on the device,
+// so one outer FCG iteration is captured once per restart-window position as a CUDA graph and
+// replayed; the host only reads ||r||^2 and the breakdown flag once per outer iteration.
+// Host code computes scalars only (the polynomial coefficients of SURVEY App. A, launch
+// configurations); every vector/matrix operation runs in the library's kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/amg.h"
+#include "amg_internal.h"
+
+namespace amg {
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    char buf[512];
+    snprintf(buf, sizeof(buf), "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+    throw Error(e == cudaErrorMemoryAllocation ? AMG_E_OOM : AMG_E_CUDA, buf);
+}
+
+int tiled_grid(int cap, int ntiles);
+
+}  // namespace amg
+
+using namespace amg;
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+// ------------------------------------------------------------------ host scalar math
+// SplitMix64 (docs/keys.md) -- the salt of the matching keys.
+static uint64_t host_sm64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+static double delta_of(double kappa) { return (std::sqrt(kappa) - 1.0) / (std::sqrt(kappa) + 1.0); }
+static double Em_of(int m, double kappa) { return std::pow(delta_of(kappa), m) * (kappa - 1.0) * 0.5; }
+
+// Reading A8 (rule R1): kappa = 10 if E_m(10) < 1, else the kappa with E_m = 1/2:
+// t = sqrt(kappa) solves (t-1)^(m+1) = (t+1)^(m-1) (Newton from t = 3, then stop at a fixed point).
+static double kappa_rule(int m) {
+    if (Em_of(m, 10.0) < 1.0) return 10.0;
+    double t = 3.0;
+    for (int it = 0; it < 200; ++it) {
+        double f = std::pow(t - 1.0, m + 1) - std::pow(t + 1.0, m - 1);
+        double df = (m + 1) * std::pow(t - 1.0, m) - (m - 1) * std::pow(t + 1.0, m - 2);
+        double tn = t - f / df;
+        if (tn == t) break;
+        t = tn;
+    }
+    return t * t;
+}
+
+// Three-term recurrence coefficients: x_{k+1} = a_k x_k + (1-a_k) x_{k-1} + b_k (f - A x_k)
+static void poly_coeffs(double l1, double kappa, int m, double* a, double* b) {
+    const double l0 = l1 / kappa, d = delta_of(kappa), d2 = d * d;
+    for (int k = 0; k <= m; ++k) {
+        if (k == 0) { a[k] = 1.0; b[k] = (l0 + l1) / (2.0 * l0 * l1); }
+        else if (k == 1) { a[k] = 1.0 + 2.0 * d2 * (1.0 - d2) / ((1.0 + d2) * (1.0 + d2)); b[k] = 2.0 / (l0 + l1); }
+        else { a[k] = 1.0 + d2; b[k] = 4.0 * d / (l1 - l0); }
+    }
+}
+
+// ------------------------------------------------------------------ hierarchy
+struct Level {
+    Csr A;
+    Tiles T;
+    double lambda1 = 0, kappa = 0;
+    double alpha[kMaxDeg + 1] = {}, beta[kMaxDeg + 1] = {};
+    int nc = 0;
+    int* agg = nullptr;
+    int* perm = nullptr;
+    int* aptr = nullptr;
+    int rounds[kMaxDeg] = {};
+    // workspaces
+    double *X = nullptr, *XA = nullptr, *RES = nullptr;  // B_l
+    double *RHO = nullptr, *E = nullptr;                  // written / read by the parent level
+    double *Z = nullptr, *D = nullptr, *Q = nullptr;      // inner FCG (nu slots)
+    double* sc = nullptr;                                 // dq[kMaxWin], dr[kMaxWin], c[kMaxWin]
+};
+
+struct amg_hierarchy {
+    cudaStream_t s = nullptr;
+    cudaStream_t user = nullptr;
+    int L = 0, m = 0, p = 0;
+    bool singular = false;
+    amg_options opt{};
+    Level lev[kMaxLevels];
+    double* Minv = nullptr;
+    // outer FCG
+    int n = 0, W = 5;
+    double *b = nullptr, *x = nullptr, *r = nullptr, *Z = nullptr, *D = nullptr, *Q = nullptr;
+    double* osc = nullptr;  // dq[kMaxWin], c[kMaxWin], dr, rr, bb, tmp, rr_true
+    int* flag = nullptr;
+    double* hsc = nullptr;  // pinned host mirror: rr, flag
+    DotScratch ds;
+    int nu_ws = 0;          // nu the inner workspaces are sized for
+    std::vector<cudaGraphExec_t> graphs;
+    int graph_nu = 0;
+    long long graph_launches = 0;
+    std::vector<void*> allocs;
+    std::vector<void*> ws_allocs;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;  // live profile of the level-0 smoother steps
+    bool prof_on = false;
+    int64_t bytes = 0;
+    amg_info info{};
+};
+
+template <class T>
+static T* halloc(amg_hierarchy* h, size_t n, bool ws = false) {
+    T* p = dalloc<T>(n + 8, h->s);  // +8: padding for the 16-byte vector loads
+    (ws ? h->ws_allocs : h->allocs).push_back(p);
+    h->bytes += (int64_t)((n + 8) * sizeof(T));
+    return p;
+}
+
+static bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Stage a caller array on the device (copy if host). Returns device pointer; *tmp set if allocated.
+template <class T>
+static const T* stage_in(const T* p, size_t n, cudaStream_t s, void** tmp) {
+    *tmp = nullptr;
+    if (!p) return nullptr;
+    if (is_device_ptr(p)) return p;
+    T* d = dalloc<T>(n + 8, s);
+    CK(cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    *tmp = d;
+    return d;
+}
+
+static void copy_out(void* dst, const void* src_dev, size_t bytes, cudaStream_t s) {
+    CK(cudaMemcpyAsync(dst, src_dev, bytes, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+}
+
+// event record that is a real event node when the stream is being captured into a graph
+static void record_event(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+        CK(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+    else
+        CK(cudaEventRecord(e, s));
+}
+
+static void destroy_graphs(amg_hierarchy* h) {
+    for (auto g : h->graphs)
+        if (g) cudaGraphExecDestroy(g);
+    h->graphs.clear();
+    h->graph_nu = 0;
+}
+
+static void release(amg_hierarchy* h) {
+    if (!h) return;
+    destroy_graphs(h);
+    if (h->s) {
+        for (int l = 0; l < h->L; ++l) {
+            dfree(h->lev[l].A.rp, h->s);
+            dfree(h->lev[l].A.ci, h->s);
+            dfree(h->lev[l].A.v, h->s);
+            dfree(h->lev[l].T.row, h->s);
+        }
+        for (void* p : h->allocs) dfree(p, h->s);
+        for (void* p : h->ws_allocs) dfree(p, h->s);
+        cudaStreamSynchronize(h->s);
+        cudaStreamDestroy(h->s);
+    }
+    if (h->hsc) cudaFreeHost(h->hsc);
+    if (h->e0) cudaEventDestroy(h->e0);
+    if (h->e1) cudaEventDestroy(h->e1);
+    if (h->pe0) cudaEventDestroy(h->pe0);
+    if (h->pe1) cudaEventDestroy(h->pe1);
+    delete h;
+}
+
+// ------------------------------------------------------------------ setup
+static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int32_t* ci_in, const double* v_in,
+                  const double* d_in) {
+    cudaStream_t s = h->s;
+    if (n64 < 1 || n64 >= (int64_t(1) << 31) - 8) throw Error(AMG_E_ARG, "n out of range");
+    const int n = (int)n64;
+    // row_ptr first (to learn nnz)
+    void* t_rp;
+    const int64_t* rp = stage_in(rp_in, (size_t)n + 1, s, &t_rp);
+    int64_t nnz_in = 0, rp0 = 0;
+    CK(cudaMemcpyAsync(&nnz_in, rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&rp0, rp, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (rp0 != 0 || nnz_in < 0 || nnz_in + n64 >= (int64_t(1) << 31) - 64) {
+        dfree(t_rp, s);
+        throw Error(rp0 != 0 || nnz_in < 0 ? AMG_E_INPUT : AMG_E_ARG, "row_ptr[0] != 0 or nnz out of range");
+    }
+    void *t_ci, *t_v, *t_d;
+    const int32_t* ci = stage_in(ci_in, (size_t)nnz_in, s, &t_ci);
+    const double* v = stage_in(v_in, (size_t)nnz_in, s, &t_v);
+    const double* d = stage_in(d_in, (size_t)n, s, &t_d);
+    int vf = validate_input(n, rp, ci, v, d, s);
+    if (vf) {
+        dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
+        char buf[128];
+        snprintf(buf, sizeof(buf), "invalid CSR input (flags 0x%x: 1 range, 2 unsorted, 4 positive off-diagonal, "
+                 "8 asymmetric, 16 diagonal, 32 d<0, 64 row_ptr)", vf);
+        throw Error(AMG_E_INPUT, buf);
+    }
+    h->singular = !(d && any_nonzero(n, d, s));
+    h->lev[0].A = form_A0(n, rp, ci, v, d, s);
+    dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
+    h->n = n;
+
+    const int m = h->m, p = h->p;
+    int l = 0;
+    for (;;) {
+        Level& Lv = h->lev[l];
+        Lv.lambda1 = inf_norm(Lv.A, s);
+        Lv.kappa = h->opt.kappa > 1.0 ? h->opt.kappa : kappa_rule(m);
+        poly_coeffs(Lv.lambda1, Lv.kappa, m, Lv.alpha, Lv.beta);
+        if (Lv.A.n <= h->opt.coarsest_size) break;
+        if (l + 1 >= kMaxLevels) throw Error(AMG_E_SETUP, "too many levels");
+        PassGraph G = pass_graph0(Lv.A, s);
+        int* agg = nullptr;
+        int nc = Lv.A.n;
+        for (int t = 0; t < p; ++t) {
+            const uint64_t salt = host_sm64(h->opt.seed ^ (((uint64_t)l << 8) ^ (uint64_t)t));
+            int* agg_t = dalloc<int>((size_t)G.n + 8, s);
+            int nct = 0;
+            aggregate_pass(G, salt, agg_t, &nct, &Lv.rounds[t], s);
+            if (t + 1 < p) {
+                PassGraph G2 = quotient_graph(G, agg_t, nct, s);
+                free_graph(G, s);
+                G = G2;
+            }
+            if (t == 0) {
+                agg = agg_t;
+            } else {
+                compose(Lv.A.n, agg, agg_t, s);
+                dfree(agg_t, s);
+            }
+            nc = nct;
+        }
+        free_graph(G, s);
+        if (nc >= Lv.A.n) {
+            dfree(agg, s);
+            throw Error(AMG_E_SETUP, "coarsening stagnated (n_{l+1} = n_l)");
+        }
+        Lv.nc = nc;
+        Lv.agg = agg;
+        h->allocs.push_back(agg);
+        Lv.perm = halloc<int>(h, Lv.A.n);
+        Lv.aptr = halloc<int>(h, (size_t)nc + 1);
+        aggregate_order(Lv.A.n, agg, nc, Lv.perm, Lv.aptr, s);
+        h->lev[l + 1].A = galerkin(Lv.A, agg, nc, s);
+        ++l;
+    }
+    h->L = l + 1;
+    // coarsest (a7)
+    Level& C = h->lev[h->L - 1];
+    const double shift = C.lambda1 > 0.0 ? C.lambda1 : 1.0;
+    h->Minv = coarse_inverse(C.A, h->singular, shift, s);
+    h->allocs.push_back(h->Minv);
+    // tiles of every level the SpMV-class kernels run on (all but the coarsest; level 0 always)
+    for (int k = 0; k < h->L; ++k)
+        if (k < h->L - 1 || k == 0) h->lev[k].T = build_tiles(h->lev[k].A, 0, s);
+    // level workspaces
+    for (int k = 0; k < h->L; ++k) {
+        Level& Lv = h->lev[k];
+        const size_t nk = Lv.A.n;
+        if (k < h->L - 1) {
+            Lv.X = halloc<double>(h, nk);
+            Lv.XA = halloc<double>(h, nk);
+            Lv.RES = halloc<double>(h, nk);
+        }
+        if (k >= 1) {
+            Lv.RHO = halloc<double>(h, nk);
+            Lv.E = halloc<double>(h, nk);
+        }
+        Lv.sc = halloc<double>(h, 3 * kMaxWin);
+    }
+    // outer FCG
+    h->W = h->opt.restart;
+    h->b = halloc<double>(h, n);
+    h->x = halloc<double>(h, n);
+    h->r = halloc<double>(h, n);
+    h->Z = halloc<double>(h, n);
+    h->D = halloc<double>(h, (size_t)n * h->W);
+    h->Q = halloc<double>(h, (size_t)n * h->W);
+    h->osc = halloc<double>(h, 2 * kMaxWin + 8);
+    h->flag = halloc<int>(h, 4);
+    h->ds.partials = halloc<double>(h, (size_t)(kMaxWin + 2) * 4096);
+    h->ds.ticket = halloc<unsigned>(h, 4);
+    CK(cudaMemsetAsync(h->ds.ticket, 0, 4 * sizeof(unsigned), s));
+    CK(cudaMallocHost(&h->hsc, 8 * sizeof(double)));
+    CK(cudaStreamSynchronize(s));
+}
+
+static void ensure_inner_ws(amg_hierarchy* h, int nu) {
+    if (nu <= h->nu_ws) return;
+    for (void* p : h->ws_allocs) dfree(p, h->s);
+    h->ws_allocs.clear();
+    for (int k = 1; k < h->L - 1; ++k) {
+        Level& Lv = h->lev[k];
+        const size_t nk = Lv.A.n;
+        Lv.Z = halloc<double>(h, nk, true);
+        Lv.D = halloc<double>(h, nk * nu, true);
+        Lv.Q = halloc<double>(h, nk * nu, true);
+    }
+    h->nu_ws = nu;
+    destroy_graphs(h);
+}
+
+// ------------------------------------------------------------------ solve schedule
+static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* out);
+
+// FCG_inner(l, RHO_l, nu) -> E_l
+static void fcg_inner(amg_hierarchy* h, int l, int nu) {
+    Level& Lv = h->lev[l];
+    cudaStream_t s = h->s;
+    const int n = Lv.A.n;
+    double* rho = Lv.RHO;
+    double* dq = Lv.sc;
+    double* dr = Lv.sc + kMaxWin;
+    double* c = Lv.sc + 2 * kMaxWin;
+    const double* Dp[kMaxWin];
+    const double* Qp[kMaxWin];
+    for (int i = 0; i < nu; ++i) {
+        double* Di = Lv.D + (size_t)i * n;
+        double* Qi = Lv.Q + (size_t)i * n;
+        Dp[i] = Di;
+        Qp[i] = Qi;
+        if (i == 0) {
+            apply_B(h, l, nu, rho, Di);
+        } else {
+            apply_B(h, l, nu, rho, Lv.Z);
+            launch_multidot(n, Lv.Z, Qp, i, c, h->ds, s);
+            launch_direction(n, Lv.Z, Dp, c, dq, i, Di, s);
+        }
+        launch_spmv_dots(Lv.A, Lv.T, Di, rho, Qi, dq + i, dr + i, h->ds, s);  // q = A d, d.q, d.rho
+        launch_fcg_update(n, dr + i, dq + i, Di, Qi, Lv.E, i == 0, (i < nu - 1) ? rho : nullptr, nullptr, nullptr,
+                          h->ds, s);
+    }
+}
+
+// z = B_l(r): pre-smoothing from 0, residual, restriction, coarse correction,
+// prolongation, post-smoothing; the last smoothing step writes `out` (distinct from rin and the
+// level buffers).
+static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* out) {
+    cudaStream_t s = h->s;
+    if (l == h->L - 1) {
+        launch_gemv(h->lev[l].A.n, h->Minv, rin, out, s);
+        return;
+    }
+    Level& Lv = h->lev[l];
+    const int m = h->m;
+    const double* a = Lv.alpha;
+    const double* b = Lv.beta;
+    // pre-smoothing S(r, 0): step 0 is free (x_1 = b0 r implicit)
+    double* cur = Lv.X;
+    double* prev = Lv.XA;
+    launch_smooth(Lv.A, Lv.T, rin, b[0], rin, nullptr, 0.0, a[1], b[1], Lv.X, s);  // k = 1 (x_0 = 0)
+    if (m >= 2) {
+        launch_smooth(Lv.A, Lv.T, Lv.X, 1.0, rin, nullptr, b[0], a[2], b[2], Lv.XA, s);  // k = 2 (x_1 = b0 r)
+        cur = Lv.XA;
+        prev = Lv.X;
+        for (int k = 3; k <= m; ++k) {
+            launch_smooth(Lv.A, Lv.T, cur, 1.0, rin, prev, 0.0, a[k], b[k], prev, s);
+            std::swap(cur, prev);
+        }
+    }
+    // residual + restriction
+    launch_resid(Lv.A, Lv.T, cur, rin, Lv.RES, nullptr, h->ds, s);
+    Level& C = h->lev[l + 1];
+    launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO, s);
+    // coarse correction (A12: exact solve when the next level is the coarsest)
+    if (l + 1 == h->L - 1)
+        launch_gemv(C.A.n, h->Minv, C.RHO, C.E, s);
+    else
+        fcg_inner(h, l + 1, nu);
+    launch_prolong(Lv.A.n, Lv.agg, C.E, cur, s);
+    // post-smoothing S(r, x): x_{-1} = x_0 = cur
+    double* other = (cur == Lv.X) ? Lv.XA : Lv.X;
+    launch_smooth(Lv.A, Lv.T, cur, 1.0, rin, cur, 0.0, 1.0, b[0], other, s);  // k = 0
+    prev = cur;
+    cur = other;
+    const bool prof = (l == 0 && h->prof_on);
+    if (prof) record_event(h->pe0, s);
+    for (int k = 1; k <= m; ++k) {
+        double* target = (k == m) ? out : prev;
+        launch_smooth(Lv.A, Lv.T, cur, 1.0, rin, prev, 0.0, a[k], b[k], target, s);
+        prev = cur;
+        cur = target;
+    }
+    if (prof) record_event(h->pe1, s);
+}
+
+// one outer FCG iteration at window position p
+static void outer_iteration(amg_hierarchy* h, int pos, int nu) {
+    cudaStream_t s = h->s;
+    const int n = h->n;
+    double* dq = h->osc;
+    double* c = h->osc + kMaxWin;
+    double* dr = h->osc + 2 * kMaxWin;
+    double* rr = h->osc + 2 * kMaxWin + 1;
+    double* Dp = h->D + (size_t)pos * n;
+    double* Qp = h->Q + (size_t)pos * n;
+    double* zdst = (pos == 0) ? Dp : h->Z;
+    h->prof_on = true;
+    apply_B(h, 0, nu, h->r, zdst);
+    h->prof_on = false;
+    if (h->singular) launch_mean_project(n, zdst, h->osc + 2 * kMaxWin + 3, h->ds, s);
+    if (pos > 0) {
+        const double* Ds[kMaxWin];
+        const double* Qs[kMaxWin];
+        for (int j = 0; j < pos; ++j) {
+            Ds[j] = h->D + (size_t)j * n;
+            Qs[j] = h->Q + (size_t)j * n;
+        }
+        launch_multidot(n, h->Z, Qs, pos, c, h->ds, s);
+        launch_direction(n, h->Z, Ds, c, dq, pos, Dp, s);
+    }
+    launch_spmv_dots(h->lev[0].A, h->lev[0].T, Dp, h->r, Qp, dq + pos, dr, h->ds, s);
+    launch_fcg_update(n, dr, dq + pos, Dp, Qp, h->x, false, h->r, rr, h->flag, h->ds, s);
+}
+
+static void capture_graphs(amg_hierarchy* h, int nu) {
+    destroy_graphs(h);
+    h->graphs.resize(h->W, nullptr);
+    for (int pos = 0; pos < h->W; ++pos) {
+        cudaGraph_t g;
+        long long before = g_launches;
+        CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+        try {
+            outer_iteration(h, pos, nu);
+        } catch (...) {
+            cudaStreamEndCapture(h->s, &g);
+            throw;
+        }
+        CK(cudaStreamEndCapture(h->s, &g));
+        h->graph_launches = g_launches - before;
+        g_launches = before;
+        CK(cudaGraphInstantiate(&h->graphs[pos], g, 0));
+        CK(cudaGraphDestroy(g));
+    }
+    h->graph_nu = nu;
+}
+
+static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol, int nu, int* iters_out,
+                 double* relres_out) {
+    cudaStream_t s = h->s;
+    const int n = h->n;
+    if (h->user) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, h->user));
+        CK(cudaStreamWaitEvent(s, ev, 0));
+        CK(cudaEventDestroy(ev));
+    }
+    ensure_inner_ws(h, nu);
+    if (h->opt.use_graphs && h->graph_nu != nu) capture_graphs(h, nu);
+    long long launches0 = g_launches;
+    CK(cudaEventRecord(h->e0, s));
+    // inputs
+    CK(cudaMemcpyAsync(h->b, b_in, sizeof(double) * n, is_device_ptr(b_in) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h->x, x_out, sizeof(double) * n, is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    double* bb = h->osc + 2 * kMaxWin + 2;
+    double* rr = h->osc + 2 * kMaxWin + 1;
+    if (h->singular) launch_mean_project(n, h->b, h->osc + 2 * kMaxWin + 3, h->ds, s);  // S:449, A16
+    launch_dot(n, h->b, h->b, bb, h->ds, s);
+    launch_resid(h->lev[0].A, h->lev[0].T, h->x, h->b, h->r, rr, h->ds, s);
+    CK(cudaMemsetAsync(h->flag, 0, sizeof(int), s));
+    CK(cudaMemcpyAsync(h->hsc, rr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double bnorm = std::sqrt(h->hsc[1]);
+    double rnorm = std::sqrt(h->hsc[0]);
+    int status = AMG_NOT_CONVERGED, k = 0;
+    long long graph_runs = 0;
+    double prof_ms = 0.0;
+    int64_t prof_n = 0;
+    if (bnorm == 0.0) {
+        CK(cudaMemsetAsync(h->x, 0, sizeof(double) * n, s));
+        status = AMG_OK;
+        rnorm = 0.0;
+    } else {
+        int pos = 0;
+        for (k = 0;; ++k) {
+            if (rnorm <= tol * bnorm) { status = AMG_OK; break; }
+            if (k >= h->opt.max_iter) break;
+            if (h->opt.use_graphs) {
+                CK(cudaGraphLaunch(h->graphs[pos], s));
+                ++graph_runs;
+            } else {
+                outer_iteration(h, pos, nu);
+            }
+            CK(cudaMemcpyAsync(h->hsc, rr, sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(h->hsc + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            int fl;
+            memcpy(&fl, h->hsc + 2, sizeof(int));
+            if (h->L > 1) {
+                float pm = 0.f;
+                CK(cudaEventElapsedTime(&pm, h->pe0, h->pe1));
+                prof_ms += pm;
+                prof_n += h->m;
+            }
+            if (fl) { status = AMG_E_BREAKDOWN; ++k; break; }
+            rnorm = std::sqrt(h->hsc[0]);
+            pos = (pos + 1) % h->W;
+        }
+    }
+    // true residual ||b - A x|| (reported) and the solution back to the caller
+    double* rt = h->osc + 2 * kMaxWin + 6;
+    launch_resid(h->lev[0].A, h->lev[0].T, h->x, h->b, h->Z, rt, h->ds, s);
+    copy_out(x_out, h->x, sizeof(double) * n, s);
+    CK(cudaEventRecord(h->e1, s));
+    CK(cudaMemcpyAsync(h->hsc + 3, rt, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->e0, h->e1));
+    h->info.solve_ms = ms;
+    h->info.last_iters = k;
+    h->info.last_relres = bnorm > 0 ? rnorm / bnorm : 0.0;
+    h->info.last_true_relres = bnorm > 0 ? std::sqrt(h->hsc[3]) / bnorm : 0.0;
+    h->info.launches_last_solve = (g_launches - launches0) + graph_runs * h->graph_launches;
+    h->info.launches_per_iter = h->graph_launches;
+    h->info.prof_smoother_ms = prof_ms;
+    h->info.prof_smoother_launches = prof_n;
+    h->info.prof_smoother_bytes = 12 * h->lev[0].A.nnz + 36 * (int64_t)h->lev[0].A.n;
+    if (h->user) {  // order the caller's stream after this call's work
+        CK(cudaEventRecord(h->e1, s));
+        CK(cudaStreamWaitEvent(h->user, h->e1, 0));
+    }
+    if (iters_out) *iters_out = k;
+    if (relres_out) *relres_out = h->info.last_relres;
+    if (status == AMG_E_BREAKDOWN) g_last_error = "FCG breakdown: d.q <= 0 or not finite";
+    return status;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int amg_options_default(amg_options* o) {
+    if (!o) return fail(AMG_E_ARG, "amg_options_default: NULL");
+    memset(o, 0, sizeof(*o));
+    o->coarsest_size = 100;
+    o->kappa = 0.0;
+    o->restart = 5;
+    o->max_iter = 500;
+    o->seed = 0;
+    o->stream = nullptr;
+    o->use_graphs = 1;
+    return AMG_OK;
+}
+
+const char* amg_last_error(void) { return g_last_error.c_str(); }
+
+int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+              const double* d, int32_t n_match_passes, int32_t poly_degree, const amg_options* opt) {
+    if (!out) return fail(AMG_E_ARG, "amg_setup: out is NULL");
+    *out = nullptr;
+    if (!row_ptr || !val || !col) return fail(AMG_E_ARG, "amg_setup: NULL array");
+    if (n_match_passes < 1 || n_match_passes > kMaxDeg) return fail(AMG_E_ARG, "amg_setup: n_match_passes out of range");
+    if (poly_degree < 1 || poly_degree > kMaxDeg) return fail(AMG_E_ARG, "amg_setup: poly_degree out of range");
+    amg_options o;
+    amg_options_default(&o);
+    if (opt) o = *opt;
+    if (o.coarsest_size < 1 || o.restart < 1 || o.restart > kMaxWin || o.max_iter < 0)
+        return fail(AMG_E_ARG, "amg_setup: bad options");
+    if (o.kappa != 0.0 && !(o.kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: kappa must be 0 or > 1");
+    if (o.kappa > 1.0 && !(Em_of(poly_degree, o.kappa) < 1.0))
+        return fail(AMG_E_ARG, "amg_setup: E_m(kappa) >= 1: the smoother would not converge (reading A9)");
+    amg_hierarchy* h = new amg_hierarchy();
+    try {
+        init_device_props();
+        h->opt = o;
+        h->m = poly_degree;
+        h->p = n_match_passes;
+        h->user = (cudaStream_t)o.stream;
+        CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&h->e0));
+        CK(cudaEventCreate(&h->e1));
+        CK(cudaEventCreate(&h->pe0));
+        CK(cudaEventCreate(&h->pe1));
+        if (h->user) {
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, h->user));
+            CK(cudaStreamWaitEvent(h->s, ev, 0));
+            CK(cudaEventDestroy(ev));
+        }
+        CK(cudaEventRecord(h->e0, h->s));
+        long long l0 = g_launches;
+        build(h, n, row_ptr, col, val, d);
+        h->info.launches_last_setup = g_launches - l0;
+        CK(cudaEventRecord(h->e1, h->s));
+        CK(cudaEventSynchronize(h->e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->e0, h->e1));
+        h->info.setup_ms = ms;
+        if (h->user) CK(cudaStreamWaitEvent(h->user, h->e1, 0));
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        cudaGetLastError();
+        release(h);
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        release(h);
+        return AMG_E_CUDA;
+    }
+    *out = h;
+    return AMG_OK;
+}
+
+int amg_solve(amg_handle h, const double* b, double* x, double tol, int32_t k_inner, int32_t* iters, double* relres) {
+    if (!h || !b || !x) return fail(AMG_E_ARG, "amg_solve: NULL argument");
+    if (!(tol > 0.0) || k_inner < 1 || k_inner > kMaxWin) return fail(AMG_E_ARG, "amg_solve: bad tol or k_inner");
+    try {
+        int it = 0;
+        int st = solve(h, b, x, tol, k_inner, &it, relres);
+        if (iters) *iters = it;
+        return st;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        cudaGetLastError();
+        return e.code;
+    }
+}
+
+int amg_free(amg_handle h) {
+    if (!h) return AMG_OK;
+    release(h);
+    return AMG_OK;
+}
+
+int amg_get_info(amg_handle h, amg_info* info) {
+    if (!h || !info) return fail(AMG_E_ARG, "amg_get_info: NULL argument");
+    amg_info r = h->info;
+    r.levels = h->L;
+    r.poly_degree = h->m;
+    r.n_match_passes = h->p;
+    r.singular = h->singular;
+    double sn = 0, snz = 0;
+    for (int l = 0; l < h->L; ++l) {
+        sn += h->lev[l].A.n;
+        snz += (double)h->lev[l].A.nnz;
+        if (l < 32) {
+            r.n[l] = h->lev[l].A.n;
+            r.nnz[l] = h->lev[l].A.nnz;
+            r.lambda1[l] = h->lev[l].lambda1;
+            r.kappa[l] = h->lev[l].kappa;
+        }
+    }
+    r.grid_complexity = sn / h->lev[0].A.n;
+    r.operator_complexity = snz / (double)h->lev[0].A.nnz;
+    r.device_bytes = h->bytes;
+    *info = r;
+    return AMG_OK;
+}
+
+// ---- parity hooks ----
+int amg_level_sizes(amg_handle h, int32_t level, int64_t* n, int64_t* nnz, int64_t* nc, double* lambda1,
+                    double* kappa, double* alpha, double* beta) {
+    if (!h || level < 0 || level >= h->L) return fail(AMG_E_ARG, "amg_level_sizes: bad level");
+    const Level& Lv = h->lev[level];
+    if (n) *n = Lv.A.n;
+    if (nnz) *nnz = Lv.A.nnz;
+    if (nc) *nc = (level < h->L - 1) ? Lv.nc : 0;
+    if (lambda1) *lambda1 = Lv.lambda1;
+    if (kappa) *kappa = Lv.kappa;
+    if (alpha) memcpy(alpha, Lv.alpha, sizeof(double) * (h->m + 1));
+    if (beta) memcpy(beta, Lv.beta, sizeof(double) * (h->m + 1));
+    return AMG_OK;
+}
+
+int amg_level_export(amg_handle h, int32_t level, int64_t* row_ptr, int32_t* col, double* val, int32_t* agg) {
+    if (!h || level < 0 || level >= h->L) return fail(AMG_E_ARG, "amg_level_export: bad level");
+    try {
+        const Level& Lv = h->lev[level];
+        cudaStream_t s = h->s;
+        if (row_ptr) {
+            std::vector<int> tmp((size_t)Lv.A.n + 1);
+            CK(cudaMemcpyAsync(tmp.data(), Lv.A.rp, sizeof(int) * tmp.size(), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::vector<int64_t> w(tmp.begin(), tmp.end());
+            CK(cudaMemcpy(row_ptr, w.data(), sizeof(int64_t) * w.size(),
+                          is_device_ptr(row_ptr) ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
+        }
+        if (col) copy_out(col, Lv.A.ci, sizeof(int) * Lv.A.nnz, s);
+        if (val) copy_out(val, Lv.A.v, sizeof(double) * Lv.A.nnz, s);
+        if (agg && level < h->L - 1) copy_out(agg, Lv.agg, sizeof(int) * Lv.A.n, s);
+        CK(cudaStreamSynchronize(s));
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    }
+    return AMG_OK;
+}
+
+int amg_level_smooth(amg_handle h, int32_t level, const double* f, const double* x0, double* x) {
+    if (!h || level < 0 || level >= h->L - 1 || !f || !x0 || !x) return fail(AMG_E_ARG, "amg_level_smooth: bad args");
+    try {
+        Level& Lv = h->lev[level];
+        cudaStream_t s = h->s;
+        const int n = Lv.A.n;
+        double* F = dalloc<double>((size_t)n + 8, s);
+        double* O = dalloc<double>((size_t)n + 8, s);
+        CK(cudaMemcpyAsync(F, f, sizeof(double) * n, cudaMemcpyDefault, s));
+        CK(cudaMemcpyAsync(Lv.X, x0, sizeof(double) * n, cudaMemcpyDefault, s));
+        // S(f, x0): x_{-1} = x_0
+        double* cur = Lv.X;
+        double* other = Lv.XA;
+        launch_smooth(Lv.A, Lv.T, cur, 1.0, F, cur, 0.0, 1.0, Lv.beta[0], other, s);
+        double* prev = cur;
+        cur = other;
+        for (int k = 1; k <= h->m; ++k) {
+            double* target = (k == h->m) ? O : prev;
+            launch_smooth(Lv.A, Lv.T, cur, 1.0, F, prev, 0.0, Lv.alpha[k], Lv.beta[k], target, s);
+            prev = cur;
+            cur = target;
+        }
+        copy_out(x, cur, sizeof(double) * n, s);
+        CK(cudaStreamSynchronize(s));
+        dfree(F, s);
+        dfree(O, s);
+        CK(cudaStreamSynchronize(s));
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    }
+    return AMG_OK;
+}
+
+int amg_level_precond(amg_handle h, int32_t level, int32_t k_inner, const double* r, double* z) {
+    if (!h || level < 0 || level >= h->L || !r || !z || k_inner < 1 || k_inner > kMaxWin)
+        return fail(AMG_E_ARG, "amg_level_precond: bad args");
+    try {
+        cudaStream_t s = h->s;
+        ensure_inner_ws(h, k_inner);
+        const int n = h->lev[level].A.n;
+        double* R = dalloc<double>((size_t)n + 8, s);
+        double* O = dalloc<double>((size_t)n + 8, s);
+        CK(cudaMemcpyAsync(R, r, sizeof(double) * n, cudaMemcpyDefault, s));
+        apply_B(h, level, k_inner, R, O);
+        copy_out(z, O, sizeof(double) * n, s);
+        CK(cudaStreamSynchronize(s));
+        dfree(R, s);
+        dfree(O, s);
+        CK(cudaStreamSynchronize(s));
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    }
+    return AMG_OK;
+}
+
+int amg_coarse_solve(amg_handle h, const double* r, double* e) {
+    if (!h || !r || !e) return fail(AMG_E_ARG, "amg_coarse_solve: bad args");
+    try {
+        cudaStream_t s = h->s;
+        const int n = h->lev[h->L - 1].A.n;
+        double* R = dalloc<double>((size_t)n + 8, s);
+        double* O = dalloc<double>((size_t)n + 8, s);
+        CK(cudaMemcpyAsync(R, r, sizeof(double) * n, cudaMemcpyDefault, s));
+        launch_gemv(n, h->Minv, R, O, s);
+        copy_out(e, O, sizeof(double) * n, s);
+        CK(cudaStreamSynchronize(s));
+        dfree(R, s);
+        dfree(O, s);
+    } catch (const Error& e2) {
+        g_last_error = e2.what();
+        return e2.code;
+    }
+    return AMG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,680 @@
+// k_setup.cu -- setup-phase kernels of libamg_b200.so (sm_100a): SURVEY.md 8(a) rows a1-a8.
+//
+//  * lambda_1 = ||A||_inf: per-row |a| sums in CSR order, max by an
+//    ordered-integer atomicMax (exact, order independent).
+//  * Aggregation by repeated pairwise matching (l.62-73; readings A1-A5 in DESIGN.md): the
+//    integer-keyed handshake (propose / accept rounds) -- equal to the sequential edge-greedy
+//    matching for the strict key order of docs/keys.md -- then attach, leader numbering by an
+//    exclusive scan, and the quotient pass graph (l.88-95) by radix sort + segmented sums.
+//  * Galerkin A_H = P^T A P (l.112, "simple summations", l.401-402): keys (agg(i), agg(j)) for
+//    every stored entry, stable radix sort of the entry indices, then one sequential sum per
+//    coarse entry in (row, CSR position) order.
+//  * Dense coarsest (pseudo-)inverse by Gauss-Jordan steps (SPD, no pivoting).
+// CUB (header-only, CUDA 12.9) supplies the radix sorts and scans.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <vector>
+
+#include "amg_internal.h"
+
+namespace amg {
+
+void dfree(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+static int grid_for(int64_t n) {
+    int64_t g = (n + kBlock - 1) / kBlock;
+    if (g < 1) g = 1;
+    if (g > 65535 * 8) g = 65535 * 8;
+    return (int)g;
+}
+
+template <class T>
+static T read_scalar(const T* dptr, cudaStream_t s) {
+    T h;
+    CK(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return h;
+}
+
+static int bits_for(int64_t x) {  // smallest b >= 1 with 2^b >= x
+    int b = 1;
+    while ((int64_t(1) << b) < x) ++b;
+    return b;
+}
+
+// exclusive scan of int32 flags/counts into out (n+1 entries: out[n] = total); returns total
+static int64_t exclusive_scan_total(const int* in, int* out, int n, cudaStream_t s) {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n + 1, s));
+    void* tmp = dalloc<char>(tb, s);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, n + 1, s));
+    dfree(tmp, s);
+    int total = read_scalar(out + n, s);
+    return total;
+}
+
+template <class K, class V>
+static void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, int n, int end_bit, cudaStream_t s) {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, end_bit, s));
+    void* tmp = dalloc<char>(tb, s);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, n, 0, end_bit, s));
+    dfree(tmp, s);
+}
+
+void free_csr(Csr& A, cudaStream_t s) {
+    dfree(A.rp, s);
+    dfree(A.ci, s);
+    dfree(A.v, s);
+    A = Csr{};
+}
+
+void free_graph(PassGraph& g, cudaStream_t s) {
+    dfree(g.rp, s);
+    dfree(g.ci, s);
+    dfree(g.w, s);
+    g = PassGraph{};
+}
+
+// ------------------------------------------------------------------ validation (A17)
+enum : int {
+    VF_RANGE = 1, VF_UNSORTED = 2, VF_POSOFF = 4, VF_ASYM = 8, VF_DIAG = 16, VF_D = 32, VF_RP = 64
+};
+
+__global__ void k_validate(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const double* __restrict__ v, const double* __restrict__ d, int* flags) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int f = 0;
+        const int64_t p0 = rp[i], p1 = rp[i + 1];
+        if (p1 < p0 || (i == 0 && p0 != 0)) { atomicOr(flags, VF_RP); continue; }
+        double off = 0.0, dv = 0.0;
+        bool has = false;
+        for (int64_t p = p0; p < p1; ++p) {
+            const int c = ci[p];
+            if (c < 0 || c >= n) { f |= VF_RANGE; continue; }
+            if (p > p0 && c <= ci[p - 1]) f |= VF_UNSORTED;
+            if (c == i) { has = true; dv = v[p]; continue; }
+            if (!(v[p] < 0.0)) f |= VF_POSOFF;
+            off += -v[p];
+            int64_t lo = rp[c], hi = rp[c + 1];
+            while (lo < hi) {
+                int64_t mid = (lo + hi) >> 1;
+                if (ci[mid] < i) lo = mid + 1; else hi = mid;
+            }
+            if (!(lo < rp[c + 1] && ci[lo] == i && v[lo] == v[p])) f |= VF_ASYM;
+        }
+        if (has && fabs(dv - off) > 1e-10 * (fabs(dv) + off)) f |= VF_DIAG;
+        if (d && !(d[i] >= 0.0)) f |= VF_D;
+        if (f) atomicOr(flags, f);
+    }
+}
+
+int validate_input(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s) {
+    int* fl = dalloc<int>(1, s);
+    CK(cudaMemsetAsync(fl, 0, sizeof(int), s));
+    k_validate<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, v, d, fl);
+    ++g_launches;
+    CK(cudaGetLastError());
+    int f = read_scalar(fl, s);
+    dfree(fl, s);
+    return f;
+}
+
+// ------------------------------------------------------------------ A_0 = L + diag(d) (Eq. (prob))
+__global__ void k_a0_count(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int* cnt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        bool has = false;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) has |= (ci[p] == i);
+        cnt[i] = (int)(rp[i + 1] - rp[i]) + (has ? 0 : 1);
+    }
+}
+
+__global__ void k_a0_fill(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const double* __restrict__ d, const int* __restrict__ orp,
+                          int* __restrict__ oci, double* __restrict__ ov) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        bool has = false;
+        double off = 0.0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            has |= (ci[p] == i);
+            if (ci[p] != i) off += -v[p];
+        }
+        const double di = d ? d[i] : 0.0;
+        int q = orp[i];
+        bool done = has;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            if (!done && ci[p] > i) { oci[q] = i; ov[q] = off + di; ++q; done = true; }
+            oci[q] = ci[p];
+            ov[q] = (ci[p] == i) ? v[p] + di : v[p];
+            ++q;
+        }
+        if (!done) { oci[q] = i; ov[q] = off + di; }
+    }
+}
+
+Csr form_A0(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s) {
+    int* cnt = dalloc<int>((size_t)n + 1, s);
+    CK(cudaMemsetAsync(cnt + n, 0, sizeof(int), s));
+    k_a0_count<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, cnt);
+    ++g_launches;
+    CK(cudaGetLastError());
+    Csr A;
+    A.n = n;
+    A.rp = dalloc<int>((size_t)n + 1, s);
+    // nnz must fit int32 (checked by the caller on the input nnz + n)
+    A.nnz = exclusive_scan_total(cnt, A.rp, n, s);
+    dfree(cnt, s);
+    A.ci = dalloc<int>((size_t)A.nnz + 8, s);
+    A.v = dalloc<double>((size_t)A.nnz + 8, s);
+    CK(cudaMemsetAsync(A.ci + A.nnz, 0, 8 * sizeof(int), s));
+    CK(cudaMemsetAsync(A.v + A.nnz, 0, 8 * sizeof(double), s));
+    k_a0_fill<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, v, d, A.rp, A.ci, A.v);
+    ++g_launches;
+    CK(cudaGetLastError());
+    return A;
+}
+
+__global__ void k_any_nonzero(int n, const double* __restrict__ d, int* flag) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (d[i] != 0.0) *flag = 1;
+}
+
+bool any_nonzero(int n, const double* d, cudaStream_t s) {
+    int* fl = dalloc<int>(1, s);
+    CK(cudaMemsetAsync(fl, 0, sizeof(int), s));
+    k_any_nonzero<<<grid_for(n), kBlock, 0, s>>>(n, d, fl);
+    ++g_launches;
+    CK(cudaGetLastError());
+    int f = read_scalar(fl, s);
+    dfree(fl, s);
+    return f != 0;
+}
+
+// ------------------------------------------------------------------ lambda_1 (a1)
+__global__ void k_rowabs_max(int n, const int* __restrict__ rp, const double* __restrict__ v,
+                             unsigned long long* out) {
+    double m = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) s += fabs(v[p]);
+        m = fmax(m, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+double inf_norm(const Csr& A, cudaStream_t s) {
+    unsigned long long* o = dalloc<unsigned long long>(1, s);
+    CK(cudaMemsetAsync(o, 0, sizeof(unsigned long long), s));
+    k_rowabs_max<<<grid_for(A.n), kBlock, 0, s>>>(A.n, A.rp, A.v, o);
+    ++g_launches;
+    CK(cudaGetLastError());
+    unsigned long long h = read_scalar(o, s);
+    dfree(o, s);
+    double r;
+    memcpy(&r, &h, sizeof(double));
+    return r;
+}
+
+// ------------------------------------------------------------------ pass graph G_0 (A5)
+__global__ void k_g0_count(int n, const int* __restrict__ rp, const int* __restrict__ ci, int* cnt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int c = 0;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) c += (ci[p] != i);
+        cnt[i] = c;
+    }
+}
+
+__global__ void k_g0_fill(int n, const int* __restrict__ rp, const int* __restrict__ ci, const int* __restrict__ grp,
+                          int* __restrict__ gci, uint32_t* __restrict__ gw) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int q = grp[i];
+        for (int p = rp[i]; p < rp[i + 1]; ++p)
+            if (ci[p] != i) { gci[q] = ci[p]; gw[q] = 1u; ++q; }
+    }
+}
+
+PassGraph pass_graph0(const Csr& A, cudaStream_t s) {
+    PassGraph G;
+    G.n = A.n;
+    int* cnt = dalloc<int>((size_t)A.n + 1, s);
+    CK(cudaMemsetAsync(cnt + A.n, 0, sizeof(int), s));
+    k_g0_count<<<grid_for(A.n), kBlock, 0, s>>>(A.n, A.rp, A.ci, cnt);
+    ++g_launches;
+    CK(cudaGetLastError());
+    G.rp = dalloc<int>((size_t)A.n + 1, s);
+    G.nnz = exclusive_scan_total(cnt, G.rp, A.n, s);
+    dfree(cnt, s);
+    G.ci = dalloc<int>((size_t)G.nnz, s);
+    G.w = dalloc<uint32_t>((size_t)G.nnz, s);
+    k_g0_fill<<<grid_for(A.n), kBlock, 0, s>>>(A.n, A.rp, A.ci, G.rp, G.ci, G.w);
+    ++g_launches;
+    CK(cudaGetLastError());
+    return G;
+}
+
+// ------------------------------------------------------------------ matching keys (docs/keys.md)
+__device__ __forceinline__ uint64_t sm64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+struct EKey {
+    uint32_t w;
+    uint64_t h;
+    int lo, hi;
+};
+
+__device__ __forceinline__ EKey make_key(uint32_t w, int a, int b, uint64_t salt) {
+    EKey k;
+    k.w = w;
+    k.lo = a < b ? a : b;
+    k.hi = a < b ? b : a;
+    k.h = sm64((((uint64_t)(uint32_t)k.lo) << 32 | (uint64_t)(uint32_t)k.hi) ^ salt);
+    return k;
+}
+
+__device__ __forceinline__ bool key_gt(const EKey& a, const EKey& b) {
+    if (a.w != b.w) return a.w > b.w;
+    if (a.h != b.h) return a.h > b.h;
+    if (a.lo != b.lo) return a.lo > b.lo;
+    return a.hi > b.hi;
+}
+
+// handshake round, step 1: every free vertex proposes to its max-key free neighbour
+__global__ void k_propose(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                          const uint32_t* __restrict__ w, const int* __restrict__ mate, int* __restrict__ prop,
+                          uint64_t salt, int* any) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        int best = -1;
+        if (mate[v] < 0) {
+            EKey bk{};
+            for (int p = rp[v]; p < rp[v + 1]; ++p) {
+                const int u = ci[p];
+                if (mate[u] >= 0) continue;
+                EKey k = make_key(w[p], v, u, salt);
+                if (best < 0 || key_gt(k, bk)) { bk = k; best = u; }
+            }
+        }
+        prop[v] = best;
+        if (best >= 0) *any = 1;
+    }
+}
+
+// handshake round, step 2: mutual proposals match
+__global__ void k_accept(int n, int* __restrict__ mate, const int* __restrict__ prop) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int u = prop[v];
+        if (u >= 0 && mate[v] < 0 && prop[u] == v) mate[v] = u;
+    }
+}
+
+// attach (A3) + leader (A4)
+__global__ void k_leader(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                         const uint32_t* __restrict__ w, const int* __restrict__ mate, uint64_t salt,
+                         int* __restrict__ leader, int* __restrict__ isl) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int m = mate[v];
+        if (m >= 0) {
+            leader[v] = v < m ? v : m;
+            isl[v] = v < m;
+        } else if (rp[v + 1] > rp[v]) {
+            EKey bk{};
+            int bu = -1;
+            for (int p = rp[v]; p < rp[v + 1]; ++p) {
+                EKey k = make_key(w[p], v, ci[p], salt);
+                if (bu < 0 || key_gt(k, bk)) { bk = k; bu = ci[p]; }
+            }
+            const int mu = mate[bu];  // matched by maximality
+            leader[v] = bu < mu ? bu : mu;
+            isl[v] = 0;
+        } else {
+            leader[v] = v;
+            isl[v] = 1;
+        }
+    }
+}
+
+__global__ void k_assign(int n, const int* __restrict__ leader, const int* __restrict__ id, int* __restrict__ agg) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) agg[v] = id[leader[v]];
+}
+
+int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* rounds, cudaStream_t s) {
+    const int n = G.n;
+    int* mate = dalloc<int>(n, s);
+    int* prop = dalloc<int>(n, s);
+    int* any = dalloc<int>(1, s);
+    int* hany = nullptr;
+    CK(cudaMallocHost(&hany, sizeof(int)));
+    CK(cudaMemsetAsync(mate, 0xff, sizeof(int) * (size_t)n, s));
+    int r = 0;
+    const int g = grid_for(n);
+    for (;;) {
+        CK(cudaMemsetAsync(any, 0, sizeof(int), s));
+        k_propose<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, prop, salt, any);
+        ++g_launches;
+        k_accept<<<g, kBlock, 0, s>>>(n, mate, prop);
+        ++g_launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hany, any, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (!*hany) break;
+        ++r;
+        if (r > 10000) throw Error(-7, "matching did not terminate");
+    }
+    CK(cudaFreeHost(hany));
+    int* leader = prop;  // reuse
+    int* isl = dalloc<int>((size_t)n + 1, s);
+    CK(cudaMemsetAsync(isl + n, 0, sizeof(int), s));
+    k_leader<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, salt, leader, isl);
+    ++g_launches;
+    CK(cudaGetLastError());
+    int* id = dalloc<int>((size_t)n + 1, s);
+    *nc = (int)exclusive_scan_total(isl, id, n, s);
+    k_assign<<<g, kBlock, 0, s>>>(n, leader, id, agg_t);
+    ++g_launches;
+    CK(cudaGetLastError());
+    dfree(id, s);
+    dfree(isl, s);
+    dfree(mate, s);
+    dfree(prop, s);
+    dfree(any, s);
+    *rounds = r;
+    return 0;
+}
+
+// ------------------------------------------------------------------ segmented reductions
+// keys for every stored entry of a CSR: (agg(i) << b) | agg(j); `drop` => self entries get the
+// sentinel (all ones in the low 2b bits) which sorts last.
+__global__ void k_pair_keys(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const int* __restrict__ agg, int b, bool drop, uint64_t* __restrict__ keys,
+                            int* __restrict__ idx) {
+    const uint64_t sentinel = (b >= 32) ? ~0ULL : ((1ULL << (2 * b)) - 1ULL);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t I = (uint64_t)agg[i];
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            const uint64_t J = (uint64_t)agg[ci[p]];
+            keys[p] = (drop && I == J) ? sentinel : ((I << b) | J);
+            idx[p] = p;
+        }
+    }
+}
+
+__global__ void k_heads(int64_t m, const uint64_t* __restrict__ keys, uint64_t sentinel, bool drop, int* head) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[t];
+        head[t] = (t == 0 || k != keys[t - 1]) && !(drop && k == sentinel);
+    }
+}
+
+__global__ void k_seg_start(int64_t m, const int* __restrict__ head, const int* __restrict__ pos,
+                            int* __restrict__ start) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+        if (head[t]) start[pos[t]] = (int)t;
+}
+
+// per segment: coarse column and the sequential sum of the segment's values
+template <class VAL>
+__global__ void k_seg_sum(int S, const int* __restrict__ start, int64_t m_valid, const uint64_t* __restrict__ keys,
+                          const int* __restrict__ idx, const VAL* __restrict__ src, int b, int* __restrict__ ocol,
+                          int* __restrict__ orow, VAL* __restrict__ oval) {
+    const uint64_t mask = (1ULL << b) - 1ULL;
+    for (int sg = blockIdx.x * blockDim.x + threadIdx.x; sg < S; sg += gridDim.x * blockDim.x) {
+        const int t0 = start[sg];
+        const int t1 = (sg + 1 < S) ? start[sg + 1] : (int)m_valid;
+        VAL acc = src[idx[t0]];
+        for (int t = t0 + 1; t < t1; ++t) acc += src[idx[t]];
+        const uint64_t k = keys[t0];
+        ocol[sg] = (int)(k & mask);
+        orow[sg] = (int)(k >> b);
+        oval[sg] = acc;
+    }
+}
+
+__global__ void k_rowptr_from_rows(int nrows, int S, const int* __restrict__ orow, int* __restrict__ rp) {
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I <= nrows; I += gridDim.x * blockDim.x) {
+        int lo = 0, hi = S;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (orow[mid] < I) lo = mid + 1; else hi = mid;
+        }
+        rp[I] = lo;
+    }
+}
+
+__global__ void k_lower_bound_u64(int64_t m, const uint64_t* keys, uint64_t x, int* out) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    *out = (int)lo;
+}
+
+// Quotient of a CSR under agg: returns (rp, ci, val) of the nc x nc result.  VAL = uint32
+// multiplicities (pass graphs, drop self entries) or double values (Galerkin, keep all).
+template <class VAL>
+static void quotient_impl(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg, int nc,
+                          bool drop, int** orp, int** oci, VAL** oval, int64_t* onnz, cudaStream_t s) {
+    const int b = bits_for(nc);
+    const uint64_t sentinel = (b >= 32) ? ~0ULL : ((1ULL << (2 * b)) - 1ULL);
+    const int m = (int)nnz;
+    uint64_t* k0 = dalloc<uint64_t>(m, s);
+    uint64_t* k1 = dalloc<uint64_t>(m, s);
+    int* i0 = dalloc<int>(m, s);
+    int* i1 = dalloc<int>(m, s);
+    k_pair_keys<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, agg, b, drop, k0, i0);
+    ++g_launches;
+    CK(cudaGetLastError());
+    sort_pairs(k0, k1, i0, i1, m, 2 * b, s);  // stable: equal keys keep (row, position) order
+    dfree(k0, s);
+    dfree(i0, s);
+    int* head = dalloc<int>((size_t)m + 1, s);
+    int* pos = dalloc<int>((size_t)m + 1, s);
+    CK(cudaMemsetAsync(head + m, 0, sizeof(int), s));
+    k_heads<<<grid_for(m), kBlock, 0, s>>>(m, k1, sentinel, drop, head);
+    ++g_launches;
+    CK(cudaGetLastError());
+    const int S = (int)exclusive_scan_total(head, pos, m, s);
+    int* start = dalloc<int>((size_t)S + 1, s);
+    k_seg_start<<<grid_for(m), kBlock, 0, s>>>(m, head, pos, start);
+    ++g_launches;
+    CK(cudaGetLastError());
+    int64_t m_valid = m;  // number of non-sentinel sorted entries (sentinels sort last)
+    dfree(head, s);
+    dfree(pos, s);
+    int* ocol = dalloc<int>((size_t)S + 8, s);
+    int* orow = dalloc<int>((size_t)S + 1, s);
+    VAL* ov = dalloc<VAL>((size_t)S + 8, s);
+    CK(cudaMemsetAsync(ocol, 0, sizeof(int) * ((size_t)S + 8), s));
+    CK(cudaMemsetAsync(ov, 0, sizeof(VAL) * ((size_t)S + 8), s));
+    if (drop) {
+        // m_valid = index of the first sentinel = number of non-sentinel keys
+        int* cnt = dalloc<int>(1, s);
+        k_lower_bound_u64<<<1, 1, 0, s>>>(m, k1, sentinel, cnt);
+        ++g_launches;
+        CK(cudaGetLastError());
+        m_valid = read_scalar(cnt, s);
+        dfree(cnt, s);
+    }
+    if (S > 0) {
+        k_seg_sum<VAL><<<grid_for(S), kBlock, 0, s>>>(S, start, m_valid, k1, i1, src, b, ocol, orow, ov);
+        ++g_launches;
+        CK(cudaGetLastError());
+    }
+    int* nrp = dalloc<int>((size_t)nc + 1, s);
+    k_rowptr_from_rows<<<grid_for(nc + 1), kBlock, 0, s>>>(nc, S, orow, nrp);
+    ++g_launches;
+    CK(cudaGetLastError());
+    dfree(orow, s);
+    dfree(start, s);
+    dfree(k1, s);
+    dfree(i1, s);
+    *orp = nrp;
+    *oci = ocol;
+    *oval = ov;
+    *onnz = S;
+}
+
+PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStream_t s) {
+    PassGraph H;
+    H.n = nc;
+    quotient_impl<uint32_t>(G.n, G.nnz, G.rp, G.ci, G.w, agg_t, nc, true, &H.rp, &H.ci, &H.w, &H.nnz, s);
+    return H;
+}
+
+Csr galerkin(const Csr& A, const int* agg, int nc, cudaStream_t s) {
+    Csr H;
+    H.n = nc;
+    quotient_impl<double>(A.n, A.nnz, A.rp, A.ci, A.v, agg, nc, false, &H.rp, &H.ci, &H.v, &H.nnz, s);
+    return H;
+}
+
+__global__ void k_compose(int n, int* __restrict__ agg, const int* __restrict__ agg_t) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) agg[i] = agg_t[agg[i]];
+}
+
+void compose(int n, int* agg, const int* agg_t, cudaStream_t s) {
+    k_compose<<<grid_for(n), kBlock, 0, s>>>(n, agg, agg_t);
+    ++g_launches;
+    CK(cudaGetLastError());
+}
+
+__global__ void k_iota(int n, int* a) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+__global__ void k_aptr(int nc, int n, const int* __restrict__ sorted_agg, int* __restrict__ aptr) {
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I <= nc; I += gridDim.x * blockDim.x) {
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (sorted_agg[mid] < I) lo = mid + 1; else hi = mid;
+        }
+        aptr[I] = lo;
+    }
+}
+
+void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s) {
+    int* iota = dalloc<int>(n, s);
+    int* sk = dalloc<int>(n, s);
+    k_iota<<<grid_for(n), kBlock, 0, s>>>(n, iota);
+    ++g_launches;
+    CK(cudaGetLastError());
+    sort_pairs(agg, sk, iota, perm, n, bits_for(nc), s);
+    k_aptr<<<grid_for(nc + 1), kBlock, 0, s>>>(nc, n, sk, aptr);
+    ++g_launches;
+    CK(cudaGetLastError());
+    dfree(iota, s);
+    dfree(sk, s);
+}
+
+// ------------------------------------------------------------------ tiles
+// Tile boundary at row r iff the bucket floor(rp[r]/H) changes, or r or r-1 is longer than H.
+// Then every tile holds <= 2H - 1 entries, or is a single long row (long path if > 2H).
+__global__ void k_tile_flags(int n, const int* __restrict__ rp, int H, int* __restrict__ flag) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        int f = (r == 0);
+        if (r > 0) {
+            const int a = rp[r - 1], b = rp[r], c = rp[r + 1];
+            f = (a / H != b / H) || (c - b > H) || (b - a > H);
+        }
+        flag[r] = f;
+    }
+}
+
+__global__ void k_tile_rows(int n, const int* __restrict__ flag, const int* __restrict__ pos, int* __restrict__ row,
+                            int ntiles) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+        if (flag[r]) row[pos[r]] = r;
+    if (blockIdx.x == 0 && threadIdx.x == 0) row[ntiles] = n;
+}
+
+int tiled_grid(int cap, int ntiles);  // k_solve.cu
+
+Tiles build_tiles(const Csr& A, int grid_per_sm, cudaStream_t s) {
+    (void)grid_per_sm;
+    Tiles T;
+    const double avg = A.n > 0 ? (double)A.nnz / (double)A.n : 1.0;
+    int H = (int)std::ceil(256.0 * avg);
+    H = (H + 3) & ~3;
+    if (H < 256) H = 256;
+    if (H > 2048) H = 2048;
+    T.cap = 2 * H;
+    int* flag = dalloc<int>((size_t)A.n + 1, s);
+    int* pos = dalloc<int>((size_t)A.n + 1, s);
+    CK(cudaMemsetAsync(flag + A.n, 0, sizeof(int), s));
+    k_tile_flags<<<grid_for(A.n), kBlock, 0, s>>>(A.n, A.rp, H, flag);
+    ++g_launches;
+    CK(cudaGetLastError());
+    T.ntiles = (int)exclusive_scan_total(flag, pos, A.n, s);
+    T.row = dalloc<int>((size_t)T.ntiles + 1, s);
+    k_tile_rows<<<grid_for(A.n), kBlock, 0, s>>>(A.n, flag, pos, T.row, T.ntiles);
+    ++g_launches;
+    CK(cudaGetLastError());
+    dfree(flag, s);
+    dfree(pos, s);
+    T.grid = tiled_grid(T.cap, T.ntiles);
+    return T;
+}
+
+// ------------------------------------------------------------------ coarsest (a7)
+__global__ void k_densify(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                          double shift_per_entry, double* __restrict__ M) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        for (int j = 0; j < n; ++j) M[(size_t)i * n + j] = shift_per_entry;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) M[(size_t)i * n + ci[p]] += v[p];
+    }
+}
+
+// one Gauss-Jordan step k (in-place inverse of an SPD matrix, no pivoting): B' from B
+__global__ void k_gj_step(int n, int k, const double* __restrict__ B, double* __restrict__ Bn) {
+    const double piv = B[(size_t)k * n + k];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / n), j = (int)(e % n);
+        double r;
+        if (i == k && j == k) r = 1.0 / piv;
+        else if (i == k) r = B[(size_t)k * n + j] / piv;
+        else if (j == k) r = -B[(size_t)i * n + k] / piv;
+        else r = B[e] - B[(size_t)i * n + k] * B[(size_t)k * n + j] / piv;
+        Bn[e] = r;
+    }
+}
+
+__global__ void k_add_const(int64_t m, double c, double* a) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+        a[e] += c;
+}
+
+double* coarse_inverse(const Csr& A, bool singular, double shift, cudaStream_t s) {
+    const int n = A.n;
+    const size_t m = (size_t)n * n;
+    double* M0 = dalloc<double>(m, s);
+    double* M1 = dalloc<double>(m, s);
+    // singular: factor A + (s/n) 1 1^T; A^dagger = (A + s J)^{-1} - J/s, J = 1 1^T / n  (reading A16)
+    k_densify<<<grid_for(n), kBlock, 0, s>>>(n, A.rp, A.ci, A.v, singular ? shift / (double)n : 0.0, M0);
+    ++g_launches;
+    CK(cudaGetLastError());
+    for (int k = 0; k < n; ++k) {
+        k_gj_step<<<grid_for((int64_t)m), kBlock, 0, s>>>(n, k, M0, M1);
+        ++g_launches;
+        std::swap(M0, M1);
+    }
+    CK(cudaGetLastError());
+    if (singular) {
+        k_add_const<<<grid_for((int64_t)m), kBlock, 0, s>>>((int64_t)m, -1.0 / (shift * (double)n), M0);
+        ++g_launches;
+        CK(cudaGetLastError());
+    }
+    dfree(M1, s);
+    return M0;
+}
+
+}  // namespace amg

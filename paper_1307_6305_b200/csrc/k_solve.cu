@@ -1,0 +1,446 @@
+// k_solve.cu -- solve-phase kernels of libamg_b200.so (sm_100a): the hot path of SURVEY.md 8(a)
+// rows a9-a16.  HBM-bound fp64 CSR work; no tensor cores (nothing here is a dense contraction).
+//
+//  * SpMV-class kernels (smoother step a9, residual a10, SpMV+dots a15) share one tiled,
+//    grid-stride kernel: each tile's contiguous col/val run is streamed into shared memory with
+//    16-byte non-allocating loads (coalesced), then one thread per row reduces its row from shared
+//    memory, gathers x through the read-only path, and runs the fused epilogue (three-term update,
+//    residual, dots).  One pass over A per smoother degree step.
+//  * Reductions are deterministic: per-block partials in a fixed order, the last block to finish
+//    (atomic ticket) sums them in a fixed order and resets the ticket.
+//  * Restriction (a11) is a per-aggregate sequential sum over the aggregate-sorted order; the
+//    prolongation (a12) is fused with its axpy.
+#include <cuda_runtime.h>
+
+#include "amg_internal.h"
+
+namespace amg {
+
+long long g_launches = 0;
+static int g_num_sms = 148;
+
+void init_device_props() {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+}
+
+int vector_grid() { return g_num_sms * 4; }
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum (fixed order => deterministic).  All threads get the result.
+__device__ double block_sum(double v) {
+    __shared__ double red[32];
+    __shared__ double total;
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = lane < nw ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) total = t;
+    }
+    __syncthreads();
+    return total;
+}
+
+struct DotOut {
+    double* p[4];
+};
+
+// Two-stage deterministic reduction of ND per-thread accumulators into *out.p[k], k < ND.
+template <int ND>
+__device__ void finalize_dots(double (&acc)[ND], double* partials, unsigned* ticket, DotOut out) {
+    __shared__ bool amlast;
+    const int G = gridDim.x;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+        double b = block_sum(acc[k]);
+        if (threadIdx.x == 0) partials[k * G + blockIdx.x] = b;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) amlast = (atomicAdd(ticket, 1u) == (unsigned)(G - 1));
+    __syncthreads();
+    if (amlast) {
+        __threadfence();
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+            double v = 0.0;
+            for (int b = threadIdx.x; b < G; b += blockDim.x) v += __ldcg(partials + k * G + b);
+            v = block_sum(v);
+            if (threadIdx.x == 0) *out.p[k] = v;
+        }
+        if (threadIdx.x == 0) *ticket = 0u;
+    }
+}
+
+// ------------------------------------------------------------------ epilogues
+struct EpiSmooth {  // three-term recurrence step, optional implicit x_{k-1} = cp*f
+    const double* f;
+    const double* xprev;
+    double* out;
+    double alpha, beta, cg, cp;
+    static constexpr int ND = 0;
+    __device__ __forceinline__ void operator()(int i, double s, double xgi, double*) const {
+        double fi = f[i];
+        double prev = xprev ? xprev[i] : cp * fi;
+        out[i] = alpha * (cg * xgi) + (1.0 - alpha) * prev + beta * (fi - cg * s);
+    }
+};
+
+struct EpiResid {  // out = f - A x; acc[0] += out^2 (used only when a dot pointer is given)
+    const double* f;
+    double* out;
+    static constexpr int ND = 1;
+    __device__ __forceinline__ void operator()(int i, double s, double, double* acc) const {
+        double r = f[i] - s;
+        out[i] = r;
+        acc[0] += r * r;
+    }
+};
+
+struct EpiSpmvDots {  // q = A d; acc = (d.q, d.rho)
+    const double* rho;
+    double* q;
+    static constexpr int ND = 2;
+    __device__ __forceinline__ void operator()(int i, double s, double di, double* acc) const {
+        q[i] = s;
+        acc[0] += di * s;
+        acc[1] += di * rho[i];
+    }
+};
+
+// ------------------------------------------------------------------ tiled SpMV-class kernel
+// Shared memory per block: cap+2 doubles and cap+4 ints (16-byte aligned staging of the tile's
+// col/val run from the 16-byte-aligned chunk containing its first entry).
+template <class Epi, bool DOTS>
+__global__ void __launch_bounds__(kBlock) k_tiled(Csr A, const double* __restrict__ xg,
+                                                  const int* __restrict__ tile_row, int ntiles, int cap, Epi epi,
+                                                  double* partials, unsigned* ticket, DotOut dot_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* sv = reinterpret_cast<double*>(smem_raw);
+    int* sc = reinterpret_cast<int*>(sv + cap + 2);
+    double acc[Epi::ND > 0 ? Epi::ND : 1];
+#pragma unroll
+    for (int k = 0; k < (Epi::ND > 0 ? Epi::ND : 1); ++k) acc[k] = 0.0;
+    const int* __restrict__ rp = A.rp;
+    const int* __restrict__ ci = A.ci;
+    const double* __restrict__ va = A.v;
+
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int r0 = tile_row[t], r1 = tile_row[t + 1];
+        const int p0 = rp[r0], p1 = rp[r1];
+        if (p1 - p0 <= cap) {
+            const int a0 = p0 & ~1;
+            const int nv2 = (p1 - a0 + 1) >> 1;
+            const double2* gv = reinterpret_cast<const double2*>(va + a0);
+            double2* sv2 = reinterpret_cast<double2*>(sv);
+            const int c0 = p0 & ~3;
+            const int nc4 = (p1 - c0 + 3) >> 2;
+            const int4* gc = reinterpret_cast<const int4*>(ci + c0);
+            int4* sc4 = reinterpret_cast<int4*>(sc);
+            for (int k = threadIdx.x; k < nv2; k += kBlock) sv2[k] = ld_stream(gv + k);
+            for (int k = threadIdx.x; k < nc4; k += kBlock) sc4[k] = ld_stream(gc + k);
+            __syncthreads();
+            for (int i = r0 + threadIdx.x; i < r1; i += kBlock) {
+                const int q0 = rp[i], q1 = rp[i + 1];
+                double s = 0.0;
+                for (int q = q0; q < q1; ++q) s = fma(sv[q - a0], __ldg(xg + sc[q - c0]), s);
+                epi(i, s, __ldg(xg + i), acc);
+            }
+            __syncthreads();
+        } else {  // single long row: block-wide reduction straight from global memory
+            double s = 0.0;
+            for (int q = p0 + threadIdx.x; q < p1; q += kBlock) s = fma(va[q], __ldg(xg + ci[q]), s);
+            s = block_sum(s);
+            if (threadIdx.x == 0) epi(r0, s, __ldg(xg + r0), acc);
+            __syncthreads();
+        }
+    }
+    if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
+}
+
+static size_t tile_smem(const Tiles& T) { return (size_t)(T.cap + 2) * sizeof(double) + (size_t)(T.cap + 4) * sizeof(int); }
+
+template <class Epi, bool DOTS>
+static void configure_tiled() {
+    static bool configured = false;  // per template instance
+    if (!configured) {
+        CK(cudaFuncSetAttribute(k_tiled<Epi, DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+    }
+}
+
+int tiled_grid(int cap, int ntiles) {
+    configure_tiled<EpiSmooth, false>();
+    const size_t sm = (size_t)(cap + 2) * sizeof(double) + (size_t)(cap + 4) * sizeof(int);
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_tiled<EpiSmooth, false>, kBlock, sm));
+    if (bps < 1) bps = 1;
+    int g = g_num_sms * bps;
+    if (g > ntiles) g = ntiles;
+    if (g < 1) g = 1;
+    return g;
+}
+
+template <class Epi, bool DOTS>
+static void launch_tiled(const Csr& A, const Tiles& T, const double* xg, const Epi& epi, const DotScratch* ds,
+                         DotOut dot_out, cudaStream_t s) {
+    size_t sm = tile_smem(T);
+    configure_tiled<Epi, DOTS>();
+    k_tiled<Epi, DOTS><<<T.grid, kBlock, sm, s>>>(A, xg, T.row, T.ntiles, T.cap, epi, ds ? ds->partials : nullptr,
+                                                   ds ? ds->ticket : nullptr, dot_out);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+void launch_smooth(const Csr& A, const Tiles& T, const double* xg, double cg, const double* f, const double* xprev,
+                   double cp, double alpha, double beta, double* out, cudaStream_t s) {
+    EpiSmooth e{f, xprev, out, alpha, beta, cg, cp};
+    launch_tiled<EpiSmooth, false>(A, T, xg, e, nullptr, DotOut{}, s);
+}
+
+void launch_resid(const Csr& A, const Tiles& T, const double* xg, const double* f, double* out, double* dot_rr,
+                  const DotScratch& ds, cudaStream_t s) {
+    EpiResid e{f, out};
+    if (dot_rr)
+        launch_tiled<EpiResid, true>(A, T, xg, e, &ds, DotOut{{dot_rr}}, s);
+    else
+        launch_tiled<EpiResid, false>(A, T, xg, e, nullptr, DotOut{}, s);
+}
+
+void launch_spmv_dots(const Csr& A, const Tiles& T, const double* d, const double* rho, double* q, double* dot_dq,
+                      double* dot_dr, const DotScratch& ds, cudaStream_t s) {
+    EpiSpmvDots e{rho, q};
+    launch_tiled<EpiSpmvDots, true>(A, T, d, e, &ds, DotOut{{dot_dq, dot_dr}}, s);
+}
+
+// ------------------------------------------------------------------ transfers
+__global__ void __launch_bounds__(kBlock) k_restrict(int nc, const int* __restrict__ aptr,
+                                                     const int* __restrict__ perm, const double* __restrict__ r,
+                                                     double* __restrict__ rH) {
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+        const int t0 = aptr[I], t1 = aptr[I + 1];
+        double s = 0.0;
+        for (int t = t0; t < t1; ++t) s += __ldg(r + perm[t]);
+        rH[I] = s;
+    }
+}
+
+void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, double* rH, cudaStream_t s) {
+    int grid = (nc + kBlock - 1) / kBlock;
+    if (grid > vector_grid()) grid = vector_grid();
+    k_restrict<<<grid, kBlock, 0, s>>>(nc, aptr, perm, r, rH);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+__global__ void __launch_bounds__(kBlock) k_prolong(int n, const int* __restrict__ agg,
+                                                    const double* __restrict__ eH, double* __restrict__ x) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += __ldg(eH + agg[i]);
+}
+
+void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s) {
+    int grid = (n + kBlock - 1) / kBlock;
+    if (grid > vector_grid()) grid = vector_grid();
+    k_prolong<<<grid, kBlock, 0, s>>>(n, agg, eH, x);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+// warp per row GEMV of the dense coarsest (pseudo-)inverse
+__global__ void __launch_bounds__(kBlock) k_gemv(int n, const double* __restrict__ M, const double* __restrict__ r,
+                                                 double* __restrict__ e) {
+    const int lane = threadIdx.x & 31;
+    const int nwarp = (gridDim.x * blockDim.x) >> 5;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarp) {
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32) s = fma(M[(size_t)i * n + j], __ldg(r + j), s);
+        s = warp_sum(s);
+        if (lane == 0) e[i] = s;
+    }
+}
+
+void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_t s) {
+    int grid = (n * 32 + kBlock - 1) / kBlock;
+    if (grid > vector_grid()) grid = vector_grid();
+    k_gemv<<<grid, kBlock, 0, s>>>(n, M, r, e);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+// ------------------------------------------------------------------ FCG vector kernels
+struct PtrArr {
+    const double* p[kMaxWin];
+};
+
+__global__ void __launch_bounds__(kBlock) k_multidot(int n, const double* __restrict__ z, PtrArr Q, int w,
+                                                     double* partials, unsigned* ticket, double* c) {
+    double acc[kMaxWin];
+#pragma unroll
+    for (int j = 0; j < kMaxWin; ++j) acc[j] = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double zi = z[i];
+#pragma unroll
+        for (int j = 0; j < kMaxWin; ++j)
+            if (j < w) acc[j] += zi * Q.p[j][i];
+    }
+    // reduce only the first w accumulators (w is uniform)
+    __shared__ bool amlast;
+    const int G = gridDim.x;
+    for (int j = 0; j < w; ++j) {
+        double b = block_sum(acc[j]);
+        if (threadIdx.x == 0) partials[j * G + blockIdx.x] = b;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) amlast = (atomicAdd(ticket, 1u) == (unsigned)(G - 1));
+    __syncthreads();
+    if (amlast) {
+        __threadfence();
+        for (int j = 0; j < w; ++j) {
+            double v = 0.0;
+            for (int b = threadIdx.x; b < G; b += blockDim.x) v += __ldcg(partials + j * G + b);
+            v = block_sum(v);
+            if (threadIdx.x == 0) c[j] = v;
+        }
+        if (threadIdx.x == 0) *ticket = 0u;
+    }
+}
+
+void launch_multidot(int n, const double* z, const double* const* Q, int w, double* c, const DotScratch& ds,
+                     cudaStream_t s) {
+    PtrArr a{};
+    for (int j = 0; j < w; ++j) a.p[j] = Q[j];
+    k_multidot<<<vector_grid(), kBlock, 0, s>>>(n, z, a, w, ds.partials, ds.ticket, c);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+__global__ void __launch_bounds__(kBlock) k_direction(int n, const double* __restrict__ z, PtrArr D,
+                                                      const double* __restrict__ c, const double* __restrict__ dq,
+                                                      int w, double* __restrict__ d) {
+    double beta[kMaxWin];
+#pragma unroll
+    for (int j = 0; j < kMaxWin; ++j) beta[j] = j < w ? c[j] / dq[j] : 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double v = z[i];
+#pragma unroll
+        for (int j = 0; j < kMaxWin; ++j)
+            if (j < w) v -= beta[j] * D.p[j][i];
+        d[i] = v;
+    }
+}
+
+void launch_direction(int n, const double* z, const double* const* D, const double* c, const double* dq, int w,
+                      double* d, cudaStream_t s) {
+    PtrArr a{};
+    for (int j = 0; j < w; ++j) a.p[j] = D[j];
+    k_direction<<<vector_grid(), kBlock, 0, s>>>(n, z, a, c, dq, w, d);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+template <bool ASSIGN, bool UPD_R, bool RR>
+__global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __restrict__ dr,
+                                                       const double* __restrict__ dq, const double* __restrict__ d,
+                                                       const double* __restrict__ q, double* __restrict__ x,
+                                                       double* __restrict__ r, int* breakdown, double* partials,
+                                                       unsigned* ticket, double* rr) {
+    const double den = *dq;
+    double alpha;
+    if (breakdown) {  // outer FCG: d.q <= 0 or NaN is a breakdown
+        alpha = (den > 0.0) ? (*dr) / den : 0.0;
+        if (!(den > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) *breakdown = 1;
+    } else {          // inner: rho = 0 => d = 0 => 0/0, take alpha = 0 (DESIGN.md readings)
+        alpha = (den != 0.0) ? (*dr) / den : 0.0;
+    }
+    double acc[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double di = d[i];
+        if (ASSIGN) x[i] = alpha * di; else x[i] += alpha * di;
+        if (UPD_R) {
+            double ri = r[i] - alpha * q[i];
+            r[i] = ri;
+            if (RR) acc[0] += ri * ri;
+        }
+    }
+    if (RR) finalize_dots<1>(acc, partials, ticket, DotOut{{rr}});
+}
+
+void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
+                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s) {
+    dim3 g(vector_grid()), b(kBlock);
+    if (assign_x) {
+        if (r) k_fcg_update<true, true, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
+        else   k_fcg_update<true, false, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
+    } else if (r && rr) {
+        k_fcg_update<false, true, true><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, ds.partials, ds.ticket, rr);
+    } else if (r) {
+        k_fcg_update<false, true, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
+    } else {
+        k_fcg_update<false, false, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
+    }
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+__global__ void __launch_bounds__(kBlock) k_dot(int n, const double* __restrict__ x, const double* __restrict__ y,
+                                                double* partials, unsigned* ticket, double* out) {
+    double acc[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        acc[0] += x[i] * (y ? y[i] : 1.0);
+    finalize_dots<1>(acc, partials, ticket, DotOut{{out}});
+}
+
+void launch_dot(int n, const double* x, const double* y, double* out, const DotScratch& ds, cudaStream_t s) {
+    k_dot<<<vector_grid(), kBlock, 0, s>>>(n, x, y, ds.partials, ds.ticket, out);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+__global__ void __launch_bounds__(kBlock) k_sub_scalar(int n, double* __restrict__ v, const double* __restrict__ sum) {
+    const double mu = (*sum) / (double)n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] -= mu;
+}
+
+void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cudaStream_t s) {
+    launch_dot(n, v, nullptr, tmp, ds, s);
+    k_sub_scalar<<<vector_grid(), kBlock, 0, s>>>(n, v, tmp);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+__global__ void __launch_bounds__(kBlock) k_copy(int n, const double* __restrict__ x, double* __restrict__ y) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = x[i];
+}
+
+void launch_copy(int n, const double* x, double* y, cudaStream_t s) {
+    k_copy<<<vector_grid(), kBlock, 0, s>>>(n, x, y);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+}  // namespace amg

@@ -1,0 +1,279 @@
+"""-m gpu parity of the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star): aggregate ids and coarse sparsity bit-exact; per-level coarse
+values <= 1e-12 relative; one preconditioner application <= 1e-10 relative; final relative
+residual <= tol with FCG iteration counts within +-1 of the oracle.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def amg():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1307_6305_b200 import amg as A
+
+    A.load()
+    return A
+
+
+def gpu_setup(amg, p, device_arrays=False, **over):
+    prm = dict(p.params)
+    prm.update(over)
+    o = amg.amg_options_default(coarsest_size=prm.get("coarsest_size", 100), kappa=prm.get("kappa", 0.0),
+                                seed=prm.get("seed", 0), restart=prm.get("restart", 5))
+    arrs = [p.rp, p.ci, p.val, p.d]
+    if device_arrays:
+        import torch
+
+        arrs = [None if a is None else torch.from_numpy(a).cuda() for a in arrs]
+    h = amg.amg_setup(*arrs, prm["passes"], prm["degree"], o)
+    return h
+
+
+def compare_hierarchy(amg, h, hier, m, exact_values):
+    info = amg.amg_get_info(h)
+    assert info["levels"] == hier.nlev
+    for l in range(hier.nlev):
+        rp, ci, v, agg = amg.amg_level_export(h, l, m)
+        orp, oci, ov = hier.level_csr(l)
+        oi = hier.level_info(l)
+        assert np.array_equal(rp, orp), f"level {l} row_ptr"
+        assert np.array_equal(ci, oci), f"level {l} col"
+        if exact_values:
+            assert np.array_equal(v, ov), f"level {l} values not bit-exact"
+        else:
+            assert np.max(np.abs(v - ov)) <= 1e-12 * np.max(np.abs(ov)), f"level {l} values"
+        s = amg.amg_level_sizes(h, l, m)
+        assert s["lambda1"] == pytest.approx(oi["lambda1"], rel=1e-15, abs=0)
+        assert s["kappa"] == pytest.approx(oi["kappa"], rel=4e-16)
+        a, b = hier.level_coeffs(l)
+        assert np.allclose(s["alpha"], a, rtol=4e-15, atol=0) and np.allclose(s["beta"], b, rtol=4e-15, atol=0)
+        if l < hier.nlev - 1:
+            assert s["nc"] == oi["nc"]
+            assert np.array_equal(agg, hier.level_agg(l)), f"level {l} aggregates"
+
+
+def small_cases(gen):
+    cases = [gen.problem("C1"), gen.problem("C2", size=96)]
+    c = gen.problem("C4", size=14)
+    c.params["coarsest_size"] = 30
+    cases.append(c)
+    for seed, (n, weighted, dirichlet) in enumerate([(700, True, True), (900, False, False), (1500, True, False)]):
+        q = gen.random_graph(n, 6, seed=seed + 40, weighted=weighted, dirichlet=dirichlet)
+        q.params = dict(passes=2, degree=3, coarsest_size=40, seed=seed)
+        cases.append(q)
+    q = gen.rgg(5000, seed=3)
+    q.params = dict(passes=3, degree=4, coarsest_size=60, seed=1)
+    cases.append(q)
+    return cases
+
+
+def test_hierarchy_bit_exact_small(amg, gen_mod, oracle_mod):
+    for p in small_cases(gen_mod):
+        hier = oracle_mod.setup_problem(p)
+        h = gpu_setup(amg, p)
+        try:
+            integer_valued = bool(np.all(p.val == np.round(p.val)) and (p.d is None or np.all(p.d == np.round(p.d))))
+            compare_hierarchy(amg, h, hier, p.params["degree"], exact_values=True)
+            del integer_valued
+        finally:
+            amg.amg_free(h)
+
+
+def test_device_pointer_inputs(amg, gen_mod, oracle_mod):
+    p = gen_mod.problem("C1")
+    hier = oracle_mod.setup_problem(p)
+    h = gpu_setup(amg, p, device_arrays=True)
+    try:
+        compare_hierarchy(amg, h, hier, p.params["degree"], exact_values=True)
+    finally:
+        amg.amg_free(h)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C4s", "rgg"])
+def test_smoother_precond_coarse_parity(amg, gen_mod, oracle_mod, name):
+    p = {"C1": lambda: gen_mod.problem("C1"), "C2s": lambda: gen_mod.problem("C2", size=128),
+         "C4s": lambda: gen_mod.problem("C4", size=16)}.get(name, None)
+    if p is None:
+        p = gen_mod.rgg(6000, seed=5)
+        p.params = dict(passes=3, degree=3, coarsest_size=50, seed=0)
+    else:
+        p = p()
+    hier = oracle_mod.setup_problem(p)
+    h = gpu_setup(amg, p)
+    m = p.params["degree"]
+    rng = np.random.default_rng(1)
+    try:
+        for l in range(hier.nlev - 1):
+            n = hier.level_info(l)["n"]
+            f = rng.uniform(-1, 1, n)
+            x0 = rng.uniform(-1, 1, n)
+            x = np.empty(n)
+            amg.amg_level_smooth(h, l, f, x0, x)
+            ref = hier.smooth(l, f, x0)
+            assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref), f"smoother level {l}"
+        for l in range(hier.nlev):
+            n = hier.level_info(l)["n"]
+            r = rng.uniform(-1, 1, n)
+            z = np.empty(n)
+            amg.amg_level_precond(h, l, 2, r, z)
+            ref = hier.precond(r, nu=2, level=l)
+            assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref), f"B_{l}(r)"
+        nL = hier.level_info(hier.nlev - 1)["n"]
+        r = rng.uniform(-1, 1, nL)
+        e = np.empty(nL)
+        amg.amg_coarse_solve(h, r, e)
+        ref = hier.coarse_solve(r)
+        assert np.linalg.norm(e - ref) <= 1e-10 * np.linalg.norm(ref)
+    finally:
+        amg.amg_free(h)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4s", "rgg", "rand_spd"])
+def test_full_solve_parity(amg, gen_mod, oracle_mod, name):
+    if name == "C4s":
+        p = gen_mod.problem("C4", size=24)
+    elif name == "rgg":
+        p = gen_mod.rgg(20000, seed=7)
+        p.params = dict(passes=4, degree=4, coarsest_size=100, seed=0, tol=1e-8, k_inner=2)
+    elif name == "rand_spd":
+        p = gen_mod.random_graph(3000, 7, seed=9, weighted=True, dirichlet=True)
+        p.params = dict(passes=2, degree=2, coarsest_size=50, seed=0, tol=1e-8, k_inner=2)
+    else:
+        p = gen_mod.problem(name)
+    hier = oracle_mod.setup_problem(p)
+    b = gen_mod.rhs(p.n, 0)
+    ref = hier.solve(b, tol=1e-8, nu=2)
+    h = gpu_setup(amg, p)
+    try:
+        for use_host in (True, False):
+            if use_host:
+                x = np.zeros(p.n)
+                st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+            else:
+                import torch
+
+                bt = torch.from_numpy(b).cuda()
+                xt = torch.zeros(p.n, dtype=torch.float64, device="cuda")
+                st, it, rr = amg.amg_solve(h, bt, xt, 1e-8, 2)
+                x = xt.cpu().numpy()
+            info = amg.amg_get_info(h)
+            assert st == 0 and rr <= 1e-8 and info["last_true_relres"] <= 2e-8
+            assert abs(it - ref["iters"]) <= 1, (it, ref["iters"])
+            assert np.linalg.norm(x - ref["x"]) <= 1e-6 * np.linalg.norm(ref["x"])
+        # determinism: a second solve is bitwise identical (T6)
+        x1 = np.zeros(p.n)
+        x2 = np.zeros(p.n)
+        amg.amg_solve(h, b, x1, 1e-8, 2)
+        amg.amg_solve(h, b, x2, 1e-8, 2)
+        assert np.array_equal(x1, x2)
+    finally:
+        amg.amg_free(h)
+
+
+def test_no_graph_path_matches_graph_path(amg, gen_mod):
+    p = gen_mod.problem("C2", size=200)
+    b = gen_mod.rhs(p.n, 2)
+    xs = []
+    for g in (1, 0):
+        o = amg.amg_options_default(coarsest_size=100, use_graphs=g)
+        h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 3, 3, o)
+        x = np.zeros(p.n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        assert st == 0
+        xs.append((it, x))
+        amg.amg_free(h)
+    assert xs[0][0] == xs[1][0] and np.array_equal(xs[0][1], xs[1][1])
+
+
+def test_edge_cases(amg, gen_mod, oracle_mod):
+    # one level only (n <= coarsest): exact solve, 1 iteration
+    p = gen_mod.grid2d(8)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 2, 3, amg.amg_options_default(coarsest_size=100))
+    b = gen_mod.rhs(p.n, 0)
+    x = np.zeros(p.n)
+    st, it, rr = amg.amg_solve(h, b, x, 1e-10, 2)
+    assert st == 0 and it == 1 and rr < 1e-12
+    # zero rhs -> zero solution, 0 iterations
+    x = np.ones(p.n)
+    st, it, rr = amg.amg_solve(h, np.zeros(p.n), x, 1e-8, 2)
+    assert st == 0 and it == 0 and np.all(x == 0)
+    # x0 = exact solution -> 0 iterations
+    xs = np.linalg.solve(np.diag(np.zeros(p.n)) + _dense(p), b)
+    x = xs.copy()
+    st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+    assert it == 0
+    amg.amg_free(h)
+    # invalid inputs
+    bad = p.val.copy()
+    bad[1] = 0.25
+    with pytest.raises(amg.AmgError) as e:
+        amg.amg_setup(p.rp, p.ci, bad, p.d, 2, 3)
+    assert e.value.code == amg.AMG_E_INPUT
+    ci = p.ci.copy()
+    ci[0], ci[1] = ci[1], ci[0]
+    with pytest.raises(amg.AmgError) as e:
+        amg.amg_setup(p.rp, ci, p.val, p.d, 2, 3)
+    assert e.value.code == amg.AMG_E_INPUT
+    with pytest.raises(amg.AmgError) as e:
+        amg.amg_setup(p.rp, p.ci, p.val, -p.d, 2, 3)
+    assert e.value.code == amg.AMG_E_INPUT
+    # stagnation: diagonal-only above the coarsest size
+    n = 500
+    with pytest.raises(amg.AmgError) as e:
+        amg.amg_setup(np.zeros(n + 1, np.int64), np.zeros(0, np.int32), np.zeros(0), np.ones(n), 1, 2,
+                      amg.amg_options_default(coarsest_size=10))
+    assert e.value.code == amg.AMG_E_SETUP
+    # missing diagonals are inserted exactly like the oracle does
+    q = gen_mod.random_graph(400, 5, seed=3, weighted=True)
+    keep = q.ci != np.repeat(np.arange(q.n), np.diff(q.rp))
+    rp = np.concatenate([[0], np.cumsum(np.add.reduceat(keep.astype(np.int64), q.rp[:-1]))]).astype(np.int64)
+    hier = oracle_mod.Hierarchy(rp, q.ci[keep], q.val[keep], q.d, 2, 3, coarsest_size=20)
+    h = amg.amg_setup(rp, np.ascontiguousarray(q.ci[keep]), np.ascontiguousarray(q.val[keep]), q.d, 2, 3,
+                      amg.amg_options_default(coarsest_size=20))
+    compare_hierarchy(amg, h, hier, 3, exact_values=True)
+    amg.amg_free(h)
+
+
+def _dense(p):
+    A = np.zeros((p.n, p.n))
+    for i in range(p.n):
+        A[i, p.ci[p.rp[i]:p.rp[i + 1]]] += p.val[p.rp[i]:p.rp[i + 1]]
+    return A + np.diag(p.d)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3"])
+def test_full_size_hierarchy_and_precond(amg, gen_mod, oracle_mod, name):
+    """Full BASELINE size, in the configuration bench.py times: the whole hierarchy bit-exact, one
+    B_0(r) within 1e-10, and the solve's iteration count within +-1 of the committed oracle count
+    (tests/golden/oracle_iters.json, written by tools/oracle_golden.py from oracle/ only)."""
+    p = gen_mod.problem(name)
+    hier = oracle_mod.setup_problem(p)
+    h = gpu_setup(amg, p)
+    try:
+        compare_hierarchy(amg, h, hier, p.params["degree"], exact_values=True)
+        r = gen_mod.rhs(p.n, 11)
+        z = np.empty(p.n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        ref = hier.precond(r, nu=2)
+        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        b = gen_mod.rhs(p.n, 0)
+        x = np.zeros(p.n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        gold = json.load(open(os.path.join(GOLD, "oracle_iters.json")))
+        assert st == 0 and rr <= 1e-8
+        assert abs(it - gold[name]["iters"]) <= 1
+    finally:
+        amg.amg_free(h)
