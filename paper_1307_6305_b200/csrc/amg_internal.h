@@ -40,6 +40,22 @@ struct Tiles {         // row tiles of the SpMV-class kernels: tile t = rows [ro
     int* row = nullptr;
 };
 
+struct Sell {          // SELL-32: 32-row slices, entries column-major inside a slice (lane = row % 32)
+    int n = 0;
+    int nslices = 0;
+    int* sptr = nullptr;   // [nslices+1] slice offsets in units of 32 entries; width_s = sptr[s+1]-sptr[s]
+    int* col = nullptr;    // [32 * sptr[nslices]]; padding: col = a valid row, val = 0
+    double* val = nullptr;
+    int64_t padded = 0;    // 32 * sptr[nslices]
+};
+
+struct SpOp {          // the operator of one level as the SpMV-class kernels see it
+    Csr A;
+    Tiles T;
+    Sell S;
+    bool sell = false;     // true: SELL-32 warp-per-slice kernel; false: CSR row-tile kernel
+};
+
 struct DotScratch {    // deterministic two-stage reductions (per-block partials + last-block sum)
     double* partials = nullptr;  // [kMaxWin+2][max grid]
     unsigned* ticket = nullptr;  // zero-initialised counter, reset by the last block
@@ -87,8 +103,10 @@ void compose(int n, int* agg, const int* agg_t, cudaStream_t s);
 Csr galerkin(const Csr& A, const int* agg, int nc, cudaStream_t s);
 // perm = vertices sorted stably by aggregate, aptr[I] = first position of aggregate I
 void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s);
-// row tiles for the SpMV-class kernels
+// row tiles for the CSR SpMV-class kernels
 Tiles build_tiles(const Csr& A, int grid_per_sm, cudaStream_t s);
+// SELL-32 copy of A (built when its padding is acceptable); returns S with S.col == nullptr otherwise
+Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s);
 // dense (pseudo-)inverse of the coarsest operator, row-major n x n
 double* coarse_inverse(const Csr& A, bool singular, double shift, cudaStream_t s);
 void free_csr(Csr& A, cudaStream_t s);
@@ -100,13 +118,13 @@ extern long long g_launches;
 // SpMV-class fused kernels (one pass over A_l):
 //  smooth: out_i = alpha*cg*xg_i + (1-alpha)*prev_i + beta*(f_i - cg*(A xg)_i),
 //          prev_i = xprev ? xprev_i : cp*f_i          (three-term recurrence step)
-void launch_smooth(const Csr& A, const Tiles& T, const double* xg, double cg, const double* f, const double* xprev,
+void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f, const double* xprev,
                    double cp, double alpha, double beta, double* out, cudaStream_t s);
 //  resid: out = f - A xg; optional dot r.r into dots[0]
-void launch_resid(const Csr& A, const Tiles& T, const double* xg, const double* f, double* out, double* dot_rr,
+void launch_resid(const SpOp& op, const double* xg, const double* f, double* out, double* dot_rr,
                   const DotScratch& ds, cudaStream_t s);
 //  spmv with dots: q = A d; *dot_dq = d.q, *dot_dr = d.rho
-void launch_spmv_dots(const Csr& A, const Tiles& T, const double* d, const double* rho, double* q, double* dot_dq,
+void launch_spmv_dots(const SpOp& op, const double* d, const double* rho, double* q, double* dot_dq,
                       double* dot_dr, const DotScratch& ds, cudaStream_t s);
 
 // restriction rH[I] = sum_{t in [aptr[I], aptr[I+1])} r[perm[t]]  (sequential per aggregate)

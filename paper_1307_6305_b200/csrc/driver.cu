@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -82,6 +84,8 @@ static void poly_coeffs(double l1, double kappa, int m, double* a, double* b) {
 struct Level {
     Csr A;
     Tiles T;
+    Sell S;
+    SpOp op;  // the format the SpMV-class kernels use on this level
     double lambda1 = 0, kappa = 0;
     double alpha[kMaxDeg + 1] = {}, beta[kMaxDeg + 1] = {};
     int nc = 0;
@@ -185,6 +189,9 @@ static void release(amg_hierarchy* h) {
             dfree(h->lev[l].A.ci, h->s);
             dfree(h->lev[l].A.v, h->s);
             dfree(h->lev[l].T.row, h->s);
+            dfree(h->lev[l].S.sptr, h->s);
+            dfree(h->lev[l].S.col, h->s);
+            dfree(h->lev[l].S.val, h->s);
         }
         for (void* p : h->allocs) dfree(p, h->s);
         for (void* p : h->ws_allocs) dfree(p, h->s);
@@ -200,9 +207,29 @@ static void release(amg_hierarchy* h) {
 }
 
 // ------------------------------------------------------------------ setup
+// AMG_SETUP_TRACE=1 prints a wall-clock phase breakdown (each phase ends in a stream sync).
+struct PhaseTimer {
+    bool on;
+    cudaStream_t s;
+    double t0;
+    PhaseTimer(cudaStream_t st) : on(getenv("AMG_SETUP_TRACE") != nullptr), s(st), t0(now()) {}
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    }
+    void mark(const char* what, int l = -1) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        double t = now();
+        fprintf(stderr, "[amg setup] %-22s level %2d  %8.3f ms\n", what, l, t - t0);
+        t0 = t;
+    }
+};
 static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int32_t* ci_in, const double* v_in,
                   const double* d_in) {
     cudaStream_t s = h->s;
+    PhaseTimer pt(s);
     if (n64 < 1 || n64 >= (int64_t(1) << 31) - 8) throw Error(AMG_E_ARG, "n out of range");
     const int n = (int)n64;
     // row_ptr first (to learn nnz)
@@ -220,7 +247,9 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     const int32_t* ci = stage_in(ci_in, (size_t)nnz_in, s, &t_ci);
     const double* v = stage_in(v_in, (size_t)nnz_in, s, &t_v);
     const double* d = stage_in(d_in, (size_t)n, s, &t_d);
+    pt.mark("stage inputs");
     int vf = validate_input(n, rp, ci, v, d, s);
+    pt.mark("validate");
     if (vf) {
         dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
         char buf[128];
@@ -232,6 +261,7 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     h->lev[0].A = form_A0(n, rp, ci, v, d, s);
     dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
     h->n = n;
+    pt.mark("form A0");
 
     const int m = h->m, p = h->p;
     int l = 0;
@@ -240,9 +270,11 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         Lv.lambda1 = inf_norm(Lv.A, s);
         Lv.kappa = h->opt.kappa > 1.0 ? h->opt.kappa : kappa_rule(m);
         poly_coeffs(Lv.lambda1, Lv.kappa, m, Lv.alpha, Lv.beta);
+        pt.mark("lambda1", l);
         if (Lv.A.n <= h->opt.coarsest_size) break;
         if (l + 1 >= kMaxLevels) throw Error(AMG_E_SETUP, "too many levels");
         PassGraph G = pass_graph0(Lv.A, s);
+        pt.mark("pass graph 0", l);
         int* agg = nullptr;
         int nc = Lv.A.n;
         for (int t = 0; t < p; ++t) {
@@ -250,10 +282,12 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
             int* agg_t = dalloc<int>((size_t)G.n + 8, s);
             int nct = 0;
             aggregate_pass(G, salt, agg_t, &nct, &Lv.rounds[t], s);
+            pt.mark("matching pass", l);
             if (t + 1 < p) {
                 PassGraph G2 = quotient_graph(G, agg_t, nct, s);
                 free_graph(G, s);
                 G = G2;
+                pt.mark("quotient graph", l);
             }
             if (t == 0) {
                 agg = agg_t;
@@ -274,7 +308,9 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         Lv.perm = halloc<int>(h, Lv.A.n);
         Lv.aptr = halloc<int>(h, (size_t)nc + 1);
         aggregate_order(Lv.A.n, agg, nc, Lv.perm, Lv.aptr, s);
+        pt.mark("aggregate order", l);
         h->lev[l + 1].A = galerkin(Lv.A, agg, nc, s);
+        pt.mark("galerkin", l);
         ++l;
     }
     h->L = l + 1;
@@ -283,9 +319,20 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     const double shift = C.lambda1 > 0.0 ? C.lambda1 : 1.0;
     h->Minv = coarse_inverse(C.A, h->singular, shift, s);
     h->allocs.push_back(h->Minv);
+    pt.mark("coarse inverse", h->L - 1);
     // tiles of every level the SpMV-class kernels run on (all but the coarsest; level 0 always)
-    for (int k = 0; k < h->L; ++k)
-        if (k < h->L - 1 || k == 0) h->lev[k].T = build_tiles(h->lev[k].A, 0, s);
+    for (int k = 0; k < h->L; ++k) {
+        Level& Lv = h->lev[k];
+        if (k < h->L - 1 || k == 0) {
+            Lv.T = build_tiles(Lv.A, 0, s);
+            if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
+        }
+        Lv.op.A = Lv.A;
+        Lv.op.T = Lv.T;
+        Lv.op.S = Lv.S;
+        Lv.op.sell = Lv.S.col != nullptr;
+    }
+    pt.mark("tiles");
     // level workspaces
     for (int k = 0; k < h->L; ++k) {
         Level& Lv = h->lev[k];
@@ -316,6 +363,7 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     CK(cudaMemsetAsync(h->ds.ticket, 0, 4 * sizeof(unsigned), s));
     CK(cudaMallocHost(&h->hsc, 8 * sizeof(double)));
     CK(cudaStreamSynchronize(s));
+    pt.mark("workspaces");
 }
 
 static void ensure_inner_ws(amg_hierarchy* h, int nu) {
@@ -359,7 +407,7 @@ static void fcg_inner(amg_hierarchy* h, int l, int nu) {
             launch_multidot(n, Lv.Z, Qp, i, c, h->ds, s);
             launch_direction(n, Lv.Z, Dp, c, dq, i, Di, s);
         }
-        launch_spmv_dots(Lv.A, Lv.T, Di, rho, Qi, dq + i, dr + i, h->ds, s);  // q = A d, d.q, d.rho
+        launch_spmv_dots(Lv.op, Di, rho, Qi, dq + i, dr + i, h->ds, s);  // q = A d, d.q, d.rho
         launch_fcg_update(n, dr + i, dq + i, Di, Qi, Lv.E, i == 0, (i < nu - 1) ? rho : nullptr, nullptr, nullptr,
                           h->ds, s);
     }
@@ -381,18 +429,18 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     // pre-smoothing S(r, 0): step 0 is free (x_1 = b0 r implicit)
     double* cur = Lv.X;
     double* prev = Lv.XA;
-    launch_smooth(Lv.A, Lv.T, rin, b[0], rin, nullptr, 0.0, a[1], b[1], Lv.X, s);  // k = 1 (x_0 = 0)
+    launch_smooth(Lv.op, rin, b[0], rin, nullptr, 0.0, a[1], b[1], Lv.X, s);  // k = 1 (x_0 = 0)
     if (m >= 2) {
-        launch_smooth(Lv.A, Lv.T, Lv.X, 1.0, rin, nullptr, b[0], a[2], b[2], Lv.XA, s);  // k = 2 (x_1 = b0 r)
+        launch_smooth(Lv.op, Lv.X, 1.0, rin, nullptr, b[0], a[2], b[2], Lv.XA, s);  // k = 2 (x_1 = b0 r)
         cur = Lv.XA;
         prev = Lv.X;
         for (int k = 3; k <= m; ++k) {
-            launch_smooth(Lv.A, Lv.T, cur, 1.0, rin, prev, 0.0, a[k], b[k], prev, s);
+            launch_smooth(Lv.op, cur, 1.0, rin, prev, 0.0, a[k], b[k], prev, s);
             std::swap(cur, prev);
         }
     }
     // residual + restriction
-    launch_resid(Lv.A, Lv.T, cur, rin, Lv.RES, nullptr, h->ds, s);
+    launch_resid(Lv.op, cur, rin, Lv.RES, nullptr, h->ds, s);
     Level& C = h->lev[l + 1];
     launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO, s);
     // coarse correction (A12: exact solve when the next level is the coarsest)
@@ -403,14 +451,14 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     launch_prolong(Lv.A.n, Lv.agg, C.E, cur, s);
     // post-smoothing S(r, x): x_{-1} = x_0 = cur
     double* other = (cur == Lv.X) ? Lv.XA : Lv.X;
-    launch_smooth(Lv.A, Lv.T, cur, 1.0, rin, cur, 0.0, 1.0, b[0], other, s);  // k = 0
+    launch_smooth(Lv.op, cur, 1.0, rin, cur, 0.0, 1.0, b[0], other, s);  // k = 0
     prev = cur;
     cur = other;
     const bool prof = (l == 0 && h->prof_on);
     if (prof) record_event(h->pe0, s);
     for (int k = 1; k <= m; ++k) {
         double* target = (k == m) ? out : prev;
-        launch_smooth(Lv.A, Lv.T, cur, 1.0, rin, prev, 0.0, a[k], b[k], target, s);
+        launch_smooth(Lv.op, cur, 1.0, rin, prev, 0.0, a[k], b[k], target, s);
         prev = cur;
         cur = target;
     }
@@ -442,7 +490,7 @@ static void outer_iteration(amg_hierarchy* h, int pos, int nu) {
         launch_multidot(n, h->Z, Qs, pos, c, h->ds, s);
         launch_direction(n, h->Z, Ds, c, dq, pos, Dp, s);
     }
-    launch_spmv_dots(h->lev[0].A, h->lev[0].T, Dp, h->r, Qp, dq + pos, dr, h->ds, s);
+    launch_spmv_dots(h->lev[0].op, Dp, h->r, Qp, dq + pos, dr, h->ds, s);
     launch_fcg_update(n, dr, dq + pos, Dp, Qp, h->x, false, h->r, rr, h->flag, h->ds, s);
 }
 
@@ -490,7 +538,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     double* rr = h->osc + 2 * kMaxWin + 1;
     if (h->singular) launch_mean_project(n, h->b, h->osc + 2 * kMaxWin + 3, h->ds, s);  // S:449, A16
     launch_dot(n, h->b, h->b, bb, h->ds, s);
-    launch_resid(h->lev[0].A, h->lev[0].T, h->x, h->b, h->r, rr, h->ds, s);
+    launch_resid(h->lev[0].op, h->x, h->b, h->r, rr, h->ds, s);
     CK(cudaMemsetAsync(h->flag, 0, sizeof(int), s));
     CK(cudaMemcpyAsync(h->hsc, rr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -533,7 +581,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     }
     // true residual ||b - A x|| (reported) and the solution back to the caller
     double* rt = h->osc + 2 * kMaxWin + 6;
-    launch_resid(h->lev[0].A, h->lev[0].T, h->x, h->b, h->Z, rt, h->ds, s);
+    launch_resid(h->lev[0].op, h->x, h->b, h->Z, rt, h->ds, s);
     copy_out(x_out, h->x, sizeof(double) * n, s);
     CK(cudaEventRecord(h->e1, s));
     CK(cudaMemcpyAsync(h->hsc + 3, rt, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -595,6 +643,14 @@ int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t*
     amg_hierarchy* h = new amg_hierarchy();
     try {
         init_device_props();
+        {   // keep freed stream-ordered memory in the pool (default threshold 0 unmaps it at every sync)
+            int dev = 0;
+            cudaMemPool_t pool;
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+            uint64_t thr = UINT64_MAX;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         h->opt = o;
         h->m = poly_degree;
         h->p = n_match_passes;
@@ -733,12 +789,12 @@ int amg_level_smooth(amg_handle h, int32_t level, const double* f, const double*
         // S(f, x0): x_{-1} = x_0
         double* cur = Lv.X;
         double* other = Lv.XA;
-        launch_smooth(Lv.A, Lv.T, cur, 1.0, F, cur, 0.0, 1.0, Lv.beta[0], other, s);
+        launch_smooth(Lv.op, cur, 1.0, F, cur, 0.0, 1.0, Lv.beta[0], other, s);
         double* prev = cur;
         cur = other;
         for (int k = 1; k <= h->m; ++k) {
             double* target = (k == h->m) ? O : prev;
-            launch_smooth(Lv.A, Lv.T, cur, 1.0, F, prev, 0.0, Lv.alpha[k], Lv.beta[k], target, s);
+            launch_smooth(Lv.op, cur, 1.0, F, prev, 0.0, Lv.alpha[k], Lv.beta[k], target, s);
             prev = cur;
             cur = target;
         }

@@ -31,12 +31,19 @@ static int grid_for(int64_t n) {
     return (int)g;
 }
 
+// persistent pinned host scratch (one per host thread) for the few scalars setup reads back
+static void* pinned_scratch() {
+    static thread_local void* p = nullptr;
+    if (!p) CK(cudaMallocHost(&p, 256));
+    return p;
+}
+
 template <class T>
 static T read_scalar(const T* dptr, cudaStream_t s) {
-    T h;
-    CK(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    T* h = static_cast<T*>(pinned_scratch());
+    CK(cudaMemcpyAsync(h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    return h;
+    return *h;
 }
 
 static int bits_for(int64_t x) {  // smallest b >= 1 with 2^b >= x
@@ -349,26 +356,30 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* 
     const int n = G.n;
     int* mate = dalloc<int>(n, s);
     int* prop = dalloc<int>(n, s);
-    int* any = dalloc<int>(1, s);
-    int* hany = nullptr;
-    CK(cudaMallocHost(&hany, sizeof(int)));
+    int* any = dalloc<int>(4, s);
+    int* hany = static_cast<int*>(pinned_scratch()) + 16;
     CK(cudaMemsetAsync(mate, 0xff, sizeof(int) * (size_t)n, s));
     int r = 0;
     const int g = grid_for(n);
+    // Rounds are issued in batches of 3 and only the last round's "some vertex proposed" flag is
+    // read back: a round without proposals means the matching is maximal, and further rounds are
+    // no-ops, so the result does not depend on the batch size.
+    constexpr int kBatch = 3;
     for (;;) {
-        CK(cudaMemsetAsync(any, 0, sizeof(int), s));
-        k_propose<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, prop, salt, any);
-        ++g_launches;
-        k_accept<<<g, kBlock, 0, s>>>(n, mate, prop);
-        ++g_launches;
+        for (int k = 0; k < kBatch; ++k) {
+            CK(cudaMemsetAsync(any, 0, sizeof(int), s));
+            k_propose<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, prop, salt, any);
+            ++g_launches;
+            k_accept<<<g, kBlock, 0, s>>>(n, mate, prop);
+            ++g_launches;
+        }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(hany, any, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        r += kBatch;
         if (!*hany) break;
-        ++r;
-        if (r > 10000) throw Error(-7, "matching did not terminate");
+        if (r > 30000) throw Error(-7, "matching did not terminate");
     }
-    CK(cudaFreeHost(hany));
     int* leader = prop;  // reuse
     int* isl = dalloc<int>((size_t)n + 1, s);
     CK(cudaMemsetAsync(isl + n, 0, sizeof(int), s));
@@ -622,6 +633,62 @@ Tiles build_tiles(const Csr& A, int grid_per_sm, cudaStream_t s) {
     dfree(pos, s);
     T.grid = tiled_grid(T.cap, T.ntiles);
     return T;
+}
+
+// ------------------------------------------------------------------ SELL-32
+__global__ void k_sell_width(int n, int nslices, const int* __restrict__ rp, int* __restrict__ width) {
+    for (int sl = blockIdx.x * blockDim.x + threadIdx.x; sl < nslices; sl += gridDim.x * blockDim.x) {
+        int w = 0;
+        const int i1 = min(n, sl * 32 + 32);
+        for (int i = sl * 32; i < i1; ++i) w = max(w, rp[i + 1] - rp[i]);
+        width[sl] = w;
+    }
+}
+
+__global__ void k_sell_fill(int n, int nslices, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const int* __restrict__ sptr, int* __restrict__ scol,
+                            double* __restrict__ sval) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nslices * 32;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int sl = (int)(t >> 5), lane = (int)(t & 31);
+        const int i = sl * 32 + lane;
+        const int w = sptr[sl + 1] - sptr[sl];
+        const int64_t base = (int64_t)sptr[sl] * 32 + lane;
+        const int p0 = i < n ? rp[i] : 0;
+        const int len = i < n ? rp[i + 1] - p0 : 0;
+        for (int j = 0; j < w; ++j) {
+            const bool real = j < len;
+            scol[base + (int64_t)j * 32] = real ? ci[p0 + j] : (i < n ? i : 0);
+            sval[base + (int64_t)j * 32] = real ? v[p0 + j] : 0.0;
+        }
+    }
+}
+
+Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s) {
+    Sell S;
+    S.n = A.n;
+    S.nslices = (A.n + 31) / 32;
+    int* width = dalloc<int>((size_t)S.nslices + 1, s);
+    CK(cudaMemsetAsync(width + S.nslices, 0, sizeof(int), s));
+    k_sell_width<<<grid_for(S.nslices), kBlock, 0, s>>>(A.n, S.nslices, A.rp, width);
+    CK(cudaGetLastError());
+    ++g_launches;
+    int* sptr = dalloc<int>((size_t)S.nslices + 1, s);
+    const int64_t units = exclusive_scan_total(width, sptr, S.nslices, s);
+    dfree(width, s);
+    S.padded = units * 32;
+    if ((double)S.padded > max_pad_ratio * (double)A.nnz + 64.0) {  // too irregular: keep CSR tiles
+        dfree(sptr, s);
+        return Sell{};
+    }
+    S.sptr = sptr;
+    S.col = dalloc<int>((size_t)S.padded + 32, s);
+    S.val = dalloc<double>((size_t)S.padded + 32, s);
+    k_sell_fill<<<grid_for((int64_t)S.nslices * 32), kBlock, 0, s>>>(A.n, S.nslices, A.rp, A.ci, A.v, sptr, S.col,
+                                                                      S.val);
+    CK(cudaGetLastError());
+    ++g_launches;
+    return S;
 }
 
 // ------------------------------------------------------------------ coarsest (a7)

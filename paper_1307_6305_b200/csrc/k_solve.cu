@@ -97,25 +97,42 @@ __device__ void finalize_dots(double (&acc)[ND], double* partials, unsigned* tic
 }
 
 // ------------------------------------------------------------------ epilogues
+// Each epilogue splits into load(i) -- the row's vector operands, issued BEFORE the matrix stream
+// and the dependent x gathers so their DRAM latency overlaps -- and store(i, s, x_i, pre, acc).
+// The read-only streaming loads (.nc, no L1 allocate) are safe even when `out` aliases `xprev`:
+// every element is read and then written by the same thread only.
+__device__ __forceinline__ double ld_nc(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+
 struct EpiSmooth {  // three-term recurrence step, optional implicit x_{k-1} = cp*f
     const double* f;
     const double* xprev;
     double* out;
     double alpha, beta, cg, cp;
     static constexpr int ND = 0;
-    __device__ __forceinline__ void operator()(int i, double s, double xgi, double*) const {
-        double fi = f[i];
-        double prev = xprev ? xprev[i] : cp * fi;
-        out[i] = alpha * (cg * xgi) + (1.0 - alpha) * prev + beta * (fi - cg * s);
+    struct Pre { double fi, prev; };
+    __device__ __forceinline__ Pre load(int i) const {
+        Pre p;
+        p.fi = ld_nc(f + i);
+        p.prev = xprev ? ld_nc(xprev + i) : cp * p.fi;
+        return p;
+    }
+    __device__ __forceinline__ void store(int i, double s, double xgi, const Pre& p, double*) const {
+        out[i] = alpha * (cg * xgi) + (1.0 - alpha) * p.prev + beta * (p.fi - cg * s);
     }
 };
 
-struct EpiResid {  // out = f - A x; acc[0] += out^2 (used only when a dot pointer is given)
+struct EpiResid {  // out = f - A x; acc[0] += out^2 (reduced only when a dot pointer is given)
     const double* f;
     double* out;
     static constexpr int ND = 1;
-    __device__ __forceinline__ void operator()(int i, double s, double, double* acc) const {
-        double r = f[i] - s;
+    struct Pre { double fi; };
+    __device__ __forceinline__ Pre load(int i) const { return Pre{ld_nc(f + i)}; }
+    __device__ __forceinline__ void store(int i, double s, double, const Pre& p, double* acc) const {
+        double r = p.fi - s;
         out[i] = r;
         acc[0] += r * r;
     }
@@ -125,10 +142,12 @@ struct EpiSpmvDots {  // q = A d; acc = (d.q, d.rho)
     const double* rho;
     double* q;
     static constexpr int ND = 2;
-    __device__ __forceinline__ void operator()(int i, double s, double di, double* acc) const {
+    struct Pre { double ri; };
+    __device__ __forceinline__ Pre load(int i) const { return Pre{ld_nc(rho + i)}; }
+    __device__ __forceinline__ void store(int i, double s, double di, const Pre& p, double* acc) const {
         q[i] = s;
         acc[0] += di * s;
-        acc[1] += di * rho[i];
+        acc[1] += di * p.ri;
     }
 };
 
@@ -165,76 +184,206 @@ __global__ void __launch_bounds__(kBlock) k_tiled(Csr A, const double* __restric
             for (int k = threadIdx.x; k < nc4; k += kBlock) sc4[k] = ld_stream(gc + k);
             __syncthreads();
             for (int i = r0 + threadIdx.x; i < r1; i += kBlock) {
+                const typename Epi::Pre pre = epi.load(i);
+                const double xi = __ldg(xg + i);
                 const int q0 = rp[i], q1 = rp[i + 1];
                 double s = 0.0;
                 for (int q = q0; q < q1; ++q) s = fma(sv[q - a0], __ldg(xg + sc[q - c0]), s);
-                epi(i, s, __ldg(xg + i), acc);
+                epi.store(i, s, xi, pre, acc);
             }
             __syncthreads();
         } else {  // single long row: block-wide reduction straight from global memory
             double s = 0.0;
             for (int q = p0 + threadIdx.x; q < p1; q += kBlock) s = fma(va[q], __ldg(xg + ci[q]), s);
             s = block_sum(s);
-            if (threadIdx.x == 0) epi(r0, s, __ldg(xg + r0), acc);
+            if (threadIdx.x == 0) epi.store(r0, s, __ldg(xg + r0), epi.load(r0), acc);
             __syncthreads();
         }
     }
     if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
 }
 
+// ------------------------------------------------------------------ SELL-32 kernel
+// Warp per 32-row slice, grid-stride over slices.  Lane l owns row 32 s + l; entry j of the slice
+// lives at 32 (sptr[s] + j) + l, so every load instruction of the warp is one contiguous 256-byte
+// (values) or 128-byte (columns) run: fully coalesced, no shared memory, no block barriers.  All
+// column/value loads of an 8-entry chunk are issued before the dependent x gathers.
+__device__ __forceinline__ int ld_stream_i(const int* p) {
+    int r;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double ld_stream_d(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+// read-only gather through L1 (x of the SpMV: neighbours share lines); volatile so that the
+// source order -- all column/value loads of a chunk, then all gathers -- is the issue order
+__device__ __forceinline__ double ld_gather(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+
+// Straight-line row reduction for a fixed slice width W: all W column and value loads, then all W
+// gathers, then the FMA chain (CSR order).  No predication, so ptxas keeps the loads hoisted.
+template <int W>
+__device__ __forceinline__ double sell_row(const int* __restrict__ cp, const double* __restrict__ vp,
+                                           const double* __restrict__ xg) {
+    int c[W];
+    double v[W], x[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+        c[u] = ld_stream_i(cp + u * 32);
+        v[u] = ld_stream_d(vp + u * 32);
+    }
+#pragma unroll
+    for (int u = 0; u < W; ++u) x[u] = ld_gather(xg + c[u]);
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < W; ++u) s = fma(v[u], x[u], s);
+    return s;
+}
+
+// generic width: chunks of 8 entries, then the remainder
+__device__ __noinline__ double sell_row_any(const int* __restrict__ cp, const double* __restrict__ vp,
+                                            const double* __restrict__ xg, int w) {
+    double s = 0.0;
+    int j = 0;
+    for (; j + 8 <= w; j += 8) {
+        int c[8];
+        double v[8], x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            c[u] = ld_stream_i(cp + (j + u) * 32);
+            v[u] = ld_stream_d(vp + (j + u) * 32);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = ld_gather(xg + c[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = fma(v[u], x[u], s);
+    }
+    for (; j < w; ++j) s = fma(ld_stream_d(vp + j * 32), ld_gather(xg + ld_stream_i(cp + j * 32)), s);
+    return s;
+}
+
+template <class Epi, bool DOTS>
+__global__ void __launch_bounds__(kBlock) k_sell(Sell S, const double* __restrict__ xg, Epi epi, double* partials,
+                                                 unsigned* ticket, DotOut dot_out) {
+    double acc[Epi::ND > 0 ? Epi::ND : 1];
+#pragma unroll
+    for (int k = 0; k < (Epi::ND > 0 ? Epi::ND : 1); ++k) acc[k] = 0.0;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < S.nslices; sl += nwarps) {
+        const int b = __ldg(S.sptr + sl), e = __ldg(S.sptr + sl + 1);
+        const int* __restrict__ cp = S.col + (size_t)b * 32 + lane;
+        const double* __restrict__ vp = S.val + (size_t)b * 32 + lane;
+        const int i = sl * 32 + lane;
+        const int w = e - b;  // warp-uniform
+        const bool act = i < S.n;
+        typename Epi::Pre pre{};
+        double xi = 0.0;
+        if (act) {  // independent row operands first (their latency overlaps the matrix stream)
+            pre = epi.load(i);
+            xi = ld_gather(xg + i);
+        }
+        double sum;
+        switch (w) {
+            case 0: sum = 0.0; break;
+            case 1: sum = sell_row<1>(cp, vp, xg); break;
+            case 2: sum = sell_row<2>(cp, vp, xg); break;
+            case 3: sum = sell_row<3>(cp, vp, xg); break;
+            case 4: sum = sell_row<4>(cp, vp, xg); break;
+            case 5: sum = sell_row<5>(cp, vp, xg); break;
+            case 6: sum = sell_row<6>(cp, vp, xg); break;
+            case 7: sum = sell_row<7>(cp, vp, xg); break;
+            case 8: sum = sell_row<8>(cp, vp, xg); break;
+            case 9: sum = sell_row<9>(cp, vp, xg); break;
+            case 10: sum = sell_row<10>(cp, vp, xg); break;
+            case 11: sum = sell_row<11>(cp, vp, xg); break;
+            case 12: sum = sell_row<12>(cp, vp, xg); break;
+            default: sum = sell_row_any(cp, vp, xg, w); break;
+        }
+        if (act) epi.store(i, sum, xi, pre, acc);
+    }
+    if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
+}
+
+// resident grid of one kernel instance (cached per instance and dynamic smem size)
+template <class K>
+static int resident_grid(K kernel, size_t smem) {
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kBlock, smem));
+    return g_num_sms * (bps < 1 ? 1 : bps);
+}
+
 static size_t tile_smem(const Tiles& T) { return (size_t)(T.cap + 2) * sizeof(double) + (size_t)(T.cap + 4) * sizeof(int); }
 
 template <class Epi, bool DOTS>
-static void configure_tiled() {
+static int tiled_resident(int cap) {
     static bool configured = false;  // per template instance
+    static int cached_cap = -1, cached = 0;
     if (!configured) {
         CK(cudaFuncSetAttribute(k_tiled<Epi, DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
+    if (cap != cached_cap) {
+        cached = resident_grid(k_tiled<Epi, DOTS>, (size_t)(cap + 2) * sizeof(double) + (size_t)(cap + 4) * sizeof(int));
+        cached_cap = cap;
+    }
+    return cached;
 }
 
 int tiled_grid(int cap, int ntiles) {
-    configure_tiled<EpiSmooth, false>();
-    const size_t sm = (size_t)(cap + 2) * sizeof(double) + (size_t)(cap + 4) * sizeof(int);
-    int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_tiled<EpiSmooth, false>, kBlock, sm));
-    if (bps < 1) bps = 1;
-    int g = g_num_sms * bps;
+    int g = tiled_resident<EpiSmooth, false>(cap);
     if (g > ntiles) g = ntiles;
-    if (g < 1) g = 1;
-    return g;
+    return g < 1 ? 1 : g;
 }
 
 template <class Epi, bool DOTS>
-static void launch_tiled(const Csr& A, const Tiles& T, const double* xg, const Epi& epi, const DotScratch* ds,
-                         DotOut dot_out, cudaStream_t s) {
-    size_t sm = tile_smem(T);
-    configure_tiled<Epi, DOTS>();
-    k_tiled<Epi, DOTS><<<T.grid, kBlock, sm, s>>>(A, xg, T.row, T.ntiles, T.cap, epi, ds ? ds->partials : nullptr,
-                                                   ds ? ds->ticket : nullptr, dot_out);
+static void launch_op(const SpOp& op, const double* xg, const Epi& epi, const DotScratch* ds, DotOut dot_out,
+                      cudaStream_t s) {
+    double* part = ds ? ds->partials : nullptr;
+    unsigned* tk = ds ? ds->ticket : nullptr;
+    if (op.sell) {
+        static int res = 0;
+        if (!res) res = resident_grid(k_sell<Epi, DOTS>, 0);
+        int need = (op.S.nslices + (kBlock / 32) - 1) / (kBlock / 32);
+        int g = need < res ? need : res;
+        if (g < 1) g = 1;
+        k_sell<Epi, DOTS><<<g, kBlock, 0, s>>>(op.S, xg, epi, part, tk, dot_out);
+    } else {
+        int g = tiled_resident<Epi, DOTS>(op.T.cap);
+        if (g > op.T.ntiles) g = op.T.ntiles;
+        if (g < 1) g = 1;
+        k_tiled<Epi, DOTS><<<g, kBlock, tile_smem(op.T), s>>>(op.A, xg, op.T.row, op.T.ntiles, op.T.cap, epi, part, tk,
+                                                              dot_out);
+    }
     CK(cudaGetLastError());
     ++g_launches;
 }
 
-void launch_smooth(const Csr& A, const Tiles& T, const double* xg, double cg, const double* f, const double* xprev,
-                   double cp, double alpha, double beta, double* out, cudaStream_t s) {
+void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f, const double* xprev, double cp,
+                   double alpha, double beta, double* out, cudaStream_t s) {
     EpiSmooth e{f, xprev, out, alpha, beta, cg, cp};
-    launch_tiled<EpiSmooth, false>(A, T, xg, e, nullptr, DotOut{}, s);
+    launch_op<EpiSmooth, false>(op, xg, e, nullptr, DotOut{}, s);
 }
 
-void launch_resid(const Csr& A, const Tiles& T, const double* xg, const double* f, double* out, double* dot_rr,
-                  const DotScratch& ds, cudaStream_t s) {
+void launch_resid(const SpOp& op, const double* xg, const double* f, double* out, double* dot_rr, const DotScratch& ds,
+                  cudaStream_t s) {
     EpiResid e{f, out};
     if (dot_rr)
-        launch_tiled<EpiResid, true>(A, T, xg, e, &ds, DotOut{{dot_rr}}, s);
+        launch_op<EpiResid, true>(op, xg, e, &ds, DotOut{{dot_rr}}, s);
     else
-        launch_tiled<EpiResid, false>(A, T, xg, e, nullptr, DotOut{}, s);
+        launch_op<EpiResid, false>(op, xg, e, nullptr, DotOut{}, s);
 }
 
-void launch_spmv_dots(const Csr& A, const Tiles& T, const double* d, const double* rho, double* q, double* dot_dq,
-                      double* dot_dr, const DotScratch& ds, cudaStream_t s) {
+void launch_spmv_dots(const SpOp& op, const double* d, const double* rho, double* q, double* dot_dq, double* dot_dr,
+                      const DotScratch& ds, cudaStream_t s) {
     EpiSpmvDots e{rho, q};
-    launch_tiled<EpiSpmvDots, true>(A, T, d, e, &ds, DotOut{{dot_dq, dot_dr}}, s);
+    launch_op<EpiSpmvDots, true>(op, d, e, &ds, DotOut{{dot_dq, dot_dr}}, s);
 }
 
 // ------------------------------------------------------------------ transfers
