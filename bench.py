@@ -64,6 +64,8 @@ class Clocks:
     def __init__(self, gpu_index: int):
         self.p = None
         self.idx = gpu_index
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                        "-i", str(gpu_index), "-lms", "200"], stdout=subprocess.PIPE,

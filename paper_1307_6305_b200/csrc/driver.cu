@@ -195,8 +195,7 @@ static void release(amg_hierarchy* h) {
         }
         for (void* p : h->allocs) dfree(p, h->s);
         for (void* p : h->ws_allocs) dfree(p, h->s);
-        cudaStreamSynchronize(h->s);
-        cudaStreamDestroy(h->s);
+        cudaStreamSynchronize(h->s);  // the stream itself is the thread's persistent library stream
     }
     if (h->hsc) cudaFreeHost(h->hsc);
     if (h->e0) cudaEventDestroy(h->e0);
@@ -655,7 +654,17 @@ int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t*
         h->m = poly_degree;
         h->p = n_match_passes;
         h->user = (cudaStream_t)o.stream;
-        CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+        // One persistent non-blocking stream per host thread and device, shared by that thread's
+        // handles: memory a handle frees (stream-ordered) is then always reusable by the next
+        // setup without growing the pool (blocks freed on destroyed streams are not reliably reused).
+        {
+            static thread_local cudaStream_t streams[64] = {};
+            int dev = 0;
+            CK(cudaGetDevice(&dev));
+            if (dev < 0 || dev >= 64) throw Error(AMG_E_ARG, "device ordinal out of range");
+            if (!streams[dev]) CK(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+            h->s = streams[dev];
+        }
         CK(cudaEventCreate(&h->e0));
         CK(cudaEventCreate(&h->e1));
         CK(cudaEventCreate(&h->pe0));

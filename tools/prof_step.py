@@ -16,6 +16,7 @@ ap.add_argument("--max-iter", type=int, default=500)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--no-graphs", action="store_true")
 ap.add_argument("--size", type=int, default=None)
+ap.add_argument("--user-stream", action="store_true")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -29,6 +30,8 @@ arrs = [torch.from_numpy(x).to(dev) if x is not None else None for x in (p.rp, p
 b = torch.from_numpy(gen.rhs(p.n, prm["seed"])).to(dev)
 x = torch.zeros(p.n, dtype=torch.float64, device=dev)
 o = amg.amg_options_default(coarsest_size=prm["coarsest_size"], max_iter=a.max_iter, use_graphs=0 if a.no_graphs else 1)
+if a.user_stream:
+    o.stream = torch.cuda.current_stream(dev).cuda_stream
 for r in range(a.reps):
     t0 = time.perf_counter()
     h = amg.amg_setup(*arrs, prm["passes"], prm["degree"], o)
