@@ -254,7 +254,7 @@ def _dense(p):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["C3"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
 def test_full_size_hierarchy_and_precond(amg, gen_mod, oracle_mod, name):
     """Full BASELINE size, in the configuration bench.py times: the whole hierarchy bit-exact, one
     B_0(r) within 1e-10, and the solve's iteration count within +-1 of the committed oracle count
