@@ -64,7 +64,10 @@ typedef struct {
     void*    stream;        /* cudaStream_t the caller orders against; NULL = legacy default stream */
     int32_t  use_graphs;    /* 1 = replay each outer iteration as a captured CUDA graph; default 1 */
     int32_t  reserved0;
-    int64_t  reserved[6];
+    int64_t  tail_nnz;      /* the first level l >= 1 with nnz(A_l) <= tail_nnz and every level below it
+                               run inside one single-CTA kernel per visit (coarse-tail megakernel);
+                               0 disables; default 8192 */
+    int64_t  reserved[5];
 } amg_options;
 
 typedef struct {

@@ -23,7 +23,8 @@ EXPORTS = ("amg_options_default", "amg_setup", "amg_solve", "amg_free", "amg_get
 class amg_options(ctypes.Structure):
     _fields_ = [("coarsest_size", ctypes.c_int64), ("kappa", ctypes.c_double), ("restart", ctypes.c_int32),
                 ("max_iter", ctypes.c_int32), ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
-                ("use_graphs", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("reserved", ctypes.c_int64 * 6)]
+                ("use_graphs", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("tail_nnz", ctypes.c_int64),
+                ("reserved", ctypes.c_int64 * 5)]
 
 
 class amg_info(ctypes.Structure):

@@ -149,6 +149,38 @@ void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cu
 void launch_copy(int n, const double* x, double* y, cudaStream_t s);
 // dot = x.y (deterministic)
 void launch_dot(int n, const double* x, const double* y, double* out, const DotScratch& ds, cudaStream_t s);
+// ---------------------------------------------------------------- coarse-tail megakernel (k_tail.cu)
+// Every level l >= l_tail (small levels) is run entirely inside ONE thread-block cluster: the whole
+// recursion B_l (smoothing, residual, restriction, inner FCG, coarsest GEMV, prolongation) with
+// cluster barriers between dependent phases and cluster-wide (DSMEM) deterministic reductions.
+struct TLevel {
+    int n = 0, nc = 0;
+    const int* rp = nullptr;
+    const int* ci = nullptr;
+    const double* v = nullptr;
+    const int* agg = nullptr;
+    const int* perm = nullptr;
+    const int* aptr = nullptr;
+    double alpha[kMaxDeg + 1] = {};
+    double beta[kMaxDeg + 1] = {};
+    double *X = nullptr, *XA = nullptr, *RES = nullptr, *RHO = nullptr, *E = nullptr;
+    double *Z = nullptr, *D = nullptr, *Q = nullptr;
+};
+struct TailArgs {
+    int l0 = 0;       // level the call starts at
+    int L = 0;        // number of levels (L-1 = coarsest)
+    int m = 0, nu = 0;
+    int mode = 0;     // 0: out = B_l0(rin);  1: FCG_inner(l0): lev[l0].RHO -> lev[l0].E
+    const double* Minv = nullptr;
+    const double* rin = nullptr;
+    double* out = nullptr;
+    const TLevel* lev = nullptr;  // device array [L]
+};
+constexpr int kTailMaxNu = 4;  // the tail kernel supports nu <= 4
+// cluster size actually used (16 if the device allows non-portable clusters, else 8)
+int tail_cluster_size();
+void launch_tail(const TailArgs& a, cudaStream_t s);
+
 // grid size used by the vector kernels
 int vector_grid();
 void init_device_props();

@@ -116,6 +116,8 @@ struct amg_hierarchy {
     double* hsc = nullptr;  // pinned host mirror: rr, flag
     DotScratch ds;
     int nu_ws = 0;          // nu the inner workspaces are sized for
+    int l_tail = 0;         // first level run by the coarse-tail cluster kernel (L = none)
+    TLevel* d_tlev = nullptr;  // device copy of the tail level descriptors
     std::vector<cudaGraphExec_t> graphs;
     int graph_nu = 0;
     long long graph_launches = 0;
@@ -361,8 +363,59 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     h->ds.ticket = halloc<unsigned>(h, 4);
     CK(cudaMemsetAsync(h->ds.ticket, 0, 4 * sizeof(unsigned), s));
     CK(cudaMallocHost(&h->hsc, 8 * sizeof(double)));
+    // coarse tail: first level l >= 1 with nnz(A_l) <= tail_nnz (one SM runs it from L1/L2)
+    h->l_tail = h->L;
+    if (h->opt.tail_nnz > 0)
+        for (int k = 1; k < h->L; ++k)
+            if (h->lev[k].A.nnz <= h->opt.tail_nnz) { h->l_tail = k; break; }
+    if (h->l_tail < h->L) {
+        tail_cluster_size();
+        size_t cur = 0;
+        CK(cudaDeviceGetLimit(&cur, cudaLimitStackSize));
+        if (cur < 4096) CK(cudaDeviceSetLimit(cudaLimitStackSize, 4096));  // t_B/t_fcg recursion
+        h->d_tlev = halloc<TLevel>(h, kMaxLevels);
+    }
     CK(cudaStreamSynchronize(s));
     pt.mark("workspaces");
+}
+
+// device descriptors of the tail levels (refreshed whenever the inner workspaces change)
+static void upload_tail_levels(amg_hierarchy* h) {
+    if (!h->d_tlev) return;
+    std::vector<TLevel> t(h->L);
+    for (int k = 0; k < h->L; ++k) {
+        const Level& Lv = h->lev[k];
+        TLevel& d = t[k];
+        d.n = Lv.A.n;
+        d.nc = Lv.nc;
+        d.rp = Lv.A.rp;
+        d.ci = Lv.A.ci;
+        d.v = Lv.A.v;
+        d.agg = Lv.agg;
+        d.perm = Lv.perm;
+        d.aptr = Lv.aptr;
+        for (int j = 0; j <= h->m; ++j) { d.alpha[j] = Lv.alpha[j]; d.beta[j] = Lv.beta[j]; }
+        d.X = Lv.X; d.XA = Lv.XA; d.RES = Lv.RES; d.RHO = Lv.RHO; d.E = Lv.E;
+        d.Z = Lv.Z; d.D = Lv.D; d.Q = Lv.Q;
+    }
+    CK(cudaMemcpyAsync(h->d_tlev, t.data(), sizeof(TLevel) * t.size(), cudaMemcpyHostToDevice, h->s));
+    CK(cudaStreamSynchronize(h->s));
+}
+
+static bool use_tail(const amg_hierarchy* h, int l, int nu) { return l >= h->l_tail && nu <= kTailMaxNu; }
+
+static void tail_call(amg_hierarchy* h, int mode, int l, int nu, const double* rin, double* out) {
+    TailArgs a;
+    a.l0 = l;
+    a.L = h->L;
+    a.m = h->m;
+    a.nu = nu;
+    a.mode = mode;
+    a.Minv = h->Minv;
+    a.rin = rin;
+    a.out = out;
+    a.lev = h->d_tlev;
+    launch_tail(a, h->s);
 }
 
 static void ensure_inner_ws(amg_hierarchy* h, int nu) {
@@ -378,6 +431,7 @@ static void ensure_inner_ws(amg_hierarchy* h, int nu) {
     }
     h->nu_ws = nu;
     destroy_graphs(h);
+    upload_tail_levels(h);
 }
 
 // ------------------------------------------------------------------ solve schedule
@@ -385,6 +439,10 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
 
 // FCG_inner(l, RHO_l, nu) -> E_l
 static void fcg_inner(amg_hierarchy* h, int l, int nu) {
+    if (use_tail(h, l, nu)) {
+        tail_call(h, 1, l, nu, nullptr, nullptr);
+        return;
+    }
     Level& Lv = h->lev[l];
     cudaStream_t s = h->s;
     const int n = Lv.A.n;
@@ -419,6 +477,10 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     cudaStream_t s = h->s;
     if (l == h->L - 1) {
         launch_gemv(h->lev[l].A.n, h->Minv, rin, out, s);
+        return;
+    }
+    if (use_tail(h, l, nu)) {
+        tail_call(h, 0, l, nu, rin, out);
         return;
     }
     Level& Lv = h->lev[l];
@@ -619,6 +681,7 @@ int amg_options_default(amg_options* o) {
     o->seed = 0;
     o->stream = nullptr;
     o->use_graphs = 1;
+    o->tail_nnz = 8192;
     return AMG_OK;
 }
 

@@ -1,0 +1,287 @@
+// k_tail.cu -- coarse-tail megakernel (sm_100a thread-block cluster).
+//
+// The W-shaped k-cycle visits level l 2^l times per outer iteration (
+// SURVEY.md 8(d) "latency floor"), so below a few tens of thousands of rows the cost is launch
+// latency, not bandwidth: C4's 7-level hierarchy issues ~850 dependent launches per outer
+// iteration.  This kernel runs the whole recursion B_l -- and the inner FCG that
+// calls it (O7) -- for every level l >= l_tail inside ONE cluster of 8 or 16 CTAs:
+//   * rows of every pass are spread over all cluster threads;
+//   * dependent phases are separated by cluster.sync() (~0.2 us, vs ~4 us per graph launch);
+//   * FCG dots are deterministic: fixed-order warp/block reductions, then every CTA sums the CTAs'
+//     partials in rank order through distributed shared memory (DSMEM);
+//   * all vectors and matrices of these levels are L2-resident; only coherent loads are used
+//     (data written inside the kernel is re-read after the barrier).
+// The arithmetic is the same three-term recurrence / residual / restriction / FCG as k_solve.cu.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "amg_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace amg {
+
+constexpr int kTailBlock = 1024;
+
+struct TCtx {
+    int t;  // cluster-wide thread id
+    int T;  // cluster-wide thread count
+};
+
+// barrier between dependent phases: a CTA barrier when the tail runs in one CTA (data stays in
+// that SM's L1), a cluster barrier (release/acquire, flushes L1) when it spans a cluster
+template <bool CL>
+__device__ __forceinline__ void csync() {
+    if constexpr (CL) cg::this_cluster().sync(); else __syncthreads();
+}
+
+__device__ __forceinline__ double t_warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Cluster-wide sums of k values (k <= kMaxWin); every thread returns the same totals.
+// Deterministic: fixed warp/block order, then CTAs in rank order.
+template <bool CL>
+__device__ void cluster_sums(double* v, int k) {
+    __shared__ double wred[kMaxWin][32];
+    __shared__ double part[kMaxWin];
+    [[maybe_unused]] cg::cluster_group cl = cg::this_cluster();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = 0; j < k; ++j) {
+        double x = t_warp_sum(v[j]);
+        if (lane == 0) wred[j][wid] = x;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        for (int j = 0; j < k; ++j) {
+            double x = lane < nw ? wred[j][lane] : 0.0;
+            x = t_warp_sum(x);
+            if (lane == 0) part[j] = x;
+        }
+    }
+    if constexpr (CL) {
+        cl.sync();  // every CTA's part[] is complete (and previous global writes are visible)
+        const unsigned ncta = cl.num_blocks();
+        for (int j = 0; j < k; ++j) {
+            double s = 0.0;
+            for (unsigned r = 0; r < ncta; ++r) s += *cl.map_shared_rank(&part[j], r);
+            v[j] = s;
+        }
+        cl.sync();  // part[] may be overwritten afterwards
+    } else {
+        __syncthreads();
+        for (int j = 0; j < k; ++j) v[j] = part[j];
+        __syncthreads();
+    }
+}
+
+// one three-term recurrence step on level L:
+// out_i = a*cg*xg_i + (1-a)*prev_i + b*(f_i - cg*(A xg)_i), prev_i = xprev ? xprev_i : cp*f_i
+template <bool CL>
+__device__ void t_step(const TLevel& L, const double* xg, double cgs, const double* f, const double* xprev, double cp,
+                       double a, double b, double* out, TCtx c) {
+    for (int i = c.t; i < L.n; i += c.T) {
+        double s = 0.0;
+        for (int p = L.rp[i]; p < L.rp[i + 1]; ++p) s = fma(L.v[p], xg[L.ci[p]], s);
+        const double fi = f[i];
+        const double prev = xprev ? xprev[i] : cp * fi;
+        out[i] = a * (cgs * xg[i]) + (1.0 - a) * prev + b * (fi - cgs * s);
+    }
+    csync<CL>();
+}
+
+template <bool CL>
+__device__ void t_gemv(int n, const double* M, const double* r, double* e, TCtx c) {
+    for (int i = c.t; i < n; i += c.T) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s = fma(M[(size_t)i * n + j], r[j], s);
+        e[i] = s;
+    }
+    csync<CL>();
+}
+
+template <bool CL>
+__device__ void t_fcg(const TailArgs& A, int l, TCtx c);
+
+// z = B_l(r) -- same schedule as driver.cu apply_B
+template <bool CL>
+__device__ __noinline__ void t_B(const TailArgs& A, int l, const double* r, double* out, TCtx c) {
+    if (l == A.L - 1) {
+        t_gemv<CL>(A.lev[l].n, A.Minv, r, out, c);
+        return;
+    }
+    const TLevel& L = A.lev[l];
+    const int m = A.m;
+    double* cur = L.X;
+    double* prev = L.XA;
+    t_step<CL>(L, r, L.beta[0], r, nullptr, 0.0, L.alpha[1], L.beta[1], L.X, c);  // k = 1 (x_0 = 0)
+    if (m >= 2) {
+        t_step<CL>(L, L.X, 1.0, r, nullptr, L.beta[0], L.alpha[2], L.beta[2], L.XA, c);  // k = 2
+        cur = L.XA;
+        prev = L.X;
+        for (int k = 3; k <= m; ++k) {
+            t_step<CL>(L, cur, 1.0, r, prev, 0.0, L.alpha[k], L.beta[k], prev, c);
+            double* t = cur;
+            cur = prev;
+            prev = t;
+        }
+    }
+    // residual
+    for (int i = c.t; i < L.n; i += c.T) {
+        double s = 0.0;
+        for (int p = L.rp[i]; p < L.rp[i + 1]; ++p) s = fma(L.v[p], cur[L.ci[p]], s);
+        L.RES[i] = r[i] - s;
+    }
+    csync<CL>();
+    // restriction
+    const TLevel& C = A.lev[l + 1];
+    for (int I = c.t; I < L.nc; I += c.T) {
+        double s = 0.0;
+        for (int t = L.aptr[I]; t < L.aptr[I + 1]; ++t) s += L.RES[L.perm[t]];
+        C.RHO[I] = s;
+    }
+    csync<CL>();
+    if (l + 1 == A.L - 1)
+        t_gemv<CL>(C.n, A.Minv, C.RHO, C.E, c);
+    else
+        t_fcg<CL>(A, l + 1, c);
+    // prolongation + axpy
+    for (int i = c.t; i < L.n; i += c.T) cur[i] += C.E[L.agg[i]];
+    csync<CL>();
+    // post-smoothing S(r, x), x_{-1} = x_0
+    double* other = (cur == L.X) ? L.XA : L.X;
+    t_step<CL>(L, cur, 1.0, r, cur, 0.0, 1.0, L.beta[0], other, c);  // k = 0
+    prev = cur;
+    cur = other;
+    for (int k = 1; k <= m; ++k) {
+        double* target = (k == m) ? out : prev;
+        t_step<CL>(L, cur, 1.0, r, prev, 0.0, L.alpha[k], L.beta[k], target, c);
+        prev = cur;
+        cur = target;
+    }
+}
+
+// FCG_inner(l): RHO_l -> E_l with nu iterations
+template <bool CL>
+__device__ __noinline__ void t_fcg(const TailArgs& A, int l, TCtx c) {
+    const TLevel& L = A.lev[l];
+    const int n = L.n, nu = A.nu;
+    double dq[kTailMaxNu];
+    for (int i = 0; i < nu; ++i) {
+        double* Di = L.D + (size_t)i * n;
+        double* Qi = L.Q + (size_t)i * n;
+        if (i == 0) {
+            t_B<CL>(A, l, L.RHO, Di, c);
+        } else {
+            t_B<CL>(A, l, L.RHO, L.Z, c);
+            double cj[kTailMaxNu];
+            for (int j = 0; j < i; ++j) cj[j] = 0.0;
+            for (int r = c.t; r < n; r += c.T) {
+                const double z = L.Z[r];
+                for (int j = 0; j < i; ++j) cj[j] += z * L.Q[(size_t)j * n + r];
+            }
+            cluster_sums<CL>(cj, i);
+            for (int r = c.t; r < n; r += c.T) {
+                double v = L.Z[r];
+                for (int j = 0; j < i; ++j) v -= (cj[j] / dq[j]) * L.D[(size_t)j * n + r];
+                Di[r] = v;
+            }
+            csync<CL>();
+        }
+        double acc[2] = {0.0, 0.0};
+        for (int r = c.t; r < n; r += c.T) {
+            double s = 0.0;
+            for (int p = L.rp[r]; p < L.rp[r + 1]; ++p) s = fma(L.v[p], Di[L.ci[p]], s);
+            Qi[r] = s;
+            acc[0] += Di[r] * s;
+            acc[1] += Di[r] * L.RHO[r];
+        }
+        cluster_sums<CL>(acc, 2);
+        dq[i] = acc[0];
+        const double alpha = acc[0] != 0.0 ? acc[1] / acc[0] : 0.0;  // rho = 0 => d = 0 (A13)
+        for (int r = c.t; r < n; r += c.T) {
+            if (i == 0) L.E[r] = alpha * Di[r]; else L.E[r] += alpha * Di[r];
+            if (i < nu - 1) L.RHO[r] -= alpha * Qi[r];
+        }
+        csync<CL>();
+    }
+}
+
+template <bool CL>
+__global__ void __launch_bounds__(kTailBlock, 1) k_tail(TailArgs a) {
+    TCtx c;
+    if constexpr (CL) {
+        cg::cluster_group cl = cg::this_cluster();
+        c = TCtx{(int)(cl.block_rank() * blockDim.x + threadIdx.x), (int)(cl.num_blocks() * blockDim.x)};
+    } else {
+        c = TCtx{(int)threadIdx.x, (int)blockDim.x};
+    }
+    if (a.mode == 0)
+        t_B<CL>(a, a.l0, a.rin, a.out, c);
+    else
+        t_fcg<CL>(a, a.l0, c);
+}
+
+static int g_tail_cs = 0;
+
+// AMG_TAIL_CLUSTER=<n> selects a cluster of n CTAs (experiments); default 1 = one CTA.
+int tail_cluster_size() {
+    if (g_tail_cs) return g_tail_cs;
+    const char* env = getenv("AMG_TAIL_CLUSTER");
+    int want = env ? atoi(env) : 1;
+    if (want <= 1) {
+        g_tail_cs = 1;
+        return 1;
+    }
+    CK(cudaFuncSetAttribute(k_tail<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (int cs : {16, 8, 4, 2}) {
+        if (cs > want) continue;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kTailBlock);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, k_tail<true>, &cfg) == cudaSuccess && nclusters > 0) {
+            g_tail_cs = cs;
+            break;
+        }
+        cudaGetLastError();
+    }
+    if (!g_tail_cs) g_tail_cs = 1;
+    return g_tail_cs;
+}
+
+void launch_tail(const TailArgs& a, cudaStream_t s) {
+    const int cs = tail_cluster_size();
+    if (cs == 1) {
+        k_tail<false><<<1, kTailBlock, 0, s>>>(a);
+        CK(cudaGetLastError());
+        ++g_launches;
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kTailBlock);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_tail<true>, a));
+    ++g_launches;
+}
+
+}  // namespace amg

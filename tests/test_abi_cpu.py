@@ -61,7 +61,7 @@ int main(void) {{
 def test_defaults_and_argument_errors(amg_mod):
     """Host-only paths: defaults, and argument validation that returns before touching the GPU."""
     o = amg_mod.amg_options_default()
-    assert (o.coarsest_size, o.kappa, o.restart, o.max_iter, o.use_graphs) == (100, 0.0, 5, 500, 1)
+    assert (o.coarsest_size, o.kappa, o.restart, o.max_iter, o.use_graphs, o.tail_nnz) == (100, 0.0, 5, 500, 1, 8192)
     lib = amg_mod.load()
     assert lib.amg_options_default(None) == amg_mod.AMG_E_ARG
     h = ctypes.c_void_p()

@@ -277,3 +277,35 @@ def test_full_size_hierarchy_and_precond(amg, gen_mod, oracle_mod, name):
         assert abs(it - gold[name]["iters"]) <= 1
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("tail_nnz", [0, 8192, 10**9])
+def test_coarse_tail_kernel_parity(amg, gen_mod, oracle_mod, tail_nnz):
+    """The coarse-tail kernel (levels with nnz <= tail_nnz run in one single-CTA launch) and the
+    per-kernel graph path both match the oracle: B_l(r) <= 1e-10 on every level, same iterations."""
+    p = gen_mod.problem("C2", size=160)
+    p.params["coarsest_size"] = 40
+    hier = oracle_mod.setup_problem(p)
+    o = amg.amg_options_default(coarsest_size=40, tail_nnz=tail_nnz)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, p.params["passes"], p.params["degree"], o)
+    rng = np.random.default_rng(3)
+    try:
+        for l in range(hier.nlev):
+            n = hier.level_info(l)["n"]
+            r = rng.uniform(-1, 1, n)
+            z = np.empty(n)
+            amg.amg_level_precond(h, l, 2, r, z)
+            ref = hier.precond(r, nu=2, level=l)
+            assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref), f"B_{l}(r), tail_nnz={tail_nnz}"
+        b = gen_mod.rhs(p.n, 0)
+        ref = hier.solve(b, tol=1e-8, nu=2)
+        x = np.zeros(p.n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        assert st == 0 and rr <= 1e-8 and abs(it - ref["iters"]) <= 1
+        # nu = 3 also exercises the tail's inner FCG window
+        ref3 = hier.solve(b, tol=1e-8, nu=3)
+        x = np.zeros(p.n)
+        st, it3, _ = amg.amg_solve(h, b, x, 1e-8, 3)
+        assert st == 0 and abs(it3 - ref3["iters"]) <= 1
+    finally:
+        amg.amg_free(h)
