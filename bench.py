@@ -280,11 +280,16 @@ def main_ours(a):
             traffic = json.load(open(tpath)).get(a.config)
         except Exception:
             traffic = None
+    fmt = {0: "CSR row tiles (fp64/int32)", 1: "SELL-32 fp64/int32", 2: "SELL-32 compressed (1-byte value/column codes)"}
+    survey_bytes = 12 * nnz + 36 * n  # SURVEY 8(d) model: int32 idx + fp64 values
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": "k_tiled<EpiSmooth> level-0 three-term smoother step",
+            "kernel": "k_sell<EpiSmooth> level-0 three-term smoother step",
+            "format": fmt.get(last.get("level0_format", 1)),
             "bytes_per_launch": bytes_launch, "avg_launch_us": avg_launch_ms * 1e3, "launches_timed": prof_n,
-            "peak_source": peak_src, "frac_of_8TBs": (achieved / 8000.0) if achieved else None}
+            "peak_source": peak_src, "frac_of_8TBs": (achieved / 8000.0) if achieved else None,
+            "survey_model_bytes": survey_bytes,
+            "survey_model_GBps": (survey_bytes / (avg_launch_ms / 1e3) / 1e9) if prof_n else None}
 
     # ---- cpu baseline: the oracle on a bounded sample of the same workload
     cpu = None

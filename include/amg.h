@@ -63,7 +63,9 @@ typedef struct {
     uint64_t seed;          /* matching-key salt seed (docs/keys.md); default 0 */
     void*    stream;        /* cudaStream_t the caller orders against; NULL = legacy default stream */
     int32_t  use_graphs;    /* 1 = replay each outer iteration as a captured CUDA graph; default 1 */
-    int32_t  reserved0;
+    int32_t  compress;      /* 1 = store each level's SELL streams losslessly compressed when possible:
+                               <= 256 distinct values -> 1-byte codes into an fp64 dictionary, column
+                               offsets col-row -> 1-byte codes (<= 256 distinct) or int16; default 1 */
     int64_t  tail_nnz;      /* the first level l >= 1 with nnz(A_l) <= tail_nnz and every level below it
                                run inside one single-CTA kernel per visit (coarse-tail megakernel);
                                0 disables; default 8192 */
@@ -96,7 +98,11 @@ typedef struct {
      * i.e. m launches of the fused three-term smoother step per outer iteration */
     double   prof_smoother_ms;        /* summed device time of the timed launches */
     int64_t  prof_smoother_launches;  /* number of timed launches */
-    int64_t  prof_smoother_bytes;     /* algorithmic bytes per launch: 12 nnz_0 + 36 n_0 (int32 idx, fp64) */
+    int64_t  prof_smoother_bytes;     /* algorithmic bytes per launch in the level-0 storage format: per entry
+                                         value+column stream bytes (12 uncompressed; 2 for paired 1-byte
+                                         codes), plus 32 n_0 for the four vectors */
+    int32_t  level0_format;           /* 0 CSR tiles, 1 SELL-32 fp64/int32, 2 SELL-32 compressed */
+    int32_t  reserved1;
 } amg_info;
 
 /* Fills *o with the defaults listed above.  Returns AMG_E_ARG if o == NULL. */

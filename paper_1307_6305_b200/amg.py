@@ -23,7 +23,7 @@ EXPORTS = ("amg_options_default", "amg_setup", "amg_solve", "amg_free", "amg_get
 class amg_options(ctypes.Structure):
     _fields_ = [("coarsest_size", ctypes.c_int64), ("kappa", ctypes.c_double), ("restart", ctypes.c_int32),
                 ("max_iter", ctypes.c_int32), ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
-                ("use_graphs", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("tail_nnz", ctypes.c_int64),
+                ("use_graphs", ctypes.c_int32), ("compress", ctypes.c_int32), ("tail_nnz", ctypes.c_int64),
                 ("reserved", ctypes.c_int64 * 5)]
 
 
@@ -37,7 +37,8 @@ class amg_info(ctypes.Structure):
                 ("last_true_relres", ctypes.c_double), ("launches_last_solve", ctypes.c_int64),
                 ("launches_per_iter", ctypes.c_int64), ("launches_last_setup", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("prof_smoother_ms", ctypes.c_double),
-                ("prof_smoother_launches", ctypes.c_int64), ("prof_smoother_bytes", ctypes.c_int64)]
+                ("prof_smoother_launches", ctypes.c_int64), ("prof_smoother_bytes", ctypes.c_int64),
+                ("level0_format", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
 
 
 class AmgError(RuntimeError):
@@ -149,7 +150,7 @@ def amg_get_info(h) -> dict:
                 launches_last_solve=inf.launches_last_solve, launches_per_iter=inf.launches_per_iter,
                 launches_last_setup=inf.launches_last_setup, device_bytes=inf.device_bytes,
                 prof_smoother_ms=inf.prof_smoother_ms, prof_smoother_launches=inf.prof_smoother_launches,
-                prof_smoother_bytes=inf.prof_smoother_bytes)
+                prof_smoother_bytes=inf.prof_smoother_bytes, level0_format=inf.level0_format)
 
 
 # ---------------------------------------------------------------- parity hooks (test-only)

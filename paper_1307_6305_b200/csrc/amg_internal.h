@@ -47,6 +47,18 @@ struct Sell {          // SELL-32: 32-row slices, entries column-major inside a 
     int* col = nullptr;    // [32 * sptr[nslices]]; padding: col = a valid row, val = 0
     double* val = nullptr;
     int64_t padded = 0;    // 32 * sptr[nslices]
+    int wmax = 0;          // maximum slice width (selects the kernel's width bucket)
+    // lossless compressed streams (same slice layout), chosen per level at setup:
+    int vmode = 0;         // 0: val (fp64); 1: vcode (uint8) into vdict (<= 256 distinct values)
+    int cmode = 0;         // 0: col (int32); 1: ccode (uint8) into cdict of offsets col-row; 2: coff (int16 col-row);
+                           // 3: pcode = vcode | ccode << 8 (uint16, one load per entry; requires vmode 1)
+    uint8_t* vcode = nullptr;
+    uint8_t* ccode = nullptr;
+    int16_t* coff = nullptr;
+    uint16_t* pcode = nullptr;
+    double* vdict = nullptr;
+    int* cdict = nullptr;
+    int nvdict = 0, ncdict = 0;
 };
 
 struct SpOp {          // the operator of one level as the SpMV-class kernels see it
@@ -107,6 +119,10 @@ void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaSt
 Tiles build_tiles(const Csr& A, int grid_per_sm, cudaStream_t s);
 // SELL-32 copy of A (built when its padding is acceptable); returns S with S.col == nullptr otherwise
 Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s);
+// Lossless compression of a SELL level: value dictionary (<= 256 distinct fp64 values) and column
+// offsets (<= 256 distinct col-row -> uint8 codes, else int16 if they fit).  Sets S.vmode/S.cmode.
+void compress_sell(Sell& S, const Csr& A, cudaStream_t s);
+void free_sell(Sell& S, cudaStream_t s);
 // dense (pseudo-)inverse of the coarsest operator, row-major n x n
 double* coarse_inverse(const Csr& A, bool singular, double shift, cudaStream_t s);
 void free_csr(Csr& A, cudaStream_t s);

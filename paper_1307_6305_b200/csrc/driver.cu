@@ -191,9 +191,7 @@ static void release(amg_hierarchy* h) {
             dfree(h->lev[l].A.ci, h->s);
             dfree(h->lev[l].A.v, h->s);
             dfree(h->lev[l].T.row, h->s);
-            dfree(h->lev[l].S.sptr, h->s);
-            dfree(h->lev[l].S.col, h->s);
-            dfree(h->lev[l].S.val, h->s);
+            free_sell(h->lev[l].S, h->s);
         }
         for (void* p : h->allocs) dfree(p, h->s);
         for (void* p : h->ws_allocs) dfree(p, h->s);
@@ -243,6 +241,12 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     if (rp0 != 0 || nnz_in < 0 || nnz_in + n64 >= (int64_t(1) << 31) - 64) {
         dfree(t_rp, s);
         throw Error(rp0 != 0 || nnz_in < 0 ? AMG_E_INPUT : AMG_E_ARG, "row_ptr[0] != 0 or nnz out of range");
+    }
+    {   // grow the stream-ordered pool once to the estimated setup peak (freed blocks stay reserved:
+        // release threshold = max), so the setup's many allocations never map memory mid-setup
+        const size_t want = (size_t)(nnz_in + n) * 64 + ((size_t)256 << 20);
+        void* r = nullptr;
+        if (cudaMallocAsync(&r, want, s) == cudaSuccess) dfree(r, s); else cudaGetLastError();
     }
     void *t_ci, *t_v, *t_d;
     const int32_t* ci = stage_in(ci_in, (size_t)nnz_in, s, &t_ci);
@@ -327,11 +331,12 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         if (k < h->L - 1 || k == 0) {
             Lv.T = build_tiles(Lv.A, 0, s);
             if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
+            if (Lv.S.sptr && h->opt.compress) compress_sell(Lv.S, Lv.A, s);
         }
         Lv.op.A = Lv.A;
         Lv.op.T = Lv.T;
         Lv.op.S = Lv.S;
-        Lv.op.sell = Lv.S.col != nullptr;
+        Lv.op.sell = Lv.S.sptr != nullptr;
     }
     pt.mark("tiles");
     // level workspaces
@@ -400,6 +405,21 @@ static void upload_tail_levels(amg_hierarchy* h) {
     }
     CK(cudaMemcpyAsync(h->d_tlev, t.data(), sizeof(TLevel) * t.size(), cudaMemcpyHostToDevice, h->s));
     CK(cudaStreamSynchronize(h->s));
+}
+
+// Algorithmic bytes of one general three-term smoother step on a level in the storage format the
+// kernel actually streams: per stored entry the value stream (fp64 8 B or 1-byte code)
+// plus the column stream (int32 4 B, 1-byte code, int16 2 B; a value/column code pair = 2 B total),
+// per row the four vectors x_k (gathered, counted once), x_{k-1}, f and the output (32 B), and the
+// row pointer (4 B) for the CSR row-tile fallback.  Uncompressed SELL: 12 nnz + 32 n.
+static int64_t smoother_bytes(const Level& Lv) {
+    const int64_t nnz = Lv.A.nnz, n = Lv.A.n;
+    if (!Lv.op.sell) return 12 * nnz + 36 * n;
+    const Sell& S = Lv.S;
+    int64_t per = 0;
+    if (S.cmode == 3) per = 2;
+    else per = (S.vmode ? 1 : 8) + (S.cmode == 0 ? 4 : S.cmode == 1 ? 1 : 2);
+    return per * nnz + 32 * n;
 }
 
 static bool use_tail(const amg_hierarchy* h, int l, int nu) { return l >= h->l_tail && nu <= kTailMaxNu; }
@@ -657,7 +677,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     h->info.launches_per_iter = h->graph_launches;
     h->info.prof_smoother_ms = prof_ms;
     h->info.prof_smoother_launches = prof_n;
-    h->info.prof_smoother_bytes = 12 * h->lev[0].A.nnz + 36 * (int64_t)h->lev[0].A.n;
+    h->info.prof_smoother_bytes = smoother_bytes(h->lev[0]);
     if (h->user) {  // order the caller's stream after this call's work
         CK(cudaEventRecord(h->e1, s));
         CK(cudaStreamWaitEvent(h->user, h->e1, 0));
@@ -682,6 +702,7 @@ int amg_options_default(amg_options* o) {
     o->stream = nullptr;
     o->use_graphs = 1;
     o->tail_nnz = 8192;
+    o->compress = 1;
     return AMG_OK;
 }
 
@@ -805,6 +826,10 @@ int amg_get_info(amg_handle h, amg_info* info) {
     r.grid_complexity = sn / h->lev[0].A.n;
     r.operator_complexity = snz / (double)h->lev[0].A.nnz;
     r.device_bytes = h->bytes;
+    {
+        const Level& L0 = h->lev[0];
+        r.level0_format = !L0.op.sell ? 0 : ((L0.S.vmode || L0.S.cmode) ? 2 : 1);
+    }
     *info = r;
     return AMG_OK;
 }

@@ -664,6 +664,12 @@ __global__ void k_sell_fill(int n, int nslices, const int* __restrict__ rp, cons
     }
 }
 
+__global__ void k_max_int(int n, const int* __restrict__ a, int* out) {
+    int m = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = max(m, a[i]);
+    atomicMax(out, m);
+}
+
 Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s) {
     Sell S;
     S.n = A.n;
@@ -675,6 +681,15 @@ Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s) {
     ++g_launches;
     int* sptr = dalloc<int>((size_t)S.nslices + 1, s);
     const int64_t units = exclusive_scan_total(width, sptr, S.nslices, s);
+    {
+        int* wm = dalloc<int>(1, s);
+        CK(cudaMemsetAsync(wm, 0, sizeof(int), s));
+        k_max_int<<<grid_for(S.nslices), kBlock, 0, s>>>(S.nslices, width, wm);
+        ++g_launches;
+        CK(cudaGetLastError());
+        S.wmax = read_scalar(wm, s);
+        dfree(wm, s);
+    }
     dfree(width, s);
     S.padded = units * 32;
     if ((double)S.padded > max_pad_ratio * (double)A.nnz + 64.0) {  // too irregular: keep CSR tiles
@@ -689,6 +704,231 @@ Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s) {
     CK(cudaGetLastError());
     ++g_launches;
     return S;
+}
+
+// ------------------------------------------------------------------ lossless SELL compression
+// Distinct fp64 values and distinct column offsets (col - row) of a level are collected with
+// per-block shared-memory hash sets (warp-deduplicated with __match_any_sync) flushed into global
+// hash sets; if <= 256 values (offsets) occur they become sorted dictionaries and each stored entry
+// keeps only a 1-byte code (int16 offsets when the offsets fit but are too many).  The SpMV kernels
+// expand codes through shared-memory copies of the dictionaries: bit-identical operands, 2-3 bytes
+// per entry instead of 12.
+constexpr int kGHT = 4096;  // global hash-set capacity (power of 2)
+constexpr int kBHT = 1024;  // per-block hash-set capacity
+constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFULL;
+
+__device__ __forceinline__ uint32_t mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return (uint32_t)x;
+}
+
+// returns true on overflow (a full or crowded set: more than kMaxProbe probes)
+constexpr int kMaxProbe = 32;
+__device__ bool set_insert(unsigned long long* tab, int cap, unsigned long long key, int* count) {
+    uint32_t h = mix64(key) & (uint32_t)(cap - 1);
+    for (int probe = 0; probe < kMaxProbe; ++probe) {
+        unsigned long long old = atomicCAS(&tab[h], kEmptyKey, key);
+        if (old == kEmptyKey) {
+            if (count) atomicAdd(count, 1);
+            return false;
+        }
+        if (old == key) return false;
+        h = (h + 1) & (uint32_t)(cap - 1);
+    }
+    return true;
+}
+
+__device__ __forceinline__ unsigned long long off_key(int off) { return (unsigned long long)(uint32_t)off; }
+
+// warp per SELL slice: insert every stored entry's value bits and offset (padding included: 0.0
+// and offset 0; lanes past n use offset 0) into the block sets, then flush into the global sets.
+__global__ void __launch_bounds__(kBlock) k_distinct(Sell S, unsigned long long* gv, unsigned long long* gc,
+                                                     int* counts, int* flags) {
+    __shared__ unsigned long long bv[kBHT], bc[kBHT];
+    __shared__ int bflag;
+    for (int k = threadIdx.x; k < kBHT; k += blockDim.x) { bv[k] = kEmptyKey; bc[k] = kEmptyKey; }
+    if (threadIdx.x == 0) bflag = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < S.nslices; sl += nw) {
+        const int b = S.sptr[sl], w = S.sptr[sl + 1] - b;
+        const int i = sl * 32 + lane;
+        const int fl = *((volatile int*)&bflag);
+        if (fl == 3) break;  // both sets overflowed: nothing left to learn
+        for (int j = 0; j < w; ++j) {
+            const size_t e = ((size_t)b + j) * 32 + lane;
+            if (!(fl & 1)) {
+                const unsigned long long vk = (unsigned long long)__double_as_longlong(S.val[e]);
+                unsigned mv = __match_any_sync(0xffffffffu, vk);
+                if (lane == __ffs(mv) - 1 && set_insert(bv, kBHT, vk, nullptr)) atomicOr(&bflag, 1);
+            }
+            if (!(fl & 2)) {
+                const unsigned long long ck = off_key(i < S.n ? S.col[e] - i : 0);
+                unsigned mc = __match_any_sync(0xffffffffu, ck);
+                if (lane == __ffs(mc) - 1 && set_insert(bc, kBHT, ck, nullptr)) atomicOr(&bflag, 2);
+            }
+        }
+    }
+    __syncthreads();
+    int f = bflag;
+    for (int k = threadIdx.x; k < kBHT; k += blockDim.x) {
+        if (!(f & 1) && bv[k] != kEmptyKey && set_insert(gv, kGHT, bv[k], counts + 0)) f |= 1;
+        if (!(f & 2) && bc[k] != kEmptyKey && set_insert(gc, kGHT, bc[k], counts + 1)) f |= 2;
+    }
+    if (f) atomicOr(flags, f);
+}
+
+// one block: compact a global set and rank-sort it into a dictionary (values as doubles, offsets as int)
+__global__ void k_dict_build(const unsigned long long* gv, const unsigned long long* gc, double* vdict, int* cdict,
+                             int nvmax, int ncmax) {
+    __shared__ unsigned long long kv[256], kc[256];
+    __shared__ int nv, nc;
+    if (threadIdx.x == 0) { nv = 0; nc = 0; }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kGHT; k += blockDim.x) {
+        if (gv[k] != kEmptyKey) { int t = atomicAdd(&nv, 1); if (t < 256) kv[t] = gv[k]; }
+        if (gc[k] != kEmptyKey) { int t = atomicAdd(&nc, 1); if (t < 256) kc[t] = gc[k]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < nv && nv <= nvmax) {
+        const double x = __longlong_as_double((long long)kv[threadIdx.x]);
+        int r = 0;
+        for (int k = 0; k < nv; ++k) {
+            const double y = __longlong_as_double((long long)kv[k]);
+            r += (y < x) || (y == x && kv[k] < kv[threadIdx.x]);  // total order (also splits +0 / -0)
+        }
+        vdict[r] = x;
+    }
+    if (threadIdx.x < nc && nc <= ncmax) {
+        const int x = (int)(uint32_t)kc[threadIdx.x];
+        int r = 0;
+        for (int k = 0; k < nc; ++k) r += ((int)(uint32_t)kc[k] < x);
+        cdict[r] = x;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_sell_encode(Sell S, int vmode, int cmode, const double* __restrict__ vdict,
+                                                        int nvd, const int* __restrict__ cdict, int ncd,
+                                                        uint8_t* vcode, uint8_t* ccode, int16_t* coff) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < S.nslices; sl += nw) {
+        const int b = S.sptr[sl], w = S.sptr[sl + 1] - b;
+        const int i = sl * 32 + lane;
+        for (int j = 0; j < w; ++j) {
+            const size_t e = ((size_t)b + j) * 32 + lane;
+            if (vmode == 1) {
+                const double x = S.val[e];
+                const unsigned long long xb = (unsigned long long)__double_as_longlong(x);
+                int lo = 0;
+                for (int k = 0; k < nvd; ++k)  // <= 256 entries, exact bit match
+                    if ((unsigned long long)__double_as_longlong(vdict[k]) == xb) { lo = k; break; }
+                vcode[e] = (uint8_t)lo;
+            }
+            const int off = i < S.n ? S.col[e] - i : 0;
+            if (cmode == 1) {
+                int lo = 0, hi = ncd;
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (cdict[mid] < off) lo = mid + 1; else hi = mid;
+                }
+                ccode[e] = (uint8_t)lo;
+            } else if (cmode == 2) {
+                coff[e] = (int16_t)off;
+            }
+        }
+    }
+}
+
+__global__ void k_pair_codes(int64_t m, const uint8_t* __restrict__ vc, const uint8_t* __restrict__ cc,
+                             uint16_t* __restrict__ pc) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+        pc[e] = (uint16_t)(vc[e] | (cc[e] << 8));
+}
+
+__global__ void k_minmax_off(Sell S, int* mm) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    int mn = 0, mx = 0;
+    for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < S.nslices; sl += nw) {
+        const int b = S.sptr[sl], w = S.sptr[sl + 1] - b;
+        const int i = sl * 32 + lane;
+        if (i >= S.n) continue;
+        for (int j = 0; j < w; ++j) {
+            const int off = S.col[((size_t)b + j) * 32 + lane] - i;
+            mn = min(mn, off);
+            mx = max(mx, off);
+        }
+    }
+    atomicMin(mm, mn);
+    atomicMax(mm + 1, mx);
+}
+
+void free_sell(Sell& S, cudaStream_t s) {
+    dfree(S.sptr, s); dfree(S.col, s); dfree(S.val, s); dfree(S.vcode, s); dfree(S.ccode, s);
+    dfree(S.coff, s); dfree(S.pcode, s); dfree(S.vdict, s); dfree(S.cdict, s);
+    S = Sell{};
+}
+
+void compress_sell(Sell& S, const Csr& A, cudaStream_t s) {
+    (void)A;
+    // only levels large enough to be HBM-bound (smaller ones are L2-resident and latency-bound)
+    if (!S.col || S.padded < (int64_t(1) << 22)) return;
+    unsigned long long* gv = dalloc<unsigned long long>(kGHT, s);
+    unsigned long long* gc = dalloc<unsigned long long>(kGHT, s);
+    int* aux = dalloc<int>(8, s);  // counts[2], flags, minmax[2]
+    CK(cudaMemsetAsync(gv, 0xff, sizeof(unsigned long long) * kGHT, s));
+    CK(cudaMemsetAsync(gc, 0xff, sizeof(unsigned long long) * kGHT, s));
+    CK(cudaMemsetAsync(aux, 0, sizeof(int) * 8, s));
+    const int g = grid_for((int64_t)S.nslices * 32);
+    k_distinct<<<g, kBlock, 0, s>>>(S, gv, gc, aux, aux + 2);
+    ++g_launches;
+    k_minmax_off<<<g, kBlock, 0, s>>>(S, aux + 3);
+    ++g_launches;
+    CK(cudaGetLastError());
+    int* h = static_cast<int*>(pinned_scratch()) + 32;
+    CK(cudaMemcpyAsync(h, aux, sizeof(int) * 5, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int nv = h[0], nc = h[1], fl = h[2], omin = h[3], omax = h[4];
+    S.vmode = (!(fl & 1) && nv <= 256) ? 1 : 0;
+    S.cmode = (!(fl & 2) && nc <= 256) ? 1 : ((omin >= -32768 && omax <= 32767) ? 2 : 0);
+    if (S.vmode || S.cmode) {
+        S.vdict = dalloc<double>(256, s);
+        S.cdict = dalloc<int>(256, s);
+        S.nvdict = S.vmode ? nv : 0;
+        S.ncdict = S.cmode == 1 ? nc : 0;
+        k_dict_build<<<1, 1024, 0, s>>>(gv, gc, S.vdict, S.cdict, S.vmode ? 256 : 0, S.cmode == 1 ? 256 : 0);
+        ++g_launches;
+        if (S.vmode) S.vcode = dalloc<uint8_t>((size_t)S.padded + 64, s);
+        if (S.cmode == 1) S.ccode = dalloc<uint8_t>((size_t)S.padded + 64, s);
+        if (S.cmode == 2) S.coff = dalloc<int16_t>((size_t)S.padded + 64, s);
+        k_sell_encode<<<g, kBlock, 0, s>>>(S, S.vmode, S.cmode, S.vdict, S.nvdict, S.cdict, S.ncdict, S.vcode,
+                                           S.ccode, S.coff);
+        ++g_launches;
+        CK(cudaGetLastError());
+        if (S.vmode == 1 && S.cmode == 1) {  // one 2-byte load per entry instead of two 1-byte loads
+            S.pcode = dalloc<uint16_t>((size_t)S.padded + 64, s);
+            k_pair_codes<<<grid_for(S.padded), kBlock, 0, s>>>(S.padded, S.vcode, S.ccode, S.pcode);
+            ++g_launches;
+            CK(cudaGetLastError());
+            dfree(S.vcode, s);
+            dfree(S.ccode, s);
+            S.vcode = nullptr;
+            S.ccode = nullptr;
+            S.cmode = 3;
+        }
+        // the replaced full-width streams are no longer needed by the solve
+        if (S.vmode) { dfree(S.val, s); S.val = nullptr; }
+        if (S.cmode) { dfree(S.col, s); S.col = nullptr; }
+    }
+    dfree(gv, s);
+    dfree(gc, s);
+    dfree(aux, s);
 }
 
 // ------------------------------------------------------------------ coarsest (a7)

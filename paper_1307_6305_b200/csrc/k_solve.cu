@@ -226,87 +226,186 @@ __device__ __forceinline__ double ld_gather(const double* p) {
     return r;
 }
 
-// Straight-line row reduction for a fixed slice width W: all W column and value loads, then all W
-// gathers, then the FMA chain (CSR order).  No predication, so ptxas keeps the loads hoisted.
-template <int W>
-__device__ __forceinline__ double sell_row(const int* __restrict__ cp, const double* __restrict__ vp,
-                                           const double* __restrict__ xg) {
-    int c[W];
+__device__ __forceinline__ int ld_stream_u8(const uint8_t* p) {
+    int r;
+    asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int ld_stream_u16(const uint16_t* p) {
+    int r;
+    asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int ld_stream_s16(const int16_t* p) {
+    int r;
+    asm volatile("ld.global.nc.L1::no_allocate.s16 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+// Operand streams of one SELL level in one of its storage formats:
+//   VM = 0: fp64 values;  VM = 1: uint8 codes into the value dictionary (shared memory)
+//   CM = 0: int32 columns; CM = 1: uint8 codes into the offset dictionary; CM = 2: int16 offsets
+template <int VM, int CM>
+struct SellOps {
+    const double* __restrict__ val;     // VM = 0
+    const uint8_t* __restrict__ vcode;  // VM = 1
+    const int* __restrict__ col;        // CM = 0
+    const uint8_t* __restrict__ ccode;  // CM = 1
+    const int16_t* __restrict__ coff;   // CM = 2
+    const uint16_t* __restrict__ pcode; // CM = 3: (value code | column code << 8), one load per entry
+    const double* sv;  // shared-memory value dictionary (VM = 1)
+    const int* sc;     // shared-memory offset dictionary (CM = 1)
+    int i;             // the lane's row
+    int nm1;           // n - 1
+    __device__ __forceinline__ void load_val(size_t e, double& v, int& vraw) const {
+        if constexpr (CM == 3) vraw = ld_stream_u16(pcode + e);
+        else if constexpr (VM == 0) v = ld_stream_d(val + e);
+        else vraw = ld_stream_u8(vcode + e);
+    }
+    // CM = 3 takes the column code from the pair already loaded by load_val
+    __device__ __forceinline__ int load_col(size_t e, int vraw) const {
+        if constexpr (CM == 0) return ld_stream_i(col + e);
+        else if constexpr (CM == 1) return ld_stream_u8(ccode + e);
+        else if constexpr (CM == 2) return ld_stream_s16(coff + e);
+        else return vraw >> 8;
+    }
+    __device__ __forceinline__ int column(int craw) const {
+        if constexpr (CM == 0) return craw;
+        else {
+            const int c = i + ((CM == 1 || CM == 3) ? sc[craw] : craw);
+            return c < nm1 ? c : nm1;  // lanes past n (last slice) read a valid element
+        }
+    }
+    __device__ __forceinline__ double value(double v, int vraw) const {
+        if constexpr (VM == 0) return v;
+        else if constexpr (CM == 3) return sv[vraw & 0xff];
+        else return sv[vraw];
+    }
+};
+
+// Straight-line row reduction for a fixed slice width W, scheduled as: all W value loads, all W
+// column loads, then (after every stream load has arrived) all W gathers, then the FMA chain in CSR
+// order.  `z` is an always-zero term that depends on every stream load, so ptxas cannot hoist a
+// gather between them and stall the warp before all streams of the slice are in flight.
+template <int W, int VM, int CM>
+__device__ __forceinline__ double sell_row(const SellOps<VM, CM>& ops, size_t e0, const double* __restrict__ xg) {
+    int c[W], vr[W];
     double v[W], x[W];
 #pragma unroll
-    for (int u = 0; u < W; ++u) {
-        c[u] = ld_stream_i(cp + u * 32);
-        v[u] = ld_stream_d(vp + u * 32);
-    }
+    for (int u = 0; u < W; ++u) ops.load_val(e0 + (size_t)u * 32, v[u], vr[u]);
 #pragma unroll
-    for (int u = 0; u < W; ++u) x[u] = ld_gather(xg + c[u]);
+    for (int u = 0; u < W; ++u) c[u] = ops.load_col(e0 + (size_t)u * 32, vr[u]);
+    int all = 0, vdep = -1;
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+        c[u] = ops.column(c[u]);
+        all |= c[u];
+        if constexpr (VM == 0) vdep &= __double2hiint(v[u]); else all |= vr[u];
+    }
+    // z == 0 always (columns and codes are >= 0; no stored value has the NaN high word 0x7ff80001),
+    // but it depends on every column and value load, so every stream load is issued before any gather
+    const int z = (all < 0 || vdep == 0x7ff80001) ? 1 : 0;
+#pragma unroll
+    for (int u = 0; u < W; ++u) x[u] = ld_gather(xg + (c[u] | z));
     double s = 0.0;
 #pragma unroll
-    for (int u = 0; u < W; ++u) s = fma(v[u], x[u], s);
+    for (int u = 0; u < W; ++u) s = fma(ops.value(v[u], vr[u]), x[u], s);
     return s;
 }
 
 // generic width: chunks of 8 entries, then the remainder
-__device__ __noinline__ double sell_row_any(const int* __restrict__ cp, const double* __restrict__ vp,
-                                            const double* __restrict__ xg, int w) {
+template <int VM, int CM>
+__device__ __noinline__ double sell_row_any(const SellOps<VM, CM> ops, size_t e0, const double* __restrict__ xg,
+                                            int w) {
     double s = 0.0;
     int j = 0;
-    for (; j + 8 <= w; j += 8) {
-        int c[8];
-        double v[8], x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            c[u] = ld_stream_i(cp + (j + u) * 32);
-            v[u] = ld_stream_d(vp + (j + u) * 32);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = ld_gather(xg + c[u]);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s = fma(v[u], x[u], s);
+    for (; j + 8 <= w; j += 8) s += sell_row<8, VM, CM>(ops, e0 + (size_t)j * 32, xg);
+    for (; j < w; ++j) {
+        int vr = 0;
+        double v = 0.0;
+        ops.load_val(e0 + (size_t)j * 32, v, vr);
+        const int c = ops.column(ops.load_col(e0 + (size_t)j * 32, vr));
+        s = fma(ops.value(v, vr), ld_gather(xg + c), s);
     }
-    for (; j < w; ++j) s = fma(ld_stream_d(vp + j * 32), ld_gather(xg + ld_stream_i(cp + j * 32)), s);
     return s;
 }
 
-template <class Epi, bool DOTS>
+// Width dispatch limited to the level's maximum slice width bucket WMAX (5, 8, 12, or 0 = generic):
+// ptxas sizes the register file for the largest straight-line case compiled in, so a level whose
+// slices are all <= 5 wide must not carry the 12-wide case (80 vs ~48 registers, 3 vs 5 CTAs/SM).
+template <int WMAX, int VM, int CM>
+__device__ __forceinline__ double sell_row_w(const SellOps<VM, CM>& ops, size_t e0, const double* __restrict__ xg,
+                                             int w) {
+    if constexpr (WMAX == 0) {
+        return sell_row_any<VM, CM>(ops, e0, xg, w);
+    } else {
+        switch (w) {
+            case 0: return 0.0;
+            case 1: return sell_row<1>(ops, e0, xg);
+            case 2: return sell_row<2>(ops, e0, xg);
+            case 3: return sell_row<3>(ops, e0, xg);
+            case 4: return sell_row<4>(ops, e0, xg);
+            case 5: return sell_row<5>(ops, e0, xg);
+            default: break;
+        }
+        if constexpr (WMAX >= 8) {
+            switch (w) {
+                case 6: return sell_row<6>(ops, e0, xg);
+                case 7: return sell_row<7>(ops, e0, xg);
+                case 8: return sell_row<8>(ops, e0, xg);
+                default: break;
+            }
+        }
+        if constexpr (WMAX >= 12) {
+            switch (w) {
+                case 9: return sell_row<9>(ops, e0, xg);
+                case 10: return sell_row<10>(ops, e0, xg);
+                case 11: return sell_row<11>(ops, e0, xg);
+                case 12: return sell_row<12>(ops, e0, xg);
+                default: break;
+            }
+        }
+        return 0.0;  // unreachable: every slice of the level is at most WMAX wide (S.wmax, setup)
+    }
+}
+
+template <class Epi, bool DOTS, int VM, int CM, int WMAX>
 __global__ void __launch_bounds__(kBlock) k_sell(Sell S, const double* __restrict__ xg, Epi epi, double* partials,
                                                  unsigned* ticket, DotOut dot_out) {
+    __shared__ double sv[VM ? 256 : 1];
+    __shared__ int sc[(CM == 1 || CM == 3) ? 256 : 1];
+    if constexpr (VM == 1)
+        for (int k = threadIdx.x; k < S.nvdict; k += blockDim.x) sv[k] = S.vdict[k];
+    if constexpr (CM == 1 || CM == 3)
+        for (int k = threadIdx.x; k < S.ncdict; k += blockDim.x) sc[k] = S.cdict[k];
+    if constexpr (VM == 1 || CM == 1 || CM == 3) __syncthreads();
     double acc[Epi::ND > 0 ? Epi::ND : 1];
 #pragma unroll
     for (int k = 0; k < (Epi::ND > 0 ? Epi::ND : 1); ++k) acc[k] = 0.0;
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < S.nslices; sl += nwarps) {
-        const int b = __ldg(S.sptr + sl), e = __ldg(S.sptr + sl + 1);
-        const int* __restrict__ cp = S.col + (size_t)b * 32 + lane;
-        const double* __restrict__ vp = S.val + (size_t)b * 32 + lane;
+    int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // slice bounds are software-pipelined: the next slice's sptr pair is fetched while this slice
+    // streams, so every slice costs two dependent memory round trips (streams, then gathers)
+    int b = 0, e = 0;
+    if (sl < S.nslices) { b = __ldg(S.sptr + sl); e = __ldg(S.sptr + sl + 1); }
+    for (; sl < S.nslices; sl += nwarps) {
+        const int sn = sl + nwarps;
+        int bn = 0, en = 0;
+        if (sn < S.nslices) { bn = __ldg(S.sptr + sn); en = __ldg(S.sptr + sn + 1); }
         const int i = sl * 32 + lane;
-        const int w = e - b;  // warp-uniform
         const bool act = i < S.n;
+        const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, i, S.n - 1};
         typename Epi::Pre pre{};
         double xi = 0.0;
         if (act) {  // independent row operands first (their latency overlaps the matrix stream)
             pre = epi.load(i);
             xi = ld_gather(xg + i);
         }
-        double sum;
-        switch (w) {
-            case 0: sum = 0.0; break;
-            case 1: sum = sell_row<1>(cp, vp, xg); break;
-            case 2: sum = sell_row<2>(cp, vp, xg); break;
-            case 3: sum = sell_row<3>(cp, vp, xg); break;
-            case 4: sum = sell_row<4>(cp, vp, xg); break;
-            case 5: sum = sell_row<5>(cp, vp, xg); break;
-            case 6: sum = sell_row<6>(cp, vp, xg); break;
-            case 7: sum = sell_row<7>(cp, vp, xg); break;
-            case 8: sum = sell_row<8>(cp, vp, xg); break;
-            case 9: sum = sell_row<9>(cp, vp, xg); break;
-            case 10: sum = sell_row<10>(cp, vp, xg); break;
-            case 11: sum = sell_row<11>(cp, vp, xg); break;
-            case 12: sum = sell_row<12>(cp, vp, xg); break;
-            default: sum = sell_row_any(cp, vp, xg, w); break;
-        }
+        const double sum = sell_row_w<WMAX>(ops, (size_t)b * 32 + lane, xg, e - b);  // width is warp-uniform
         if (act) epi.store(i, sum, xi, pre, acc);
+        b = bn;
+        e = en;
     }
     if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
 }
@@ -342,18 +441,43 @@ int tiled_grid(int cap, int ntiles) {
     return g < 1 ? 1 : g;
 }
 
+template <class Epi, bool DOTS, int VM, int CM, int WMAX>
+static void launch_sell_w(const SpOp& op, const double* xg, const Epi& epi, double* part, unsigned* tk,
+                          DotOut dot_out, cudaStream_t s) {
+    static int res = 0;  // per instance
+    if (!res) res = resident_grid(k_sell<Epi, DOTS, VM, CM, WMAX>, 0);
+    int need = (op.S.nslices + (kBlock / 32) - 1) / (kBlock / 32);
+    int g = need < res ? need : res;
+    if (g < 1) g = 1;
+    k_sell<Epi, DOTS, VM, CM, WMAX><<<g, kBlock, 0, s>>>(op.S, xg, epi, part, tk, dot_out);
+}
+
+template <class Epi, bool DOTS, int VM, int CM>
+static void launch_sell(const SpOp& op, const double* xg, const Epi& epi, double* part, unsigned* tk, DotOut dot_out,
+                        cudaStream_t s) {
+    const int w = op.S.wmax;
+    if (w <= 5) launch_sell_w<Epi, DOTS, VM, CM, 5>(op, xg, epi, part, tk, dot_out, s);
+    else if (w <= 8) launch_sell_w<Epi, DOTS, VM, CM, 8>(op, xg, epi, part, tk, dot_out, s);
+    else if (w <= 12) launch_sell_w<Epi, DOTS, VM, CM, 12>(op, xg, epi, part, tk, dot_out, s);
+    else launch_sell_w<Epi, DOTS, VM, CM, 0>(op, xg, epi, part, tk, dot_out, s);
+}
+
 template <class Epi, bool DOTS>
 static void launch_op(const SpOp& op, const double* xg, const Epi& epi, const DotScratch* ds, DotOut dot_out,
                       cudaStream_t s) {
     double* part = ds ? ds->partials : nullptr;
     unsigned* tk = ds ? ds->ticket : nullptr;
     if (op.sell) {
-        static int res = 0;
-        if (!res) res = resident_grid(k_sell<Epi, DOTS>, 0);
-        int need = (op.S.nslices + (kBlock / 32) - 1) / (kBlock / 32);
-        int g = need < res ? need : res;
-        if (g < 1) g = 1;
-        k_sell<Epi, DOTS><<<g, kBlock, 0, s>>>(op.S, xg, epi, part, tk, dot_out);
+        const int fmt = op.S.vmode * 4 + op.S.cmode;
+        switch (fmt) {
+            case 0: launch_sell<Epi, DOTS, 0, 0>(op, xg, epi, part, tk, dot_out, s); break;
+            case 1: launch_sell<Epi, DOTS, 0, 1>(op, xg, epi, part, tk, dot_out, s); break;
+            case 2: launch_sell<Epi, DOTS, 0, 2>(op, xg, epi, part, tk, dot_out, s); break;
+            case 4: launch_sell<Epi, DOTS, 1, 0>(op, xg, epi, part, tk, dot_out, s); break;
+            case 5: launch_sell<Epi, DOTS, 1, 1>(op, xg, epi, part, tk, dot_out, s); break;
+            case 6: launch_sell<Epi, DOTS, 1, 2>(op, xg, epi, part, tk, dot_out, s); break;
+            default: launch_sell<Epi, DOTS, 1, 3>(op, xg, epi, part, tk, dot_out, s); break;
+        }
     } else {
         int g = tiled_resident<Epi, DOTS>(op.T.cap);
         if (g > op.T.ntiles) g = op.T.ntiles;

@@ -105,7 +105,7 @@ __device__ void t_gemv(int n, const double* M, const double* r, double* e, TCtx 
 }
 
 template <bool CL>
-__device__ void t_fcg(const TailArgs& A, int l, TCtx c);
+__device__ __noinline__ void t_fcg(const TailArgs& A, int l, TCtx c);
 
 // z = B_l(r) -- same schedule as driver.cu apply_B
 template <bool CL>

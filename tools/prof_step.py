@@ -30,6 +30,8 @@ arrs = [torch.from_numpy(x).to(dev) if x is not None else None for x in (p.rp, p
 b = torch.from_numpy(gen.rhs(p.n, prm["seed"])).to(dev)
 x = torch.zeros(p.n, dtype=torch.float64, device=dev)
 o = amg.amg_options_default(coarsest_size=prm["coarsest_size"], max_iter=a.max_iter, use_graphs=0 if a.no_graphs else 1)
+if os.environ.get("AMG_COMPRESS"):
+    o.compress = int(os.environ["AMG_COMPRESS"])
 if os.environ.get("AMG_TAIL_NNZ"):
     o.tail_nnz = int(os.environ["AMG_TAIL_NNZ"])
 if a.user_stream:

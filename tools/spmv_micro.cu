@@ -211,6 +211,164 @@ __global__ void __launch_bounds__(256) v3(Args a, int per_block) {
     }
 }
 
+// ---- compressed variants: uint8 value codes + uint8 offset codes (dictionaries in shared memory)
+__device__ __forceinline__ int ldu8(const unsigned char* p) {
+    int r;
+    asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double ldg_nc(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+struct CArgs {
+    int n, nslices;
+    const int* sptr;
+    const unsigned char* vc;
+    const unsigned char* cc;
+    const double* vdict;
+    const int* cdict;
+    const double* xg;
+    const double* f;
+    const double* xprev;
+    double* out;
+    double alpha, beta;
+};
+
+// NS slices per warp iteration (slices sl, sl + nw, ...), fixed width W = 5 fast path
+template <int NS, int MINB>
+__global__ void __launch_bounds__(256, MINB) vc_k(CArgs a) {
+    __shared__ double sv[256];
+    __shared__ int sc[256];
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) { sv[k] = a.vdict[k]; sc[k] = a.cdict[k]; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    constexpr int W = 5;
+    for (int s0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s0 < a.nslices; s0 += NS * nw) {
+        int i[NS];
+        double fi[NS], xp[NS], xi[NS];
+        int cr[NS][W], vr[NS][W];
+        bool ok[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            int sl = s0 + k * nw;
+            ok[k] = sl < a.nslices;
+            i[k] = sl * 32 + lane;
+            bool act = ok[k] && i[k] < a.n;
+            fi[k] = act ? ldd(a.f + i[k]) : 0;
+            xp[k] = act ? ldd(a.xprev + i[k]) : 0;
+            xi[k] = act ? ldg_nc(a.xg + i[k]) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                size_t e = ((size_t)(s0 + k * nw) * W + u) * 32 + lane;
+                vr[k][u] = ok[k] ? ldu8(a.vc + e) : 0;
+                cr[k][u] = ok[k] ? ldu8(a.cc + e) : 2;
+            }
+        int all = 0;
+        int col[NS][W];
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                int c = i[k] + sc[cr[k][u]];
+                c = c < a.n ? c : a.n - 1;
+                c = c < 0 ? 0 : c;
+                col[k][u] = c;
+                all |= c | vr[k][u];
+            }
+        const int z = all < 0 ? 1 : 0;
+        double x[NS][W];
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int u = 0; u < W; ++u) x[k][u] = ldg_nc(a.xg + (col[k][u] | z));
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < W; ++u) s = fma(sv[vr[k][u]], x[k][u], s);
+            if (ok[k] && i[k] < a.n) a.out[i[k]] = a.alpha * xi[k] + (1.0 - a.alpha) * xp[k] + a.beta * (fi[k] - s);
+        }
+    }
+}
+
+// uncompressed with the same NS structure
+template <int NS, int MINB>
+__global__ void __launch_bounds__(256, MINB) vu_k(Args a) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    constexpr int W = 5;
+    for (int s0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s0 < a.nslices; s0 += NS * nw) {
+        int i[NS];
+        double fi[NS], xp[NS], xi[NS];
+        int c[NS][W];
+        double v[NS][W];
+        bool ok[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            int sl = s0 + k * nw;
+            ok[k] = sl < a.nslices;
+            i[k] = sl * 32 + lane;
+            bool act = ok[k] && i[k] < a.n;
+            fi[k] = act ? ldd(a.f + i[k]) : 0;
+            xp[k] = act ? ldd(a.xprev + i[k]) : 0;
+            xi[k] = act ? ldg_nc(a.xg + i[k]) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                size_t e = ((size_t)(s0 + k * nw) * W + u) * 32 + lane;
+                v[k][u] = ok[k] ? ldd(a.val + e) : 0;
+                c[k][u] = ok[k] ? ldi(a.col + e) : 0;
+            }
+        int all = 0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int u = 0; u < W; ++u) all |= c[k][u];
+        const int z = all < 0 ? 1 : 0;
+        double x[NS][W];
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+            for (int u = 0; u < W; ++u) x[k][u] = ldg_nc(a.xg + (c[k][u] | z));
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < W; ++u) s = fma(v[k][u], x[k][u], s);
+            if (ok[k] && i[k] < a.n) a.out[i[k]] = a.alpha * xi[k] + (1.0 - a.alpha) * xp[k] + a.beta * (fi[k] - s);
+        }
+    }
+}
+
+__global__ void build5c(int N, unsigned char* vc, unsigned char* cc) {
+    // codes: values {-1 -> 0, 4 -> 1, 0 -> 2}; offsets {-N -> 0, -1 -> 1, 0 -> 2, 1 -> 3, N -> 4}
+    const int n = N * N, nsl = (n + 31) / 32;
+    for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < (long)nsl * 32; t += (long)gridDim.x * blockDim.x) {
+        int sl = (int)(t >> 5), lane = (int)(t & 31), i = sl * 32 + lane;
+        int iy = i / N, ix = i % N;
+        int cs[5], vs[5], m = 0;
+        if (i < n) {
+            if (iy > 0) { cs[m] = 0; vs[m++] = 0; }
+            if (ix > 0) { cs[m] = 1; vs[m++] = 0; }
+            cs[m] = 2; vs[m++] = 1;
+            if (ix < N - 1) { cs[m] = 3; vs[m++] = 0; }
+            if (iy < N - 1) { cs[m] = 4; vs[m++] = 0; }
+        }
+        for (int j = 0; j < 5; ++j) {
+            vc[((size_t)sl * 5 + j) * 32 + lane] = (unsigned char)(j < m ? vs[j] : 2);
+            cc[((size_t)sl * 5 + j) * 32 + lane] = (unsigned char)(j < m ? cs[j] : 2);
+        }
+    }
+}
+
 // stream copy reference (read 2 arrays, write 1) to calibrate the achievable bandwidth
 __global__ void copy3(const double2* a, const double2* b, double2* c, size_t n2) {
     for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n2; k += (size_t)gridDim.x * blockDim.x) {
@@ -329,6 +487,48 @@ int main(int argc, char** argv) {
         int g = occ(v3<8>);
         int per = (nsl + g - 1) / g;
         run("v3<8> contiguous chunks", [&] { v3<8><<<g, 256>>>(a, per); });
+    }
+    {
+        unsigned char *vc, *cc;
+        double* vd;
+        int* cd;
+        CKM(cudaMalloc(&vc, (size_t)nsl * 160 + 256));
+        CKM(cudaMalloc(&cc, (size_t)nsl * 160 + 256));
+        CKM(cudaMalloc(&vd, 256 * 8));
+        CKM(cudaMalloc(&cd, 256 * 4));
+        double hv[256] = {-1.0, 4.0, 0.0};
+        int hc[256] = {-N, -1, 0, 1, N};
+        CKM(cudaMemcpy(vd, hv, sizeof(hv), cudaMemcpyHostToDevice));
+        CKM(cudaMemcpy(cd, hc, sizeof(hc), cudaMemcpyHostToDevice));
+        build5c<<<4096, 256>>>(N, vc, cc);
+        CKM(cudaDeviceSynchronize());
+        CArgs c{n, nsl, sptr, vc, cc, vd, cd, xg, f, xp, out, a.alpha, a.beta};
+        const double cbytes = 2.0 * nsl * 160 + 32.0 * n;
+        auto runc = [&](const char* name, auto k) {
+            int g = occ(k);
+            for (int r = 0; r < 3; ++r) k<<<g, 256>>>(c);
+            CKM(cudaDeviceSynchronize());
+            cudaEventRecord(e0);
+            for (int r = 0; r < 20; ++r) k<<<g, 256>>>(c);
+            cudaEventRecord(e1);
+            CKM(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            double us = 1e3 * ms / 20;
+            printf("%-34s %8.1f us  actual %6.0f GB/s  (grid %d)\n", name, us, cbytes / us / 1e3, g);
+        };
+        runc("vc NS=1", vc_k<1, 1>);
+        runc("vc NS=2", vc_k<2, 1>);
+        runc("vc NS=4", vc_k<4, 1>);
+        runc("vc NS=1 minb4", vc_k<1, 4>);
+        runc("vc NS=2 minb3", vc_k<2, 3>);
+        auto runu = [&](const char* name, auto k) {
+            int g = occ(k);
+            run(name, [&] { k<<<g, 256>>>(a); });
+        };
+        runu("vu NS=1", vu_k<1, 1>);
+        runu("vu NS=2", vu_k<2, 1>);
+        runu("vu NS=1 minb4", vu_k<1, 4>);
     }
     printf("occupancy (blocks/GPU): v0<8> %d v1<8,1> %d v1<8,4> %d v2<5> %d v2<8> %d\n", occ(v0<8>), occ(v1<8, 1>),
            occ(v1<8, 4>), occ(v2<5>), occ(v2<8>));
