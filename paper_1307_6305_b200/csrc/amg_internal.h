@@ -8,6 +8,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace amg {
 
@@ -196,6 +197,31 @@ constexpr int kTailMaxNu = 4;  // the tail kernel supports nu <= 4
 // cluster size actually used (16 if the device allows non-portable clusters, else 8)
 int tail_cluster_size();
 void launch_tail(const TailArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every solve kernel is launched with programmatic stream serialization: it triggers its
+// dependents at entry (so the next kernel of the k-cycle is already resident) and waits for its
+// predecessor's completion + memory visibility (griddepcontrol.wait) before touching any data the
+// predecessor may have written.  Captured into the CUDA graphs as programmatic edges.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // grid size used by the vector kernels
 int vector_grid();

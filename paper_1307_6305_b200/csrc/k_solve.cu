@@ -12,6 +12,8 @@
 //    prolongation (a12) is fused with its axpy.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "amg_internal.h"
 
 namespace amg {
@@ -26,6 +28,19 @@ void init_device_props() {
 }
 
 int vector_grid() { return g_num_sms * 4; }
+
+// grid of a grid-stride vector kernel over n elements: ~4 elements per thread, at most 4 CTAs/SM
+static int vgrid(int64_t n) {
+    int64_t g = (n + 4 * kBlock - 1) / (4 * kBlock);
+    if (g > vector_grid()) g = vector_grid();
+    return g < 1 ? 1 : (int)g;
+}
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) on = getenv("AMG_PDL") ? 1 : 0;  // measured slower on C1-C5: opt-in
+    return on == 1;
+}
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
@@ -158,6 +173,8 @@ template <class Epi, bool DOTS>
 __global__ void __launch_bounds__(kBlock) k_tiled(Csr A, const double* __restrict__ xg,
                                                   const int* __restrict__ tile_row, int ntiles, int cap, Epi epi,
                                                   double* partials, unsigned* ticket, DotOut dot_out) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* sv = reinterpret_cast<double*>(smem_raw);
     int* sc = reinterpret_cast<int*>(sv + cap + 2);
@@ -313,24 +330,28 @@ __device__ __forceinline__ double sell_row(const SellOps<VM, CM>& ops, size_t e0
     return s;
 }
 
-// generic width: chunks of 8 entries, then the remainder
+// generic width: straight-line chunks of 8 entries, then a straight-line remainder (0..7)
 template <int VM, int CM>
 __device__ __noinline__ double sell_row_any(const SellOps<VM, CM> ops, size_t e0, const double* __restrict__ xg,
                                             int w) {
     double s = 0.0;
     int j = 0;
     for (; j + 8 <= w; j += 8) s += sell_row<8, VM, CM>(ops, e0 + (size_t)j * 32, xg);
-    for (; j < w; ++j) {
-        int vr = 0;
-        double v = 0.0;
-        ops.load_val(e0 + (size_t)j * 32, v, vr);
-        const int c = ops.column(ops.load_col(e0 + (size_t)j * 32, vr));
-        s = fma(ops.value(v, vr), ld_gather(xg + c), s);
+    const size_t er = e0 + (size_t)j * 32;
+    switch (w - j) {
+        case 1: s += sell_row<1, VM, CM>(ops, er, xg); break;
+        case 2: s += sell_row<2, VM, CM>(ops, er, xg); break;
+        case 3: s += sell_row<3, VM, CM>(ops, er, xg); break;
+        case 4: s += sell_row<4, VM, CM>(ops, er, xg); break;
+        case 5: s += sell_row<5, VM, CM>(ops, er, xg); break;
+        case 6: s += sell_row<6, VM, CM>(ops, er, xg); break;
+        case 7: s += sell_row<7, VM, CM>(ops, er, xg); break;
+        default: break;
     }
     return s;
 }
 
-// Width dispatch limited to the level's maximum slice width bucket WMAX (5, 8, 12, or 0 = generic):
+// Width dispatch limited to the level's maximum slice width bucket WMAX (5, 8, 12, 16, or 0 = generic):
 // ptxas sizes the register file for the largest straight-line case compiled in, so a level whose
 // slices are all <= 5 wide must not carry the 12-wide case (80 vs ~48 registers, 3 vs 5 CTAs/SM).
 template <int WMAX, int VM, int CM>
@@ -365,6 +386,15 @@ __device__ __forceinline__ double sell_row_w(const SellOps<VM, CM>& ops, size_t 
                 default: break;
             }
         }
+        if constexpr (WMAX >= 16) {
+            switch (w) {
+                case 13: return sell_row<13>(ops, e0, xg);
+                case 14: return sell_row<14>(ops, e0, xg);
+                case 15: return sell_row<15>(ops, e0, xg);
+                case 16: return sell_row<16>(ops, e0, xg);
+                default: break;
+            }
+        }
         return 0.0;  // unreachable: every slice of the level is at most WMAX wide (S.wmax, setup)
     }
 }
@@ -374,11 +404,13 @@ __global__ void __launch_bounds__(kBlock) k_sell(Sell S, const double* __restric
                                                  unsigned* ticket, DotOut dot_out) {
     __shared__ double sv[VM ? 256 : 1];
     __shared__ int sc[(CM == 1 || CM == 3) ? 256 : 1];
+    pdl_trigger();  // the dictionaries are constant: load them before waiting on the predecessor
     if constexpr (VM == 1)
         for (int k = threadIdx.x; k < S.nvdict; k += blockDim.x) sv[k] = S.vdict[k];
     if constexpr (CM == 1 || CM == 3)
         for (int k = threadIdx.x; k < S.ncdict; k += blockDim.x) sc[k] = S.cdict[k];
     if constexpr (VM == 1 || CM == 1 || CM == 3) __syncthreads();
+    pdl_wait();
     double acc[Epi::ND > 0 ? Epi::ND : 1];
 #pragma unroll
     for (int k = 0; k < (Epi::ND > 0 ? Epi::ND : 1); ++k) acc[k] = 0.0;
@@ -449,7 +481,7 @@ static void launch_sell_w(const SpOp& op, const double* xg, const Epi& epi, doub
     int need = (op.S.nslices + (kBlock / 32) - 1) / (kBlock / 32);
     int g = need < res ? need : res;
     if (g < 1) g = 1;
-    k_sell<Epi, DOTS, VM, CM, WMAX><<<g, kBlock, 0, s>>>(op.S, xg, epi, part, tk, dot_out);
+    launch_k(k_sell<Epi, DOTS, VM, CM, WMAX>, dim3(g), dim3(kBlock), 0, s, op.S, xg, epi, part, tk, dot_out);
 }
 
 template <class Epi, bool DOTS, int VM, int CM>
@@ -459,6 +491,7 @@ static void launch_sell(const SpOp& op, const double* xg, const Epi& epi, double
     if (w <= 5) launch_sell_w<Epi, DOTS, VM, CM, 5>(op, xg, epi, part, tk, dot_out, s);
     else if (w <= 8) launch_sell_w<Epi, DOTS, VM, CM, 8>(op, xg, epi, part, tk, dot_out, s);
     else if (w <= 12) launch_sell_w<Epi, DOTS, VM, CM, 12>(op, xg, epi, part, tk, dot_out, s);
+    else if (w <= 16) launch_sell_w<Epi, DOTS, VM, CM, 16>(op, xg, epi, part, tk, dot_out, s);
     else launch_sell_w<Epi, DOTS, VM, CM, 0>(op, xg, epi, part, tk, dot_out, s);
 }
 
@@ -482,8 +515,8 @@ static void launch_op(const SpOp& op, const double* xg, const Epi& epi, const Do
         int g = tiled_resident<Epi, DOTS>(op.T.cap);
         if (g > op.T.ntiles) g = op.T.ntiles;
         if (g < 1) g = 1;
-        k_tiled<Epi, DOTS><<<g, kBlock, tile_smem(op.T), s>>>(op.A, xg, op.T.row, op.T.ntiles, op.T.cap, epi, part, tk,
-                                                              dot_out);
+        launch_k(k_tiled<Epi, DOTS>, dim3(g), dim3(kBlock), tile_smem(op.T), s, op.A, xg, (const int*)op.T.row,
+                 op.T.ntiles, op.T.cap, epi, part, tk, dot_out);
     }
     CK(cudaGetLastError());
     ++g_launches;
@@ -514,6 +547,8 @@ void launch_spmv_dots(const SpOp& op, const double* d, const double* rho, double
 __global__ void __launch_bounds__(kBlock) k_restrict(int nc, const int* __restrict__ aptr,
                                                      const int* __restrict__ perm, const double* __restrict__ r,
                                                      double* __restrict__ rH) {
+    pdl_trigger();
+    pdl_wait();
     for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
         const int t0 = aptr[I], t1 = aptr[I + 1];
         double s = 0.0;
@@ -523,22 +558,22 @@ __global__ void __launch_bounds__(kBlock) k_restrict(int nc, const int* __restri
 }
 
 void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, double* rH, cudaStream_t s) {
-    int grid = (nc + kBlock - 1) / kBlock;
-    if (grid > vector_grid()) grid = vector_grid();
-    k_restrict<<<grid, kBlock, 0, s>>>(nc, aptr, perm, r, rH);
+    const int grid = vgrid(nc);
+    launch_k(k_restrict, dim3(grid), dim3(kBlock), 0, s, nc, aptr, perm, r, rH);
     CK(cudaGetLastError());
     ++g_launches;
 }
 
 __global__ void __launch_bounds__(kBlock) k_prolong(int n, const int* __restrict__ agg,
                                                     const double* __restrict__ eH, double* __restrict__ x) {
+    pdl_trigger();
+    pdl_wait();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += __ldg(eH + agg[i]);
 }
 
 void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s) {
-    int grid = (n + kBlock - 1) / kBlock;
-    if (grid > vector_grid()) grid = vector_grid();
-    k_prolong<<<grid, kBlock, 0, s>>>(n, agg, eH, x);
+    const int grid = vgrid(n);
+    launch_k(k_prolong, dim3(grid), dim3(kBlock), 0, s, n, agg, eH, x);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -546,6 +581,8 @@ void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStre
 // warp per row GEMV of the dense coarsest (pseudo-)inverse
 __global__ void __launch_bounds__(kBlock) k_gemv(int n, const double* __restrict__ M, const double* __restrict__ r,
                                                  double* __restrict__ e) {
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int nwarp = (gridDim.x * blockDim.x) >> 5;
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarp) {
@@ -559,7 +596,7 @@ __global__ void __launch_bounds__(kBlock) k_gemv(int n, const double* __restrict
 void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_t s) {
     int grid = (n * 32 + kBlock - 1) / kBlock;
     if (grid > vector_grid()) grid = vector_grid();
-    k_gemv<<<grid, kBlock, 0, s>>>(n, M, r, e);
+    launch_k(k_gemv, dim3(grid), dim3(kBlock), 0, s, n, M, r, e);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -571,6 +608,8 @@ struct PtrArr {
 
 __global__ void __launch_bounds__(kBlock) k_multidot(int n, const double* __restrict__ z, PtrArr Q, int w,
                                                      double* partials, unsigned* ticket, double* c) {
+    pdl_trigger();
+    pdl_wait();
     double acc[kMaxWin];
 #pragma unroll
     for (int j = 0; j < kMaxWin; ++j) acc[j] = 0.0;
@@ -607,7 +646,7 @@ void launch_multidot(int n, const double* z, const double* const* Q, int w, doub
                      cudaStream_t s) {
     PtrArr a{};
     for (int j = 0; j < w; ++j) a.p[j] = Q[j];
-    k_multidot<<<vector_grid(), kBlock, 0, s>>>(n, z, a, w, ds.partials, ds.ticket, c);
+    launch_k(k_multidot, dim3(vgrid(n)), dim3(kBlock), 0, s, n, z, a, w, ds.partials, ds.ticket, c);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -615,6 +654,8 @@ void launch_multidot(int n, const double* z, const double* const* Q, int w, doub
 __global__ void __launch_bounds__(kBlock) k_direction(int n, const double* __restrict__ z, PtrArr D,
                                                       const double* __restrict__ c, const double* __restrict__ dq,
                                                       int w, double* __restrict__ d) {
+    pdl_trigger();
+    pdl_wait();
     double beta[kMaxWin];
 #pragma unroll
     for (int j = 0; j < kMaxWin; ++j) beta[j] = j < w ? c[j] / dq[j] : 0.0;
@@ -631,7 +672,7 @@ void launch_direction(int n, const double* z, const double* const* D, const doub
                       double* d, cudaStream_t s) {
     PtrArr a{};
     for (int j = 0; j < w; ++j) a.p[j] = D[j];
-    k_direction<<<vector_grid(), kBlock, 0, s>>>(n, z, a, c, dq, w, d);
+    launch_k(k_direction, dim3(vgrid(n)), dim3(kBlock), 0, s, n, z, a, c, dq, w, d);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -642,6 +683,8 @@ __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __re
                                                        const double* __restrict__ q, double* __restrict__ x,
                                                        double* __restrict__ r, int* breakdown, double* partials,
                                                        unsigned* ticket, double* rr) {
+    pdl_trigger();
+    pdl_wait();
     const double den = *dq;
     double alpha;
     if (breakdown) {  // outer FCG: d.q <= 0 or NaN is a breakdown
@@ -665,16 +708,18 @@ __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __re
 
 void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
                        bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s) {
-    dim3 g(vector_grid()), b(kBlock);
+    dim3 g(vgrid(n)), b(kBlock);
+    double* np = nullptr;
+    unsigned* nt = nullptr;
     if (assign_x) {
-        if (r) k_fcg_update<true, true, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
-        else   k_fcg_update<true, false, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
+        if (r) launch_k(k_fcg_update<true, true, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        else   launch_k(k_fcg_update<true, false, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
     } else if (r && rr) {
-        k_fcg_update<false, true, true><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, ds.partials, ds.ticket, rr);
+        launch_k(k_fcg_update<false, true, true>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, ds.partials, ds.ticket, rr);
     } else if (r) {
-        k_fcg_update<false, true, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
+        launch_k(k_fcg_update<false, true, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
     } else {
-        k_fcg_update<false, false, false><<<g, b, 0, s>>>(n, dr, dq, d, q, x, r, breakdown, nullptr, nullptr, nullptr);
+        launch_k(k_fcg_update<false, false, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
     }
     CK(cudaGetLastError());
     ++g_launches;
@@ -682,6 +727,8 @@ void launch_fcg_update(int n, const double* dr, const double* dq, const double* 
 
 __global__ void __launch_bounds__(kBlock) k_dot(int n, const double* __restrict__ x, const double* __restrict__ y,
                                                 double* partials, unsigned* ticket, double* out) {
+    pdl_trigger();
+    pdl_wait();
     double acc[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         acc[0] += x[i] * (y ? y[i] : 1.0);
@@ -689,29 +736,33 @@ __global__ void __launch_bounds__(kBlock) k_dot(int n, const double* __restrict_
 }
 
 void launch_dot(int n, const double* x, const double* y, double* out, const DotScratch& ds, cudaStream_t s) {
-    k_dot<<<vector_grid(), kBlock, 0, s>>>(n, x, y, ds.partials, ds.ticket, out);
+    launch_k(k_dot, dim3(vgrid(n)), dim3(kBlock), 0, s, n, x, y, ds.partials, ds.ticket, out);
     CK(cudaGetLastError());
     ++g_launches;
 }
 
 __global__ void __launch_bounds__(kBlock) k_sub_scalar(int n, double* __restrict__ v, const double* __restrict__ sum) {
+    pdl_trigger();
+    pdl_wait();
     const double mu = (*sum) / (double)n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] -= mu;
 }
 
 void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cudaStream_t s) {
     launch_dot(n, v, nullptr, tmp, ds, s);
-    k_sub_scalar<<<vector_grid(), kBlock, 0, s>>>(n, v, tmp);
+    launch_k(k_sub_scalar, dim3(vgrid(n)), dim3(kBlock), 0, s, n, v, (const double*)tmp);
     CK(cudaGetLastError());
     ++g_launches;
 }
 
 __global__ void __launch_bounds__(kBlock) k_copy(int n, const double* __restrict__ x, double* __restrict__ y) {
+    pdl_trigger();
+    pdl_wait();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = x[i];
 }
 
 void launch_copy(int n, const double* x, double* y, cudaStream_t s) {
-    k_copy<<<vector_grid(), kBlock, 0, s>>>(n, x, y);
+    launch_k(k_copy, dim3(vgrid(n)), dim3(kBlock), 0, s, n, x, y);
     CK(cudaGetLastError());
     ++g_launches;
 }

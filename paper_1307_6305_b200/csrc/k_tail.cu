@@ -213,6 +213,8 @@ __device__ __noinline__ void t_fcg(const TailArgs& A, int l, TCtx c) {
 
 template <bool CL>
 __global__ void __launch_bounds__(kTailBlock, 1) k_tail(TailArgs a) {
+    pdl_trigger();
+    pdl_wait();
     TCtx c;
     if constexpr (CL) {
         cg::cluster_group cl = cg::this_cluster();
@@ -264,7 +266,7 @@ int tail_cluster_size() {
 void launch_tail(const TailArgs& a, cudaStream_t s) {
     const int cs = tail_cluster_size();
     if (cs == 1) {
-        k_tail<false><<<1, kTailBlock, 0, s>>>(a);
+        launch_k(k_tail<false>, dim3(1), dim3(kTailBlock), 0, s, a);
         CK(cudaGetLastError());
         ++g_launches;
         return;
