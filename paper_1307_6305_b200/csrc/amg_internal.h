@@ -113,7 +113,7 @@ PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStrea
 void compose(int n, int* agg, const int* agg_t, cudaStream_t s);
 // A_H = P^T A P as entry sums in (row, CSR position) order per coarse entry (bit-exact with a
 // sequential left-to-right summation).
-Csr galerkin(const Csr& A, const int* agg, int nc, cudaStream_t s);
+Csr galerkin(const Csr& A, const int* agg, int nc, const int* perm, const int* aptr, cudaStream_t s);
 // perm = vertices sorted stably by aggregate, aptr[I] = first position of aggregate I
 void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s);
 // row tiles for the CSR SpMV-class kernels

@@ -314,7 +314,7 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         Lv.aptr = halloc<int>(h, (size_t)nc + 1);
         aggregate_order(Lv.A.n, agg, nc, Lv.perm, Lv.aptr, s);
         pt.mark("aggregate order", l);
-        h->lev[l + 1].A = galerkin(Lv.A, agg, nc, s);
+        h->lev[l + 1].A = galerkin(Lv.A, agg, nc, Lv.perm, Lv.aptr, s);
         pt.mark("galerkin", l);
         ++l;
     }

@@ -13,7 +13,9 @@
 // CUB (header-only, CUDA 12.9) supplies the radix sorts and scans.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "amg_internal.h"
@@ -533,16 +535,318 @@ static void quotient_impl(int n, int64_t nnz, const int* rp, const int* ci, cons
     *onnz = S;
 }
 
+// ------------------------------------------------------------------ row-merge quotient / Galerkin
+void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s);
+// Coarse row I is the merge of its members' rows (members = perm[aptr[I] .. aptr[I+1]), increasing
+// vertex order).  One warp per coarse row gathers the E <= 256 entries as keys (J = agg(col), k)
+// with k the entry's rank in (member, CSR position) order, bitonic-sorts them in shared memory,
+// and sums every run of equal J sequentially in k order -- the same order as the sequential
+// definition, so fp64 Galerkin values are bit-exact with it.  Rows with E > 256 (rare; only
+// very wide coarse rows) make the level fall back to the radix-sort path.
+constexpr int kRM = 256;          // entries per warp buffer
+constexpr int kRMWarps = 8;       // warps per block
+
+__global__ void k_rm_count(int nc, const int* __restrict__ rp, const int* __restrict__ perm,
+                          const int* __restrict__ aptr, int* __restrict__ E, int* __restrict__ emax) {
+    int m = 0;
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+        int e = 0;
+        for (int t = aptr[I]; t < aptr[I + 1]; ++t) e += rp[perm[t] + 1] - rp[perm[t]];
+        E[I] = e;
+        m = max(m, e);
+    }
+    atomicMax(emax, m);
+}
+
+template <class VAL>
+__global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                            const VAL* __restrict__ src, const int* __restrict__ agg,
+                                                            const int* __restrict__ perm, const int* __restrict__ aptr,
+                                                            const int* __restrict__ eoff, bool drop,
+                                                            int* __restrict__ tcol, VAL* __restrict__ tval,
+                                                            int* __restrict__ ucount) {
+    __shared__ unsigned long long skey[kRMWarps][kRM];
+    __shared__ VAL sval[kRMWarps][kRM];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned long long* key = skey[wib];
+    VAL* val = sval[wib];
+    const int nwarp = gridDim.x * kRMWarps;
+    for (int I = blockIdx.x * kRMWarps + wib; I < nc; I += nwarp) {
+        const int e0 = eoff[I], E = eoff[I + 1] - e0;
+        if (E > kRM) continue;  // wide rows: k_rm_merge_block
+        // gather in (member, position) order, k = running rank; members are spread over the lanes
+        // (one member per lane, a warp prefix sum of their row lengths gives each its first k)
+        const int t0 = aptr[I], t1 = aptr[I + 1];
+        int kbase = 0;
+        for (int tc = t0; tc < t1; tc += 32) {
+            const int t = tc + lane;
+            int p0 = 0, len = 0;
+            if (t < t1) {
+                const int v = perm[t];
+                p0 = rp[v];
+                len = rp[v + 1] - p0;
+            }
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int kk = kbase + incl - len;
+            for (int q = 0; q < len; ++q) {
+                const int J = agg[ci[p0 + q]];
+                const unsigned long long hi = (drop && J == I) ? 0xFFFFFFFFull : (unsigned long long)(unsigned)J;
+                key[kk + q] = (hi << 32) | (unsigned)(kk + q);
+                val[kk + q] = src[p0 + q];
+            }
+            kbase += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        int P = 1;
+        while (P < E) P <<= 1;
+        for (int q = E + lane; q < P; q += 32) key[q] = ~0ull;
+        __syncwarp();
+        // bitonic sort of key[0..P) (ascending)
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int q = lane; q < P; q += 32) {
+                    const int partner = q ^ stride;
+                    if (partner > q) {
+                        const bool up = (q & size) == 0;
+                        const unsigned long long a = key[q], b = key[partner];
+                        if ((a > b) == up) { key[q] = b; key[partner] = a; }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        // runs of equal J: heads, ranks, sequential sums in k order
+        int base = 0;
+        for (int q0 = 0; q0 < E; q0 += 32) {
+            const int q = q0 + lane;
+            bool head = false;
+            unsigned J = 0xFFFFFFFFu;
+            if (q < E) {
+                J = (unsigned)(key[q] >> 32);
+                head = J != 0xFFFFFFFFu && (q == 0 || (unsigned)(key[q - 1] >> 32) != J);
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                const int slot = e0 + base + __popc(hm & ((1u << lane) - 1));
+                VAL acc = val[(unsigned)(key[q] & 0xFFFFFFFFull)];
+                for (int r = q + 1; r < E && (unsigned)(key[r] >> 32) == J; ++r) acc += val[(unsigned)(key[r] & 0xFFFFFFFFull)];
+                tcol[slot] = (int)J;
+                tval[slot] = acc;
+            }
+            base += __popc(hm);
+        }
+        if (lane == 0) ucount[I] = base;
+        __syncwarp();
+    }
+}
+
+
+// Same merge for the rare wide coarse rows (kRM < E <= kRMB), one 256-thread CTA per row with the
+// buffers in dynamic shared memory.
+constexpr int kRMB = 4096;
+template <class VAL>
+__global__ void __launch_bounds__(256) k_rm_merge_block(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                        const VAL* __restrict__ src, const int* __restrict__ agg,
+                                                        const int* __restrict__ perm, const int* __restrict__ aptr,
+                                                        const int* __restrict__ eoff, bool drop,
+                                                        int* __restrict__ tcol, VAL* __restrict__ tval,
+                                                        int* __restrict__ ucount, const int* __restrict__ wide,
+                                                        int nwide) {
+    extern __shared__ __align__(16) unsigned char rmb_raw[];
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(rmb_raw);
+    VAL* val = reinterpret_cast<VAL*>(key + kRMB);
+    __shared__ int wsum[9];
+    for (int wi = blockIdx.x; wi < nwide; wi += gridDim.x) {
+        const int I = wide[wi];
+        const int e0 = eoff[I], E = eoff[I + 1] - e0;
+        int k = 0;
+        for (int t = aptr[I]; t < aptr[I + 1]; ++t) {
+            const int v = perm[t], p0 = rp[v], len = rp[v + 1] - p0;
+            for (int q = threadIdx.x; q < len; q += blockDim.x) {
+                const int J = agg[ci[p0 + q]];
+                const unsigned long long hi = (drop && J == I) ? 0xFFFFFFFFull : (unsigned long long)(unsigned)J;
+                key[k + q] = (hi << 32) | (unsigned)(k + q);
+                val[k + q] = src[p0 + q];
+            }
+            k += len;
+        }
+        int P = 1;
+        while (P < E) P <<= 1;
+        for (int q = E + threadIdx.x; q < P; q += blockDim.x) key[q] = ~0ull;
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int q = threadIdx.x; q < P; q += blockDim.x) {
+                    const int partner = q ^ stride;
+                    if (partner > q) {
+                        const bool up = (q & size) == 0;
+                        const unsigned long long a = key[q], b = key[partner];
+                        if ((a > b) == up) { key[q] = b; key[partner] = a; }
+                    }
+                }
+                __syncthreads();
+            }
+        // heads and ranks in chunks of blockDim (block-wide exclusive count via per-warp popc)
+        int base = 0;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int q0 = 0; q0 < E; q0 += blockDim.x) {
+            const int q = q0 + threadIdx.x;
+            bool head = false;
+            unsigned J = 0xFFFFFFFFu;
+            if (q < E) {
+                J = (unsigned)(key[q] >> 32);
+                head = J != 0xFFFFFFFFu && (q == 0 || (unsigned)(key[q - 1] >> 32) != J);
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            if (lane == 0) wsum[wid] = __popc(hm);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int acc = 0;
+                for (int w = 0; w < 8; ++w) { int t = wsum[w]; wsum[w] = acc; acc += t; }
+                wsum[8] = acc;
+            }
+            __syncthreads();
+            if (head) {
+                const int slot = e0 + base + wsum[wid] + __popc(hm & ((1u << lane) - 1));
+                VAL acc = val[(unsigned)(key[q] & 0xFFFFFFFFull)];
+                for (int r = q + 1; r < E && (unsigned)(key[r] >> 32) == J; ++r) acc += val[(unsigned)(key[r] & 0xFFFFFFFFull)];
+                tcol[slot] = (int)J;
+                tval[slot] = acc;
+            }
+            base += wsum[8];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) ucount[I] = base;
+        __syncthreads();
+    }
+}
+
+__global__ void k_wide_flags(int nc, const int* __restrict__ eoff, int lim, int* __restrict__ flag) {
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x)
+        flag[I] = (eoff[I + 1] - eoff[I]) > lim;
+}
+
+__global__ void k_scatter_flagged(int n, const int* __restrict__ flag, const int* __restrict__ pos, int* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (flag[i]) out[pos[i]] = i;
+}
+
+template <class VAL>
+__global__ void k_rm_compact(int nc, const int* __restrict__ eoff, const int* __restrict__ orp,
+                             const int* __restrict__ tcol, const VAL* __restrict__ tval, int* __restrict__ ocol,
+                             VAL* __restrict__ oval) {
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+        const int src = eoff[I], dst = orp[I], u = orp[I + 1] - orp[I];
+        for (int r = 0; r < u; ++r) {
+            ocol[dst + r] = tcol[src + r];
+            oval[dst + r] = tval[src + r];
+        }
+    }
+}
+
+// returns false (nothing allocated) if some coarse row has more than kRM entries
+template <class VAL>
+static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg, int nc,
+                              bool drop, const int* perm, const int* aptr, int** orp, int** oci, VAL** oval,
+                              int64_t* onnz, cudaStream_t s) {
+    (void)n;
+    (void)nnz;
+    int* E = dalloc<int>((size_t)nc + 1, s);
+    int* emax = dalloc<int>(1, s);
+    CK(cudaMemsetAsync(emax, 0, sizeof(int), s));
+    CK(cudaMemsetAsync(E + nc, 0, sizeof(int), s));
+    k_rm_count<<<grid_for(nc), kBlock, 0, s>>>(nc, rp, perm, aptr, E, emax);
+    ++g_launches;
+    CK(cudaGetLastError());
+    const int mx = read_scalar(emax, s);
+    dfree(emax, s);
+    if (mx > kRMB) {
+        dfree(E, s);
+        return false;
+    }
+    int* eoff = dalloc<int>((size_t)nc + 1, s);
+    const int64_t tot = exclusive_scan_total(E, eoff, nc, s);
+    int* tcol = dalloc<int>((size_t)tot + 8, s);
+    VAL* tval = dalloc<VAL>((size_t)tot + 8, s);
+    int* uc = E;  // reuse: unique counts
+    CK(cudaMemsetAsync(uc + nc, 0, sizeof(int), s));
+    const int nb = (int)std::min<int64_t>((nc + kRMWarps - 1) / kRMWarps, 148LL * 16);
+    k_rm_merge<VAL><<<nb, 32 * kRMWarps, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
+    ++g_launches;
+    CK(cudaGetLastError());
+    if (mx > kRM) {  // list the wide rows, one CTA each
+        int* flag = dalloc<int>((size_t)nc + 1, s);
+        int* pos = dalloc<int>((size_t)nc + 1, s);
+        CK(cudaMemsetAsync(flag + nc, 0, sizeof(int), s));
+        k_wide_flags<<<grid_for(nc), kBlock, 0, s>>>(nc, eoff, kRM, flag);
+        ++g_launches;
+        const int nwide = (int)exclusive_scan_total(flag, pos, nc, s);
+        int* wide = dalloc<int>((size_t)nwide + 1, s);
+        k_scatter_flagged<<<grid_for(nc), kBlock, 0, s>>>(nc, flag, pos, wide);
+        ++g_launches;
+        const size_t sm = (size_t)kRMB * (sizeof(unsigned long long) + sizeof(VAL));
+        static bool cfg = false;
+        if (!cfg) {
+            CK(cudaFuncSetAttribute(k_rm_merge_block<VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            cfg = true;
+        }
+        const int g = nwide < 148 * 2 ? (nwide > 0 ? nwide : 1) : 148 * 2;
+        k_rm_merge_block<VAL><<<g, 256, sm, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, wide,
+                                                 nwide);
+        ++g_launches;
+        CK(cudaGetLastError());
+        dfree(flag, s);
+        dfree(pos, s);
+        dfree(wide, s);
+    }
+    int* nrp = dalloc<int>((size_t)nc + 1, s);
+    const int64_t S = exclusive_scan_total(uc, nrp, nc, s);
+    int* ocol = dalloc<int>((size_t)S + 8, s);
+    VAL* ov = dalloc<VAL>((size_t)S + 8, s);
+    CK(cudaMemsetAsync(ocol + S, 0, 8 * sizeof(int), s));
+    CK(cudaMemsetAsync(ov + S, 0, 8 * sizeof(VAL), s));
+    k_rm_compact<VAL><<<grid_for(nc), kBlock, 0, s>>>(nc, eoff, nrp, tcol, tval, ocol, ov);
+    ++g_launches;
+    CK(cudaGetLastError());
+    dfree(tcol, s);
+    dfree(tval, s);
+    dfree(eoff, s);
+    dfree(E, s);
+    *orp = nrp;
+    *oci = ocol;
+    *oval = ov;
+    *onnz = S;
+    return true;
+}
+
 PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStream_t s) {
     PassGraph H;
     H.n = nc;
+    if (!getenv("AMG_RADIX_QUOTIENT")) {
+        int* perm = dalloc<int>((size_t)G.n + 8, s);
+        int* aptr = dalloc<int>((size_t)nc + 8, s);
+        aggregate_order(G.n, agg_t, nc, perm, aptr, s);
+        const bool ok = quotient_rowmerge<uint32_t>(G.n, G.nnz, G.rp, G.ci, G.w, agg_t, nc, true, perm, aptr, &H.rp,
+                                                    &H.ci, &H.w, &H.nnz, s);
+        dfree(perm, s);
+        dfree(aptr, s);
+        if (ok) return H;
+    }
     quotient_impl<uint32_t>(G.n, G.nnz, G.rp, G.ci, G.w, agg_t, nc, true, &H.rp, &H.ci, &H.w, &H.nnz, s);
     return H;
 }
 
-Csr galerkin(const Csr& A, const int* agg, int nc, cudaStream_t s) {
+Csr galerkin(const Csr& A, const int* agg, int nc, const int* perm, const int* aptr, cudaStream_t s) {
     Csr H;
     H.n = nc;
+    if (!getenv("AMG_RADIX_QUOTIENT") &&
+        quotient_rowmerge<double>(A.n, A.nnz, A.rp, A.ci, A.v, agg, nc, false, perm, aptr, &H.rp, &H.ci, &H.v, &H.nnz,
+                                  s))
+        return H;
     quotient_impl<double>(A.n, A.nnz, A.rp, A.ci, A.v, agg, nc, false, &H.rp, &H.ci, &H.v, &H.nnz, s);
     return H;
 }
@@ -814,7 +1118,8 @@ __global__ void k_dict_build(const unsigned long long* gv, const unsigned long l
 
 __global__ void __launch_bounds__(kBlock) k_sell_encode(Sell S, int vmode, int cmode, const double* __restrict__ vdict,
                                                         int nvd, const int* __restrict__ cdict, int ncd,
-                                                        uint8_t* vcode, uint8_t* ccode, int16_t* coff) {
+                                                        uint8_t* vcode, uint8_t* ccode, int16_t* coff,
+                                                        uint16_t* pcode) {
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < S.nslices; sl += nw) {
@@ -822,22 +1127,23 @@ __global__ void __launch_bounds__(kBlock) k_sell_encode(Sell S, int vmode, int c
         const int i = sl * 32 + lane;
         for (int j = 0; j < w; ++j) {
             const size_t e = ((size_t)b + j) * 32 + lane;
+            int vc = 0;
             if (vmode == 1) {
                 const double x = S.val[e];
                 const unsigned long long xb = (unsigned long long)__double_as_longlong(x);
-                int lo = 0;
                 for (int k = 0; k < nvd; ++k)  // <= 256 entries, exact bit match
-                    if ((unsigned long long)__double_as_longlong(vdict[k]) == xb) { lo = k; break; }
-                vcode[e] = (uint8_t)lo;
+                    if ((unsigned long long)__double_as_longlong(vdict[k]) == xb) { vc = k; break; }
+                if (cmode != 3) vcode[e] = (uint8_t)vc;
             }
             const int off = i < S.n ? S.col[e] - i : 0;
-            if (cmode == 1) {
+            if (cmode == 1 || cmode == 3) {
                 int lo = 0, hi = ncd;
                 while (lo < hi) {
                     int mid = (lo + hi) >> 1;
                     if (cdict[mid] < off) lo = mid + 1; else hi = mid;
                 }
-                ccode[e] = (uint8_t)lo;
+                if (cmode == 1) ccode[e] = (uint8_t)lo;
+                else pcode[e] = (uint16_t)(vc | (lo << 8));
             } else if (cmode == 2) {
                 coff[e] = (int16_t)off;
             }
@@ -865,8 +1171,16 @@ __global__ void k_minmax_off(Sell S, int* mm) {
             mx = max(mx, off);
         }
     }
-    atomicMin(mm, mn);
-    atomicMax(mm + 1, mx);
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+        atomicMin(mm, mn);
+        atomicMax(mm + 1, mx);
+    }
 }
 
 void free_sell(Sell& S, cudaStream_t s) {
@@ -903,25 +1217,17 @@ void compress_sell(Sell& S, const Csr& A, cudaStream_t s) {
         S.nvdict = S.vmode ? nv : 0;
         S.ncdict = S.cmode == 1 ? nc : 0;
         k_dict_build<<<1, 1024, 0, s>>>(gv, gc, S.vdict, S.cdict, S.vmode ? 256 : 0, S.cmode == 1 ? 256 : 0);
+        S.ncdict = S.cmode == 1 ? nc : 0;
         ++g_launches;
-        if (S.vmode) S.vcode = dalloc<uint8_t>((size_t)S.padded + 64, s);
+        if (S.vmode == 1 && S.cmode == 1) S.cmode = 3;  // one 2-byte code pair load per entry
+        if (S.vmode && S.cmode != 3) S.vcode = dalloc<uint8_t>((size_t)S.padded + 64, s);
         if (S.cmode == 1) S.ccode = dalloc<uint8_t>((size_t)S.padded + 64, s);
         if (S.cmode == 2) S.coff = dalloc<int16_t>((size_t)S.padded + 64, s);
+        if (S.cmode == 3) S.pcode = dalloc<uint16_t>((size_t)S.padded + 64, s);
         k_sell_encode<<<g, kBlock, 0, s>>>(S, S.vmode, S.cmode, S.vdict, S.nvdict, S.cdict, S.ncdict, S.vcode,
-                                           S.ccode, S.coff);
+                                           S.ccode, S.coff, S.pcode);
         ++g_launches;
         CK(cudaGetLastError());
-        if (S.vmode == 1 && S.cmode == 1) {  // one 2-byte load per entry instead of two 1-byte loads
-            S.pcode = dalloc<uint16_t>((size_t)S.padded + 64, s);
-            k_pair_codes<<<grid_for(S.padded), kBlock, 0, s>>>(S.padded, S.vcode, S.ccode, S.pcode);
-            ++g_launches;
-            CK(cudaGetLastError());
-            dfree(S.vcode, s);
-            dfree(S.ccode, s);
-            S.vcode = nullptr;
-            S.ccode = nullptr;
-            S.cmode = 3;
-        }
         // the replaced full-width streams are no longer needed by the solve
         if (S.vmode) { dfree(S.val, s); S.val = nullptr; }
         if (S.cmode) { dfree(S.col, s); S.col = nullptr; }
