@@ -53,6 +53,9 @@ extern "C" {
 #define AMG_E_SETUP        (-7) /* coarsening stagnated (n_{l+1} = n_l) above the coarsest size */
 
 typedef struct amg_hierarchy* amg_handle; /* opaque, library-owned */
+typedef struct amg_comm_s* amg_comm;       /* opaque communicator of the row-partitioned path */
+
+#define AMG_COMM_ID_BYTES 128              /* size of an NCCL unique id */
 
 typedef struct {
     int64_t  coarsest_size; /* stop coarsening once n_l <= this ("< 100"); default 100 */
@@ -69,7 +72,10 @@ typedef struct {
     int64_t  tail_nnz;      /* the first level l >= 1 with nnz(A_l) <= tail_nnz and every level below it
                                run inside one single-CTA kernel per visit (coarse-tail megakernel);
                                0 disables; default 8192 */
-    int64_t  reserved[5];
+    int64_t  gather_rows;   /* amg_setup_dist only: the first level with fewer than gather_rows rows
+                               (and always the coarsest) is gathered onto every rank, which runs the
+                               rest of the hierarchy redundantly; default 50000 */
+    int64_t  reserved[4];
 } amg_options;
 
 typedef struct {
@@ -102,6 +108,8 @@ typedef struct {
                                          value+column stream bytes (12 uncompressed; 2 for paired 1-byte
                                          codes), plus 32 n_0 for the four vectors */
     int32_t  level0_format;           /* 0 CSR tiles, 1 SELL-32 fp64/int32, 2 SELL-32 compressed */
+    int32_t  nranks;                  /* ranks of the communicator (1 for amg_setup) */
+    int32_t  dist_levels;             /* number of row-partitioned levels g (levels >= g are replicated) */
     int32_t  reserved1;
 } amg_info;
 
@@ -140,6 +148,44 @@ int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t*
 int amg_solve(amg_handle h, const double* b, double* x, double tol, int32_t k_inner, int32_t* iters,
               double* relres);
 
+/* ---------------------------------------------------------------------------------------------
+ * Row-partitioned multi-GPU path.  One process (or, for testing,
+ * one host thread) per rank.  Levels are row-partitioned with DECOUPLED aggregation (reading A20:
+ * the matching passes of a partitioned level use only the edges inside each block, so aggregates,
+ * restriction and prolongation are rank-local and the coarse blocks are the fine blocks'
+ * aggregates).  Every SpMV-class pass exchanges a halo (grouped point-to-point messages), every FCG
+ * dot batch is allgathered and summed in rank order (identical scalars on every rank), and the
+ * first level below opt->gather_rows (at the latest the coarsest) is gathered once at setup and
+ * then run redundantly on every rank.  All calls on a distributed handle are collective.
+ * ------------------------------------------------------------------------------------------- */
+/* NCCL unique id (rank 0 creates it and sends the AMG_COMM_ID_BYTES bytes to the other ranks,
+ * e.g. with torch.distributed).  Returns AMG_E_NCCL if libnccl.so.2 cannot be loaded. */
+int amg_comm_unique_id(uint8_t* id);
+/* NCCL communicator over the current CUDA device (collective over the nranks processes). */
+int amg_comm_init_nccl(amg_comm* out, const uint8_t* id, int32_t nranks, int32_t rank);
+/* nranks communicators out[0..nranks) for nranks host threads of THIS process sharing the current
+ * device (single-GPU emulation of the multi-rank path for tests: each exchange synchronises the
+ * caller's stream and meets the other threads at a host barrier; CUDA graphs are not used). */
+int amg_comm_init_threads(amg_comm* out, int32_t nranks);
+int amg_comm_rank(amg_comm c, int32_t* rank, int32_t* size);
+/* Releases a communicator (after every handle that uses it).  NULL is a no-op. */
+int amg_comm_free(amg_comm c);
+
+/*
+ * amg_setup_dist -- collective amg_setup over the ranks of `comm`.
+ *   n_global    rows of the whole problem
+ *   row_begin   first global row of this rank; the ranks' blocks [row_begin, row_begin + n_local)
+ *               must tile [0, n_global) in rank order (AMG_E_ARG on every rank otherwise)
+ *   n_local     rows of this rank (>= 1)
+ *   row_ptr     int64[n_local+1] of this rank's rows; col int32 GLOBAL column ids; val, d as in
+ *               amg_setup (d: this rank's n_local entries, or NULL on every rank)
+ * Cross-block symmetry of the values is the caller's contract (the pattern is checked through the
+ * halo requests).  amg_solve on the handle takes this rank's blocks of b and x (n_local each).
+ */
+int amg_setup_dist(amg_handle* out, amg_comm comm, int64_t n_global, int64_t row_begin, int64_t n_local,
+                   const int64_t* row_ptr, const int32_t* col_global, const double* val, const double* d,
+                   int32_t n_match_passes, int32_t poly_degree, const amg_options* opt);
+
 /* Releases the handle and all its device memory.  NULL is a no-op returning AMG_OK. */
 int amg_free(amg_handle h);
 
@@ -165,6 +211,17 @@ int amg_level_smooth(amg_handle h, int32_t level, const double* f, const double*
 int amg_level_precond(amg_handle h, int32_t level, int32_t k_inner, const double* r, double* z);
 /* e = A_L^{-1} r (or A_L^dagger r if singular) on the coarsest level. */
 int amg_coarse_solve(amg_handle h, const double* r, double* e);
+/* Partition of level l: *dist = 1 if row-partitioned (then amg_level_sizes reports this rank's rows,
+ * amg_level_export exports them with GLOBAL column ids and global coarse aggregate ids, and
+ * amg_level_smooth / amg_level_precond take this rank's blocks), 0 if every rank holds it whole. */
+int amg_level_dist(amg_handle h, int32_t level, int32_t* dist, int64_t* row_begin, int64_t* n_global);
+/* Host-only (no CUDA): the halo receive plan of one block -- for the sorted unique global ids of the
+ * columns outside [row_begin, row_begin + n_local), the runs owned by one rank (owner offs[q] <= id <
+ * offs[q+1]): seg_peer/seg_off (relative column of the run's first id: negative below the block,
+ * >= n_local above)/seg_cnt, *n_seg runs, *n_lo ids below the block.  Output arrays hold >= n_halo. */
+int amg_halo_plan(int64_t row_begin, int32_t n_local, const int64_t* offs, int32_t nranks, int32_t rank,
+                  const int32_t* halo_ids, int32_t n_halo, int32_t* seg_peer, int32_t* seg_off, int32_t* seg_cnt,
+                  int32_t* n_seg, int32_t* n_lo);
 
 #ifdef __cplusplus
 }

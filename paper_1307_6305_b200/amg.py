@@ -17,14 +17,17 @@ LIB_PATH = os.path.join(_HERE, "lib", "libamg_b200.so")
 AMG_OK, AMG_NOT_CONVERGED = 0, 1
 AMG_E_ARG, AMG_E_INPUT, AMG_E_CUDA, AMG_E_NCCL, AMG_E_OOM, AMG_E_BREAKDOWN, AMG_E_SETUP = -1, -2, -3, -4, -5, -6, -7
 EXPORTS = ("amg_options_default", "amg_setup", "amg_solve", "amg_free", "amg_get_info", "amg_last_error",
-           "amg_level_sizes", "amg_level_export", "amg_level_smooth", "amg_level_precond", "amg_coarse_solve")
+           "amg_level_sizes", "amg_level_export", "amg_level_smooth", "amg_level_precond", "amg_coarse_solve",
+           "amg_comm_unique_id", "amg_comm_init_nccl", "amg_comm_init_threads", "amg_comm_rank", "amg_comm_free",
+           "amg_setup_dist", "amg_level_dist", "amg_halo_plan")
+AMG_COMM_ID_BYTES = 128
 
 
 class amg_options(ctypes.Structure):
     _fields_ = [("coarsest_size", ctypes.c_int64), ("kappa", ctypes.c_double), ("restart", ctypes.c_int32),
                 ("max_iter", ctypes.c_int32), ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
                 ("use_graphs", ctypes.c_int32), ("compress", ctypes.c_int32), ("tail_nnz", ctypes.c_int64),
-                ("reserved", ctypes.c_int64 * 5)]
+                ("gather_rows", ctypes.c_int64), ("reserved", ctypes.c_int64 * 4)]
 
 
 class amg_info(ctypes.Structure):
@@ -38,7 +41,8 @@ class amg_info(ctypes.Structure):
                 ("launches_per_iter", ctypes.c_int64), ("launches_last_setup", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("prof_smoother_ms", ctypes.c_double),
                 ("prof_smoother_launches", ctypes.c_int64), ("prof_smoother_bytes", ctypes.c_int64),
-                ("level0_format", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
+                ("level0_format", ctypes.c_int32), ("nranks", ctypes.c_int32), ("dist_levels", ctypes.c_int32),
+                ("reserved1", ctypes.c_int32)]
 
 
 class AmgError(RuntimeError):
@@ -70,6 +74,15 @@ def load():
     L.amg_level_smooth.argtypes = [vp, i32, vp, vp, vp]
     L.amg_level_precond.argtypes = [vp, i32, i32, vp, vp]
     L.amg_coarse_solve.argtypes = [vp, vp, vp]
+    L.amg_comm_unique_id.argtypes = [vp]
+    L.amg_comm_init_nccl.argtypes = [ctypes.POINTER(vp), vp, i32, i32]
+    L.amg_comm_init_threads.argtypes = [vp, i32]
+    L.amg_comm_rank.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.amg_comm_free.argtypes = [vp]
+    L.amg_setup_dist.argtypes = [ctypes.POINTER(vp), vp, i64, i64, i64, vp, vp, vp, vp, i32, i32,
+                                 ctypes.POINTER(amg_options)]
+    L.amg_level_dist.argtypes = [vp, i32, vp, vp, vp]
+    L.amg_halo_plan.argtypes = [i64, i32, vp, i32, i32, vp, i32, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("amg_last_error",):
             getattr(L, name).restype = ctypes.c_int
@@ -150,7 +163,8 @@ def amg_get_info(h) -> dict:
                 launches_last_solve=inf.launches_last_solve, launches_per_iter=inf.launches_per_iter,
                 launches_last_setup=inf.launches_last_setup, device_bytes=inf.device_bytes,
                 prof_smoother_ms=inf.prof_smoother_ms, prof_smoother_launches=inf.prof_smoother_launches,
-                prof_smoother_bytes=inf.prof_smoother_bytes, level0_format=inf.level0_format)
+                prof_smoother_bytes=inf.prof_smoother_bytes, level0_format=inf.level0_format, nranks=inf.nranks,
+                dist_levels=inf.dist_levels)
 
 
 # ---------------------------------------------------------------- parity hooks (test-only)
@@ -186,6 +200,76 @@ def amg_level_precond(h, level: int, k_inner: int, r, z):
 
 def amg_coarse_solve(h, r, e):
     _check(load().amg_coarse_solve(h, _ptr(r, np.float64), _ptr(e, np.float64)), "amg_coarse_solve")
+
+
+# ---------------------------------------------------------------- row-partitioned path (multi-GPU)
+def amg_comm_unique_id() -> bytes:
+    """NCCL unique id (rank 0), to be sent to the other ranks (e.g. torch.distributed.broadcast)."""
+    buf = (ctypes.c_uint8 * AMG_COMM_ID_BYTES)()
+    _check(load().amg_comm_unique_id(ctypes.addressof(buf)), "amg_comm_unique_id")
+    return bytes(buf)
+
+
+def amg_comm_init_nccl(uid: bytes, nranks: int, rank: int):
+    """NCCL communicator of this process over the current CUDA device (collective)."""
+    if len(uid) != AMG_COMM_ID_BYTES:
+        raise ValueError("unique id must be AMG_COMM_ID_BYTES bytes")
+    c = ctypes.c_void_p()
+    buf = (ctypes.c_uint8 * AMG_COMM_ID_BYTES).from_buffer_copy(uid)
+    _check(load().amg_comm_init_nccl(ctypes.byref(c), ctypes.addressof(buf), nranks, rank), "amg_comm_init_nccl")
+    return c
+
+
+def amg_comm_init_threads(nranks: int):
+    """nranks communicators for nranks host threads of this process on the current device (tests)."""
+    arr = (ctypes.c_void_p * nranks)()
+    _check(load().amg_comm_init_threads(ctypes.addressof(arr), nranks), "amg_comm_init_threads")
+    return [ctypes.c_void_p(arr[r]) for r in range(nranks)]
+
+
+def amg_comm_rank(c):
+    r, n = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().amg_comm_rank(c, ctypes.byref(r), ctypes.byref(n)), "amg_comm_rank")
+    return r.value, n.value
+
+
+def amg_comm_free(c):
+    if c is not None and c.value:
+        load().amg_comm_free(c)
+        c.value = None
+
+
+def amg_setup_dist(comm, n_global: int, row_begin: int, row_ptr, col_global, val, d, n_match_passes: int,
+                   poly_degree: int, opts: amg_options | None = None):
+    """Collective setup of this rank's row block [row_begin, row_begin + n_local) (global column ids)."""
+    h = ctypes.c_void_p()
+    n_local = (row_ptr.shape[0] if hasattr(row_ptr, "shape") else len(row_ptr)) - 1
+    st = load().amg_setup_dist(ctypes.byref(h), comm, n_global, row_begin, n_local, _ptr(row_ptr, np.int64),
+                               _ptr(col_global, np.int32), _ptr(val, np.float64), _ptr(d, np.float64),
+                               n_match_passes, poly_degree, ctypes.byref(opts) if opts is not None else None)
+    _check(st, "amg_setup_dist")
+    return h
+
+
+def amg_level_dist(h, level: int):
+    dist, rb, ng = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+    _check(load().amg_level_dist(h, level, ctypes.byref(dist), ctypes.byref(rb), ctypes.byref(ng)),
+           "amg_level_dist")
+    return dict(dist=bool(dist.value), row_begin=rb.value, n_global=ng.value)
+
+
+def amg_halo_plan(row_begin: int, n_local: int, offs, rank: int, halo_ids):
+    """Host-only halo receive plan (no CUDA): list of (peer, relative offset, count) runs and n_lo."""
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    ids = np.ascontiguousarray(halo_ids, dtype=np.int32)
+    m = max(1, ids.shape[0])
+    peer, off, cnt = (np.zeros(m, np.int32) for _ in range(3))
+    nseg, nlo = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().amg_halo_plan(row_begin, n_local, offs.ctypes.data, offs.shape[0] - 1, rank, ids.ctypes.data,
+                                ids.shape[0], peer.ctypes.data, off.ctypes.data, cnt.ctypes.data, ctypes.byref(nseg),
+                                ctypes.byref(nlo)), "amg_halo_plan")
+    k = nseg.value
+    return [(int(peer[i]), int(off[i]), int(cnt[i])) for i in range(k)], nlo.value
 
 
 class Solver:

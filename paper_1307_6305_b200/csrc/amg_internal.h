@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <vector>
 
 namespace amg {
 
@@ -23,6 +24,8 @@ struct Error : std::runtime_error {
 };
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+void set_last_error(const std::string& msg);  // amg_last_error() text of the calling thread
+std::string validation_message(int flags);    // text of validate_input's flags
 #define CK(call) ::amg::cuda_check((call), #call, __FILE__, __LINE__)
 
 // ---------------------------------------------------------------- device views
@@ -49,6 +52,7 @@ struct Sell {          // SELL-32: 32-row slices, entries column-major inside a 
     double* val = nullptr;
     int64_t padded = 0;    // 32 * sptr[nslices]
     int wmax = 0;          // maximum slice width (selects the kernel's width bucket)
+    int chi = 0;           // largest valid column index (n-1; n+nhi-1 with an upper halo) -- decode clamp
     // lossless compressed streams (same slice layout), chosen per level at setup:
     int vmode = 0;         // 0: val (fp64); 1: vcode (uint8) into vdict (<= 256 distinct values)
     int cmode = 0;         // 0: col (int32); 1: ccode (uint8) into cdict of offsets col-row; 2: coff (int16 col-row);
@@ -88,7 +92,9 @@ T* dalloc(size_t n, cudaStream_t s) {
 void dfree(void* p, cudaStream_t s);
 
 // validation of the user CSR (reading A17).  Returns bit flags (0 = valid).
-int validate_input(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s);
+// Columns must lie in [cmin, cmax) ([0, n) on one GPU; [-nlo, n+nhi) relative on a row-partitioned level).
+int validate_input(int n, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v, const double* d,
+                   cudaStream_t s);
 // A_0 = L + diag(d) with inserted missing diagonals; returns a fresh Csr.
 Csr form_A0(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s);
 // lambda_1 = max_i sum_j |a_ij|  (exact: per-row sums in CSR order, max by ordered-int atomicMax)
@@ -103,17 +109,22 @@ struct PassGraph {     // matching pass graph G_t: CSR with integer multipliciti
     int* ci = nullptr;
     uint32_t* w = nullptr;
 };
+// off-diagonal entries with 0 <= col < n only (a row-partitioned level keeps its in-block edges: A20)
 PassGraph pass_graph0(const Csr& A, cudaStream_t s);
 void free_graph(PassGraph& g, cudaStream_t s);
 // one aggregation pass: handshake matching + attach + leader numbering.  agg_t[v] in [0, *nc).
-int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* rounds, cudaStream_t s);
+// id_off = global id of local vertex 0 (hash keys use global ids, docs/keys.md); 0 on one GPU.
+int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, int* nc, int* rounds, cudaStream_t s);
 // G_{t+1} = quotient of G_t under agg_t (multiplicities summed, self-loops dropped)
 PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStream_t s);
 // agg[i] = agg_t[agg[i]]
 void compose(int n, int* agg, const int* agg_t, cudaStream_t s);
 // A_H = P^T A P as entry sums in (row, CSR position) order per coarse entry (bit-exact with a
-// sequential left-to-right summation).
-Csr galerkin(const Csr& A, const int* agg, int nc, const int* perm, const int* aptr, cudaStream_t s);
+// sequential left-to-right summation).  Rows map through agg (perm/aptr), columns through cmap
+// (nullptr = agg); coarse columns lie in [0, ncols) (ncols = nc on one GPU; on a row-partitioned
+// level cmap is the shifted coarse column of every local/halo column, see dist.cu).
+Csr galerkin(const Csr& A, const int* agg, const int* cmap, int nc, int ncols, const int* perm, const int* aptr,
+             cudaStream_t s);
 // perm = vertices sorted stably by aggregate, aptr[I] = first position of aggregate I
 void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s);
 // row tiles for the CSR SpMV-class kernels
@@ -130,7 +141,7 @@ void free_csr(Csr& A, cudaStream_t s);
 
 // ---------------------------------------------------------------- solve launchers (k_solve.cu)
 // Count of kernels launched through these launchers (for the gpu_launches report).
-extern long long g_launches;
+extern thread_local long long g_launches;
 
 // SpMV-class fused kernels (one pass over A_l):
 //  smooth: out_i = alpha*cg*xg_i + (1-alpha)*prev_i + beta*(f_i - cg*(A xg)_i),
@@ -162,6 +173,8 @@ void launch_fcg_update(int n, const double* dr, const double* dq, const double* 
                        bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s);
 // v -= mean(v) (two kernels: sum then subtract); tmp = one device double
 void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cudaStream_t s);
+// v -= (*sum) / ntot  (the second half of a mean projection whose sum was allreduced)
+void launch_sub_mean(int n, double ntot, double* v, const double* sum, cudaStream_t s);
 // y = x (device copy kernel)
 void launch_copy(int n, const double* x, double* y, cudaStream_t s);
 // dot = x.y (deterministic)
@@ -227,4 +240,37 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
 int vector_grid();
 void init_device_props();
 
+// ---------------------------------------------------------------- communicator (comm.cu)
+// The three exchange steps of the row-partitioned path: a grouped point-to-point
+// exchange (halo, allgatherv) and an equal-size allgather (batched dot partials).  Both are
+// stream-ordered.  Two backends:
+//   * NCCL (one process per GPU, over NVLink / NVSwitch), capturable into CUDA graphs;
+//   * in-process host threads sharing one device (test emulation of P ranks on one GPU): each
+//     call synchronises the caller's stream, meets the other ranks at a host barrier, copies
+//     peer buffers with device-to-device cudaMemcpyAsync, and meets them again.  No kernel ever
+//     waits on another rank's kernel; not capturable.
+struct P2P {
+    int peer;
+    void* ptr;
+    size_t bytes;
+};
+struct Comm {
+    int rank = 0, size = 1;
+    virtual ~Comm() {}
+    // sends[k] goes to sends[k].peer; recvs[k] arrives from recvs[k].peer.  Messages between one
+    // pair of ranks are matched in order.  A peer may not be the caller itself.
+    virtual void sendrecv(const std::vector<P2P>& sends, const std::vector<P2P>& recvs, cudaStream_t s) = 0;
+    // out[r * bytes .. (r+1) * bytes) = rank r's in[0 .. bytes) (device buffers, out != in)
+    virtual void allgather(const void* in, void* out, size_t bytes, cudaStream_t s) = 0;
+    virtual bool capturable() const = 0;
+    virtual const char* kind() const = 0;
+    virtual void abort() {}  // wake and fail the other ranks after a local error (thread backend)
+};
+
 }  // namespace amg
+
+// opaque C-ABI communicator object (include/amg.h amg_comm)
+struct amg_comm_s {
+    amg::Comm* c = nullptr;
+};
+

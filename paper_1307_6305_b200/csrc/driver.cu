@@ -20,6 +20,7 @@
 
 #include "../../include/amg.h"
 #include "amg_internal.h"
+#include "hierarchy.h"
 
 namespace amg {
 
@@ -38,6 +39,8 @@ using namespace amg;
 
 static thread_local std::string g_last_error;
 
+void amg::set_last_error(const std::string& msg) { g_last_error = msg; }
+
 static int fail(int code, const std::string& msg) {
     g_last_error = msg;
     return code;
@@ -45,7 +48,7 @@ static int fail(int code, const std::string& msg) {
 
 // ------------------------------------------------------------------ host scalar math
 // SplitMix64 (docs/keys.md) -- the salt of the matching keys.
-static uint64_t host_sm64(uint64_t z) {
+uint64_t amg::host_sm64(uint64_t z) {
     z += 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
@@ -57,7 +60,7 @@ static double Em_of(int m, double kappa) { return std::pow(delta_of(kappa), m) *
 
 // Reading A8 (rule R1): kappa = 10 if E_m(10) < 1, else the kappa with E_m = 1/2:
 // t = sqrt(kappa) solves (t-1)^(m+1) = (t+1)^(m-1) (Newton from t = 3, then stop at a fixed point).
-static double kappa_rule(int m) {
+double amg::kappa_rule(int m) {
     if (Em_of(m, 10.0) < 1.0) return 10.0;
     double t = 3.0;
     for (int it = 0; it < 200; ++it) {
@@ -71,71 +74,13 @@ static double kappa_rule(int m) {
 }
 
 // Three-term recurrence coefficients: x_{k+1} = a_k x_k + (1-a_k) x_{k-1} + b_k (f - A x_k)
-static void poly_coeffs(double l1, double kappa, int m, double* a, double* b) {
+void amg::poly_coeffs(double l1, double kappa, int m, double* a, double* b) {
     const double l0 = l1 / kappa, d = delta_of(kappa), d2 = d * d;
     for (int k = 0; k <= m; ++k) {
         if (k == 0) { a[k] = 1.0; b[k] = (l0 + l1) / (2.0 * l0 * l1); }
         else if (k == 1) { a[k] = 1.0 + 2.0 * d2 * (1.0 - d2) / ((1.0 + d2) * (1.0 + d2)); b[k] = 2.0 / (l0 + l1); }
         else { a[k] = 1.0 + d2; b[k] = 4.0 * d / (l1 - l0); }
     }
-}
-
-// ------------------------------------------------------------------ hierarchy
-struct Level {
-    Csr A;
-    Tiles T;
-    Sell S;
-    SpOp op;  // the format the SpMV-class kernels use on this level
-    double lambda1 = 0, kappa = 0;
-    double alpha[kMaxDeg + 1] = {}, beta[kMaxDeg + 1] = {};
-    int nc = 0;
-    int* agg = nullptr;
-    int* perm = nullptr;
-    int* aptr = nullptr;
-    int rounds[kMaxDeg] = {};
-    // workspaces
-    double *X = nullptr, *XA = nullptr, *RES = nullptr;  // B_l
-    double *RHO = nullptr, *E = nullptr;                  // written / read by the parent level
-    double *Z = nullptr, *D = nullptr, *Q = nullptr;      // inner FCG (nu slots)
-    double* sc = nullptr;                                 // dq[kMaxWin], dr[kMaxWin], c[kMaxWin]
-};
-
-struct amg_hierarchy {
-    cudaStream_t s = nullptr;
-    cudaStream_t user = nullptr;
-    int L = 0, m = 0, p = 0;
-    bool singular = false;
-    amg_options opt{};
-    Level lev[kMaxLevels];
-    double* Minv = nullptr;
-    // outer FCG
-    int n = 0, W = 5;
-    double *b = nullptr, *x = nullptr, *r = nullptr, *Z = nullptr, *D = nullptr, *Q = nullptr;
-    double* osc = nullptr;  // dq[kMaxWin], c[kMaxWin], dr, rr, bb, tmp, rr_true
-    int* flag = nullptr;
-    double* hsc = nullptr;  // pinned host mirror: rr, flag
-    DotScratch ds;
-    int nu_ws = 0;          // nu the inner workspaces are sized for
-    int l_tail = 0;         // first level run by the coarse-tail cluster kernel (L = none)
-    TLevel* d_tlev = nullptr;  // device copy of the tail level descriptors
-    std::vector<cudaGraphExec_t> graphs;
-    int graph_nu = 0;
-    long long graph_launches = 0;
-    std::vector<void*> allocs;
-    std::vector<void*> ws_allocs;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    cudaEvent_t pe0 = nullptr, pe1 = nullptr;  // live profile of the level-0 smoother steps
-    bool prof_on = false;
-    int64_t bytes = 0;
-    amg_info info{};
-};
-
-template <class T>
-static T* halloc(amg_hierarchy* h, size_t n, bool ws = false) {
-    T* p = dalloc<T>(n + 8, h->s);  // +8: padding for the 16-byte vector loads
-    (ws ? h->ws_allocs : h->allocs).push_back(p);
-    h->bytes += (int64_t)((n + 8) * sizeof(T));
-    return p;
 }
 
 static bool is_device_ptr(const void* p) {
@@ -225,6 +170,7 @@ struct PhaseTimer {
         t0 = t;
     }
 };
+// Single GPU: stage and validate the caller's CSR (reading A17), A_0 = L + diag(d) (Eq. (prob)).
 static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int32_t* ci_in, const double* v_in,
                   const double* d_in) {
     cudaStream_t s = h->s;
@@ -253,25 +199,40 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     const double* v = stage_in(v_in, (size_t)nnz_in, s, &t_v);
     const double* d = stage_in(d_in, (size_t)n, s, &t_d);
     pt.mark("stage inputs");
-    int vf = validate_input(n, rp, ci, v, d, s);
+    int vf = validate_input(n, 0, n, rp, ci, v, d, s);
     pt.mark("validate");
     if (vf) {
         dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
-        char buf[128];
-        snprintf(buf, sizeof(buf), "invalid CSR input (flags 0x%x: 1 range, 2 unsorted, 4 positive off-diagonal, "
-                 "8 asymmetric, 16 diagonal, 32 d<0, 64 row_ptr)", vf);
-        throw Error(AMG_E_INPUT, buf);
+        throw Error(AMG_E_INPUT, validation_message(vf));
     }
     h->singular = !(d && any_nonzero(n, d, s));
     h->lev[0].A = form_A0(n, rp, ci, v, d, s);
     dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
-    h->n = n;
+    h->L = 1;
     pt.mark("form A0");
+    build_levels(h, 0);
+    finish_build(h);
+}
 
+std::string amg::validation_message(int vf) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "invalid CSR input (flags 0x%x: 1 range, 2 unsorted, 4 positive off-diagonal, "
+             "8 asymmetric, 16 diagonal, 32 d<0, 64 row_ptr)", vf);
+    return buf;
+}
+
+// Level loop from level l0, whose operator every rank holds whole: lambda_1,
+// kappa and coefficients, p matching passes composed into agg_l, the aggregate order and the
+// Galerkin product, until n_l <= coarsest_size.
+void amg::build_levels(amg_hierarchy* h, int l0) {
+    cudaStream_t s = h->s;
+    PhaseTimer pt(s);
     const int m = h->m, p = h->p;
-    int l = 0;
+    int l = l0;
     for (;;) {
         Level& Lv = h->lev[l];
+        Lv.nglob = Lv.A.n;
+        Lv.nnz_glob = Lv.A.nnz;
         Lv.lambda1 = inf_norm(Lv.A, s);
         Lv.kappa = h->opt.kappa > 1.0 ? h->opt.kappa : kappa_rule(m);
         poly_coeffs(Lv.lambda1, Lv.kappa, m, Lv.alpha, Lv.beta);
@@ -286,7 +247,7 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
             const uint64_t salt = host_sm64(h->opt.seed ^ (((uint64_t)l << 8) ^ (uint64_t)t));
             int* agg_t = dalloc<int>((size_t)G.n + 8, s);
             int nct = 0;
-            aggregate_pass(G, salt, agg_t, &nct, &Lv.rounds[t], s);
+            aggregate_pass(G, salt, 0, agg_t, &nct, &Lv.rounds[t], s);
             pt.mark("matching pass", l);
             if (t + 1 < p) {
                 PassGraph G2 = quotient_graph(G, agg_t, nct, s);
@@ -314,64 +275,85 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         Lv.aptr = halloc<int>(h, (size_t)nc + 1);
         aggregate_order(Lv.A.n, agg, nc, Lv.perm, Lv.aptr, s);
         pt.mark("aggregate order", l);
-        h->lev[l + 1].A = galerkin(Lv.A, agg, nc, Lv.perm, Lv.aptr, s);
+        h->lev[l + 1].A = galerkin(Lv.A, agg, nullptr, nc, nc, Lv.perm, Lv.aptr, s);
+        h->L = l + 2;
         pt.mark("galerkin", l);
         ++l;
     }
     h->L = l + 1;
-    // coarsest (a7)
+}
+
+double* amg::valloc(amg_hierarchy* h, Level& Lv, int slots, bool ws) {
+    double* base = halloc<double>(h, (size_t)Lv.ld * slots, ws);
+    return base + Lv.lo_pad;
+}
+
+void amg::finish_build(amg_hierarchy* h) {
+    cudaStream_t s = h->s;
+    PhaseTimer pt(s);
+    // coarsest (a7): every rank holds it whole
     Level& C = h->lev[h->L - 1];
     const double shift = C.lambda1 > 0.0 ? C.lambda1 : 1.0;
     h->Minv = coarse_inverse(C.A, h->singular, shift, s);
     h->allocs.push_back(h->Minv);
     pt.mark("coarse inverse", h->L - 1);
-    // tiles of every level the SpMV-class kernels run on (all but the coarsest; level 0 always)
+    // SpMV formats of every level the SpMV-class kernels run on (all but the coarsest; level 0 always)
     for (int k = 0; k < h->L; ++k) {
         Level& Lv = h->lev[k];
         if (k < h->L - 1 || k == 0) {
             Lv.T = build_tiles(Lv.A, 0, s);
             if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
+            if (Lv.S.sptr) Lv.S.chi = Lv.A.n + Lv.H.nhi - 1;
             if (Lv.S.sptr && h->opt.compress) compress_sell(Lv.S, Lv.A, s);
         }
         Lv.op.A = Lv.A;
         Lv.op.T = Lv.T;
         Lv.op.S = Lv.S;
         Lv.op.sell = Lv.S.sptr != nullptr;
+        // vector layout [pad | lower halo | own | upper halo]
+        Lv.lo_pad = (Lv.H.nlo + 3) & ~3;
+        Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : Lv.A.n;
     }
     pt.mark("tiles");
     // level workspaces
     for (int k = 0; k < h->L; ++k) {
         Level& Lv = h->lev[k];
-        const size_t nk = Lv.A.n;
         if (k < h->L - 1) {
-            Lv.X = halloc<double>(h, nk);
-            Lv.XA = halloc<double>(h, nk);
-            Lv.RES = halloc<double>(h, nk);
+            Lv.X = valloc(h, Lv, 1, false);
+            Lv.XA = valloc(h, Lv, 1, false);
+            Lv.RES = valloc(h, Lv, 1, false);
         }
         if (k >= 1) {
-            Lv.RHO = halloc<double>(h, nk);
-            Lv.E = halloc<double>(h, nk);
+            Lv.RHO = valloc(h, Lv, 1, false);
+            Lv.E = valloc(h, Lv, 1, false);
         }
         Lv.sc = halloc<double>(h, 3 * kMaxWin);
     }
-    // outer FCG
+    // outer FCG on level 0's own rows
+    Level& L0 = h->lev[0];
+    const int n = L0.A.n;
+    h->n = n;
     h->W = h->opt.restart;
-    h->b = halloc<double>(h, n);
-    h->x = halloc<double>(h, n);
-    h->r = halloc<double>(h, n);
-    h->Z = halloc<double>(h, n);
-    h->D = halloc<double>(h, (size_t)n * h->W);
-    h->Q = halloc<double>(h, (size_t)n * h->W);
+    h->b = valloc(h, L0, 1, false);
+    h->x = valloc(h, L0, 1, false);
+    h->r = valloc(h, L0, 1, false);
+    h->Z = valloc(h, L0, 1, false);
+    h->D = valloc(h, L0, h->W, false);
+    h->Q = valloc(h, L0, h->W, false);
     h->osc = halloc<double>(h, 2 * kMaxWin + 8);
     h->flag = halloc<int>(h, 4);
     h->ds.partials = halloc<double>(h, (size_t)(kMaxWin + 2) * 4096);
     h->ds.ticket = halloc<unsigned>(h, 4);
     CK(cudaMemsetAsync(h->ds.ticket, 0, 4 * sizeof(unsigned), s));
     CK(cudaMallocHost(&h->hsc, 8 * sizeof(double)));
-    // coarse tail: first level l >= 1 with nnz(A_l) <= tail_nnz (one SM runs it from L1/L2)
+    if (h->comm) {
+        h->ar_send = halloc<double>(h, kArMax);
+        h->ar_recv = halloc<double>(h, (size_t)kArMax * h->comm->size);
+    }
+    // coarse tail: first replicated level l >= 1 with nnz(A_l) <= tail_nnz (one SM runs it from L1/L2)
     h->l_tail = h->L;
     if (h->opt.tail_nnz > 0)
-        for (int k = 1; k < h->L; ++k)
+        for (int k = std::max(1, h->g); k < h->L; ++k)
             if (h->lev[k].A.nnz <= h->opt.tail_nnz) { h->l_tail = k; break; }
     if (h->l_tail < h->L) {
         tail_cluster_size();
@@ -444,10 +426,9 @@ static void ensure_inner_ws(amg_hierarchy* h, int nu) {
     h->ws_allocs.clear();
     for (int k = 1; k < h->L - 1; ++k) {
         Level& Lv = h->lev[k];
-        const size_t nk = Lv.A.n;
-        Lv.Z = halloc<double>(h, nk, true);
-        Lv.D = halloc<double>(h, nk * nu, true);
-        Lv.Q = halloc<double>(h, nk * nu, true);
+        Lv.Z = valloc(h, Lv, 1, true);
+        Lv.D = valloc(h, Lv, nu, true);
+        Lv.Q = valloc(h, Lv, nu, true);
     }
     h->nu_ws = nu;
     destroy_graphs(h);
@@ -457,7 +438,9 @@ static void ensure_inner_ws(amg_hierarchy* h, int nu) {
 // ------------------------------------------------------------------ solve schedule
 static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* out);
 
-// FCG_inner(l, RHO_l, nu) -> E_l
+// FCG_inner(l, RHO_l, nu) -> E_l.  On a row-partitioned level every SpMV
+// input is halo-exchanged first and every batch of dot partials is summed over the ranks before the
+// kernels that consume it.
 static void fcg_inner(amg_hierarchy* h, int l, int nu) {
     if (use_tail(h, l, nu)) {
         tail_call(h, 1, l, nu, nullptr, nullptr);
@@ -473,8 +456,8 @@ static void fcg_inner(amg_hierarchy* h, int l, int nu) {
     const double* Dp[kMaxWin];
     const double* Qp[kMaxWin];
     for (int i = 0; i < nu; ++i) {
-        double* Di = Lv.D + (size_t)i * n;
-        double* Qi = Lv.Q + (size_t)i * n;
+        double* Di = Lv.D + (size_t)i * Lv.ld;
+        double* Qi = Lv.Q + (size_t)i * Lv.ld;
         Dp[i] = Di;
         Qp[i] = Qi;
         if (i == 0) {
@@ -482,9 +465,16 @@ static void fcg_inner(amg_hierarchy* h, int l, int nu) {
         } else {
             apply_B(h, l, nu, rho, Lv.Z);
             launch_multidot(n, Lv.Z, Qp, i, c, h->ds, s);
+            if (Lv.dist) {
+                std::vector<double*> cs;
+                for (int j = 0; j < i; ++j) cs.push_back(c + j);
+                dot_allreduce(h, cs);
+            }
             launch_direction(n, Lv.Z, Dp, c, dq, i, Di, s);
         }
+        halo_exchange(h, l, Di);
         launch_spmv_dots(Lv.op, Di, rho, Qi, dq + i, dr + i, h->ds, s);  // q = A d, d.q, d.rho
+        if (Lv.dist) dot_allreduce(h, {dq + i, dr + i});
         launch_fcg_update(n, dr + i, dq + i, Di, Qi, Lv.E, i == 0, (i < nu - 1) ? rho : nullptr, nullptr, nullptr,
                           h->ds, s);
     }
@@ -492,7 +482,7 @@ static void fcg_inner(amg_hierarchy* h, int l, int nu) {
 
 // z = B_l(r): pre-smoothing from 0, residual, restriction, coarse correction,
 // prolongation, post-smoothing; the last smoothing step writes `out` (distinct from rin and the
-// level buffers).
+// level buffers).  `rin` must be a vector of level l's layout (it is the first step's SpMV input).
 static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* out) {
     cudaStream_t s = h->s;
     if (l == h->L - 1) {
@@ -510,28 +500,38 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     // pre-smoothing S(r, 0): step 0 is free (x_1 = b0 r implicit)
     double* cur = Lv.X;
     double* prev = Lv.XA;
+    halo_exchange(h, l, const_cast<double*>(rin));
     launch_smooth(Lv.op, rin, b[0], rin, nullptr, 0.0, a[1], b[1], Lv.X, s);  // k = 1 (x_0 = 0)
     if (m >= 2) {
+        halo_exchange(h, l, Lv.X);
         launch_smooth(Lv.op, Lv.X, 1.0, rin, nullptr, b[0], a[2], b[2], Lv.XA, s);  // k = 2 (x_1 = b0 r)
         cur = Lv.XA;
         prev = Lv.X;
         for (int k = 3; k <= m; ++k) {
+            halo_exchange(h, l, cur);
             launch_smooth(Lv.op, cur, 1.0, rin, prev, 0.0, a[k], b[k], prev, s);
             std::swap(cur, prev);
         }
     }
     // residual + restriction
+    halo_exchange(h, l, cur);
     launch_resid(Lv.op, cur, rin, Lv.RES, nullptr, h->ds, s);
     Level& C = h->lev[l + 1];
-    launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO, s);
+    // the level below the last row-partitioned one is replicated: restrict into this rank's block of
+    // it and allgather the blocks (C-gather); prolong from the same block
+    const bool gather = Lv.dist && !C.dist;
+    const int64_t cb = gather ? C.offs[h->comm->rank] : 0;
+    launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO + cb, s);
+    if (gather) allgatherv_d(h, C.RHO, C.offs);
     // coarse correction (A12: exact solve when the next level is the coarsest)
     if (l + 1 == h->L - 1)
         launch_gemv(C.A.n, h->Minv, C.RHO, C.E, s);
     else
         fcg_inner(h, l + 1, nu);
-    launch_prolong(Lv.A.n, Lv.agg, C.E, cur, s);
+    launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
     // post-smoothing S(r, x): x_{-1} = x_0 = cur
     double* other = (cur == Lv.X) ? Lv.XA : Lv.X;
+    halo_exchange(h, l, cur);
     launch_smooth(Lv.op, cur, 1.0, rin, cur, 0.0, 1.0, b[0], other, s);  // k = 0
     prev = cur;
     cur = other;
@@ -539,6 +539,7 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     if (prof) record_event(h->pe0, s);
     for (int k = 1; k <= m; ++k) {
         double* target = (k == m) ? out : prev;
+        halo_exchange(h, l, cur);
         launch_smooth(Lv.op, cur, 1.0, rin, prev, 0.0, a[k], b[k], target, s);
         prev = cur;
         cur = target;
@@ -546,33 +547,55 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     if (prof) record_event(h->pe1, s);
 }
 
+// v -= mean(v) over the whole level-0 vector (A16); the sum is allreduced when partitioned
+static void mean_project(amg_hierarchy* h, double* v) {
+    double* tmp = h->osc + 2 * kMaxWin + 3;
+    if (!h->lev[0].dist) {
+        launch_mean_project(h->n, v, tmp, h->ds, h->s);
+        return;
+    }
+    launch_dot(h->n, v, nullptr, tmp, h->ds, h->s);
+    dot_allreduce(h, {tmp});
+    launch_sub_mean(h->n, (double)h->lev[0].nglob, v, tmp, h->s);
+}
+
 // one outer FCG iteration at window position p
 static void outer_iteration(amg_hierarchy* h, int pos, int nu) {
     cudaStream_t s = h->s;
     const int n = h->n;
+    const size_t ld = h->lev[0].ld;
+    const bool dist = h->lev[0].dist;
     double* dq = h->osc;
     double* c = h->osc + kMaxWin;
     double* dr = h->osc + 2 * kMaxWin;
     double* rr = h->osc + 2 * kMaxWin + 1;
-    double* Dp = h->D + (size_t)pos * n;
-    double* Qp = h->Q + (size_t)pos * n;
+    double* Dp = h->D + (size_t)pos * ld;
+    double* Qp = h->Q + (size_t)pos * ld;
     double* zdst = (pos == 0) ? Dp : h->Z;
     h->prof_on = true;
     apply_B(h, 0, nu, h->r, zdst);
     h->prof_on = false;
-    if (h->singular) launch_mean_project(n, zdst, h->osc + 2 * kMaxWin + 3, h->ds, s);
+    if (h->singular) mean_project(h, zdst);
     if (pos > 0) {
         const double* Ds[kMaxWin];
         const double* Qs[kMaxWin];
         for (int j = 0; j < pos; ++j) {
-            Ds[j] = h->D + (size_t)j * n;
-            Qs[j] = h->Q + (size_t)j * n;
+            Ds[j] = h->D + (size_t)j * ld;
+            Qs[j] = h->Q + (size_t)j * ld;
         }
         launch_multidot(n, h->Z, Qs, pos, c, h->ds, s);
+        if (dist) {
+            std::vector<double*> cs;
+            for (int j = 0; j < pos; ++j) cs.push_back(c + j);
+            dot_allreduce(h, cs);
+        }
         launch_direction(n, h->Z, Ds, c, dq, pos, Dp, s);
     }
+    halo_exchange(h, 0, Dp);
     launch_spmv_dots(h->lev[0].op, Dp, h->r, Qp, dq + pos, dr, h->ds, s);
+    if (dist) dot_allreduce(h, {dq + pos, dr});
     launch_fcg_update(n, dr, dq + pos, Dp, Qp, h->x, false, h->r, rr, h->flag, h->ds, s);
+    if (dist) dot_allreduce(h, {rr});
 }
 
 static void capture_graphs(amg_hierarchy* h, int nu) {
@@ -608,18 +631,33 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
         CK(cudaStreamWaitEvent(s, ev, 0));
         CK(cudaEventDestroy(ev));
     }
+    // graphs need a capturable communicator (NCCL); the thread-emulated ranks run eagerly
+    const bool graphs = h->opt.use_graphs && (!h->comm || h->comm->capturable());
+    const bool dist = h->lev[0].dist;
+    // distributed handle whose whole hierarchy is replicated (g = 0): gather the caller's blocks
+    const bool gather_in = h->comm && !dist;
     ensure_inner_ws(h, nu);
-    if (h->opt.use_graphs && h->graph_nu != nu) capture_graphs(h, nu);
+    if (graphs && h->graph_nu != nu) capture_graphs(h, nu);
     long long launches0 = g_launches;
     CK(cudaEventRecord(h->e0, s));
     // inputs
-    CK(cudaMemcpyAsync(h->b, b_in, sizeof(double) * n, is_device_ptr(b_in) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(h->x, x_out, sizeof(double) * n, is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    const int64_t own0 = gather_in ? h->row_begin : 0;
+    const int nown = gather_in ? h->n_local : n;
+    CK(cudaMemcpyAsync(h->b + own0, b_in, sizeof(double) * nown,
+                       is_device_ptr(b_in) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h->x + own0, x_out, sizeof(double) * nown,
+                       is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    if (gather_in) {
+        allgatherv_d(h, h->b, h->lev[0].offs);
+        allgatherv_d(h, h->x, h->lev[0].offs);
+    }
     double* bb = h->osc + 2 * kMaxWin + 2;
     double* rr = h->osc + 2 * kMaxWin + 1;
-    if (h->singular) launch_mean_project(n, h->b, h->osc + 2 * kMaxWin + 3, h->ds, s);  // S:449, A16
+    if (h->singular) mean_project(h, h->b);  // S:449, A16
     launch_dot(n, h->b, h->b, bb, h->ds, s);
+    halo_exchange(h, 0, h->x);
     launch_resid(h->lev[0].op, h->x, h->b, h->r, rr, h->ds, s);
+    if (dist) dot_allreduce(h, {rr, bb});
     CK(cudaMemsetAsync(h->flag, 0, sizeof(int), s));
     CK(cudaMemcpyAsync(h->hsc, rr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -638,7 +676,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
         for (k = 0;; ++k) {
             if (rnorm <= tol * bnorm) { status = AMG_OK; break; }
             if (k >= h->opt.max_iter) break;
-            if (h->opt.use_graphs) {
+            if (graphs) {
                 CK(cudaGraphLaunch(h->graphs[pos], s));
                 ++graph_runs;
             } else {
@@ -662,8 +700,10 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     }
     // true residual ||b - A x|| (reported) and the solution back to the caller
     double* rt = h->osc + 2 * kMaxWin + 6;
+    halo_exchange(h, 0, h->x);
     launch_resid(h->lev[0].op, h->x, h->b, h->Z, rt, h->ds, s);
-    copy_out(x_out, h->x, sizeof(double) * n, s);
+    if (dist) dot_allreduce(h, {rt});
+    copy_out(x_out, h->x + own0, sizeof(double) * nown, s);
     CK(cudaEventRecord(h->e1, s));
     CK(cudaMemcpyAsync(h->hsc + 3, rt, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -703,13 +743,18 @@ int amg_options_default(amg_options* o) {
     o->use_graphs = 1;
     o->tail_nnz = 8192;
     o->compress = 1;
+    o->gather_rows = 50000;
     return AMG_OK;
 }
 
 const char* amg_last_error(void) { return g_last_error.c_str(); }
 
-int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
-              const double* d, int32_t n_match_passes, int32_t poly_degree, const amg_options* opt) {
+}  // extern "C"
+
+// amg_setup / amg_setup_dist: comm == nullptr is the single-GPU path (n_global = n_local, row_begin 0)
+static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t row_begin, int64_t n,
+                      const int64_t* row_ptr, const int32_t* col, const double* val, const double* d,
+                      int32_t n_match_passes, int32_t poly_degree, const amg_options* opt) {
     if (!out) return fail(AMG_E_ARG, "amg_setup: out is NULL");
     *out = nullptr;
     if (!row_ptr || !val || !col) return fail(AMG_E_ARG, "amg_setup: NULL array");
@@ -718,8 +763,9 @@ int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t*
     amg_options o;
     amg_options_default(&o);
     if (opt) o = *opt;
-    if (o.coarsest_size < 1 || o.restart < 1 || o.restart > kMaxWin || o.max_iter < 0)
+    if (o.coarsest_size < 1 || o.restart < 1 || o.restart > kMaxWin || o.max_iter < 0 || o.gather_rows < 0)
         return fail(AMG_E_ARG, "amg_setup: bad options");
+    if (comm && !comm->c) return fail(AMG_E_ARG, "amg_setup_dist: invalid communicator");
     if (o.kappa != 0.0 && !(o.kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: kappa must be 0 or > 1");
     if (o.kappa > 1.0 && !(Em_of(poly_degree, o.kappa) < 1.0))
         return fail(AMG_E_ARG, "amg_setup: E_m(kappa) >= 1: the smoother would not converge (reading A9)");
@@ -762,7 +808,12 @@ int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t*
         }
         CK(cudaEventRecord(h->e0, h->s));
         long long l0 = g_launches;
-        build(h, n, row_ptr, col, val, d);
+        if (comm) {
+            h->comm = comm->c;
+            build_dist(h, n_global, row_begin, (int)n, row_ptr, col, val, d);
+        } else {
+            build(h, n, row_ptr, col, val, d);
+        }
         h->info.launches_last_setup = g_launches - l0;
         CK(cudaEventRecord(h->e1, h->s));
         CK(cudaEventSynchronize(h->e1));
@@ -773,15 +824,32 @@ int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t*
     } catch (const Error& e) {
         g_last_error = e.what();
         cudaGetLastError();
+        if (h->comm && e.code != AMG_E_NCCL) h->comm->abort();
         release(h);
         return e.code;
     } catch (const std::exception& e) {
         g_last_error = e.what();
+        if (h->comm) h->comm->abort();
         release(h);
         return AMG_E_CUDA;
     }
     *out = h;
     return AMG_OK;
+}
+
+extern "C" {
+
+int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+              const double* d, int32_t n_match_passes, int32_t poly_degree, const amg_options* opt) {
+    return setup_impl(out, nullptr, n, 0, n, row_ptr, col, val, d, n_match_passes, poly_degree, opt);
+}
+
+int amg_setup_dist(amg_handle* out, amg_comm comm, int64_t n_global, int64_t row_begin, int64_t n_local,
+                   const int64_t* row_ptr, const int32_t* col_global, const double* val, const double* d,
+                   int32_t n_match_passes, int32_t poly_degree, const amg_options* opt) {
+    if (!comm) return fail(AMG_E_ARG, "amg_setup_dist: comm is NULL");
+    return setup_impl(out, comm, n_global, row_begin, n_local, row_ptr, col_global, val, d, n_match_passes,
+                      poly_degree, opt);
 }
 
 int amg_solve(amg_handle h, const double* b, double* x, double tol, int32_t k_inner, int32_t* iters, double* relres) {
@@ -795,6 +863,7 @@ int amg_solve(amg_handle h, const double* b, double* x, double tol, int32_t k_in
     } catch (const Error& e) {
         g_last_error = e.what();
         cudaGetLastError();
+        if (h->comm && e.code != AMG_E_NCCL) h->comm->abort();
         return e.code;
     }
 }
@@ -812,19 +881,21 @@ int amg_get_info(amg_handle h, amg_info* info) {
     r.poly_degree = h->m;
     r.n_match_passes = h->p;
     r.singular = h->singular;
-    double sn = 0, snz = 0;
+    double sn = 0, snz = 0;  // whole-level sizes (summed over the ranks on a row-partitioned level)
     for (int l = 0; l < h->L; ++l) {
-        sn += h->lev[l].A.n;
-        snz += (double)h->lev[l].A.nnz;
+        sn += (double)h->lev[l].nglob;
+        snz += (double)h->lev[l].nnz_glob;
         if (l < 32) {
-            r.n[l] = h->lev[l].A.n;
-            r.nnz[l] = h->lev[l].A.nnz;
+            r.n[l] = h->lev[l].nglob;
+            r.nnz[l] = h->lev[l].nnz_glob;
             r.lambda1[l] = h->lev[l].lambda1;
             r.kappa[l] = h->lev[l].kappa;
         }
     }
-    r.grid_complexity = sn / h->lev[0].A.n;
-    r.operator_complexity = snz / (double)h->lev[0].A.nnz;
+    r.grid_complexity = sn / (double)h->lev[0].nglob;
+    r.operator_complexity = snz / (double)h->lev[0].nnz_glob;
+    r.nranks = h->comm ? h->comm->size : 1;
+    r.dist_levels = h->comm ? h->g : 0;
     r.device_bytes = h->bytes;
     {
         const Level& L0 = h->lev[0];
@@ -862,9 +933,23 @@ int amg_level_export(amg_handle h, int32_t level, int64_t* row_ptr, int32_t* col
             CK(cudaMemcpy(row_ptr, w.data(), sizeof(int64_t) * w.size(),
                           is_device_ptr(row_ptr) ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
         }
-        if (col) copy_out(col, Lv.A.ci, sizeof(int) * Lv.A.nnz, s);
+        if (Lv.dist) {  // global column ids and global coarse ids
+            int* tmp = dalloc<int>((size_t)std::max<int64_t>(Lv.A.nnz, Lv.A.n) + 8, s);
+            if (col) {
+                export_dist_cols(h, level, tmp);
+                copy_out(col, tmp, sizeof(int) * Lv.A.nnz, s);
+            }
+            if (agg && level < h->L - 1) {
+                export_dist_agg(h, level, tmp);
+                copy_out(agg, tmp, sizeof(int) * Lv.A.n, s);
+            }
+            CK(cudaStreamSynchronize(s));
+            dfree(tmp, s);
+        } else {
+            if (col) copy_out(col, Lv.A.ci, sizeof(int) * Lv.A.nnz, s);
+            if (agg && level < h->L - 1) copy_out(agg, Lv.agg, sizeof(int) * Lv.A.n, s);
+        }
         if (val) copy_out(val, Lv.A.v, sizeof(double) * Lv.A.nnz, s);
-        if (agg && level < h->L - 1) copy_out(agg, Lv.agg, sizeof(int) * Lv.A.n, s);
         CK(cudaStreamSynchronize(s));
     } catch (const Error& e) {
         g_last_error = e.what();
@@ -886,11 +971,13 @@ int amg_level_smooth(amg_handle h, int32_t level, const double* f, const double*
         // S(f, x0): x_{-1} = x_0
         double* cur = Lv.X;
         double* other = Lv.XA;
+        halo_exchange(h, level, cur);
         launch_smooth(Lv.op, cur, 1.0, F, cur, 0.0, 1.0, Lv.beta[0], other, s);
         double* prev = cur;
         cur = other;
         for (int k = 1; k <= h->m; ++k) {
             double* target = (k == h->m) ? O : prev;
+            halo_exchange(h, level, cur);
             launch_smooth(Lv.op, cur, 1.0, F, prev, 0.0, Lv.alpha[k], Lv.beta[k], target, s);
             prev = cur;
             cur = target;
@@ -913,20 +1000,32 @@ int amg_level_precond(amg_handle h, int32_t level, int32_t k_inner, const double
     try {
         cudaStream_t s = h->s;
         ensure_inner_ws(h, k_inner);
-        const int n = h->lev[level].A.n;
-        double* R = dalloc<double>((size_t)n + 8, s);
+        Level& Lv = h->lev[level];
+        const int n = Lv.A.n;
+        // R in the level's vector layout (its halo is exchanged by the first smoothing step)
+        double* Rb = dalloc<double>((size_t)std::max(Lv.ld, n) + 8, s);
+        double* R = Rb + Lv.lo_pad;
         double* O = dalloc<double>((size_t)n + 8, s);
         CK(cudaMemcpyAsync(R, r, sizeof(double) * n, cudaMemcpyDefault, s));
         apply_B(h, level, k_inner, R, O);
         copy_out(z, O, sizeof(double) * n, s);
         CK(cudaStreamSynchronize(s));
-        dfree(R, s);
+        dfree(Rb, s);
         dfree(O, s);
         CK(cudaStreamSynchronize(s));
     } catch (const Error& e) {
         g_last_error = e.what();
         return e.code;
     }
+    return AMG_OK;
+}
+
+int amg_level_dist(amg_handle h, int32_t level, int32_t* dist, int64_t* row_begin, int64_t* n_global) {
+    if (!h || level < 0 || level >= h->L) return fail(AMG_E_ARG, "amg_level_dist: bad level");
+    const Level& Lv = h->lev[level];
+    if (dist) *dist = Lv.dist ? 1 : 0;
+    if (row_begin) *row_begin = Lv.dist ? Lv.gbeg : 0;
+    if (n_global) *n_global = Lv.nglob;
     return AMG_OK;
 }
 

@@ -1,0 +1,140 @@
+// hierarchy.h -- the handle behind amg_handle (include/amg.h): levels, workspaces, the row partition
+// of the distributed levels, and the host-side entry points shared by driver.cu (single GPU, the
+// replicated levels, the solve schedule) and dist.cu (row-partitioned setup, halo exchange, the
+// batched dot allreduce).  Internal; not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "../../include/amg.h"
+#include "amg_internal.h"
+
+namespace amg {
+
+// ------------------------------------------------------------------ row partition
+// A row-partitioned level stores its own rows [gbeg, gbeg + n) of nglob.  Columns are RELATIVE to
+// the first own row: own columns in [0, n), the halo below in [-nlo, 0) and above in [n, n + nhi),
+// both in increasing global order (blocks are contiguous in rank order, so the map global ->
+// relative is monotone: CSR rows stay sorted and the Galerkin summation order is the global one).
+// Every vector of the level is laid out [pad | lower halo | own | upper halo] so an SpMV input x
+// (pointer to its first own element) is read as x[col] for any column.
+struct Seg {
+    int peer, off, cnt;  // recv: off = relative column of the first element; send: offset into sidx
+};
+struct Halo {
+    int nlo = 0, nhi = 0;
+    std::vector<int> hid;        // sorted global ids of the halo columns (nlo below, then nhi above)
+    int* d_hid = nullptr;        // device copy of hid
+    std::vector<Seg> recv, send;
+    int nsend = 0;
+    int* sidx = nullptr;         // device [nsend]: own row of each element sent (send segments concatenated)
+    double* sbuf = nullptr;      // device [nsend] doubles (also carries int payloads at setup)
+};
+
+struct Level {
+    Csr A;
+    Tiles T;
+    Sell S;
+    SpOp op;  // the format the SpMV-class kernels use on this level
+    double lambda1 = 0, kappa = 0;
+    double alpha[kMaxDeg + 1] = {}, beta[kMaxDeg + 1] = {};
+    int nc = 0;
+    int* agg = nullptr;
+    int* perm = nullptr;
+    int* aptr = nullptr;
+    int rounds[kMaxDeg] = {};
+    // workspaces (pointers to the first own element)
+    double *X = nullptr, *XA = nullptr, *RES = nullptr;  // B_l
+    double *RHO = nullptr, *E = nullptr;                  // written / read by the parent level
+    double *Z = nullptr, *D = nullptr, *Q = nullptr;      // inner FCG (nu slots, stride ld)
+    double* sc = nullptr;                                 // dq[kMaxWin], dr[kMaxWin], c[kMaxWin]
+    // partition
+    bool dist = false;           // row-partitioned (levels < g of a distributed handle)
+    int64_t gbeg = 0, nglob = 0; // own rows [gbeg, gbeg + A.n) of nglob (nglob = A.n when not partitioned)
+    int64_t nnz_glob = 0;        // nnz of the whole level (sum over ranks)
+    std::vector<int64_t> offs;   // block offsets of all ranks (P+1): the partition this level's rows came in
+    Halo H;
+    int lo_pad = 0;              // own element offset inside a vector allocation (>= H.nlo, multiple of 4)
+    int ld = 0;                  // vector slot stride (lo_pad + n + nhi, rounded up to 4)
+};
+
+}  // namespace amg
+
+struct amg_hierarchy {
+    cudaStream_t s = nullptr;
+    cudaStream_t user = nullptr;
+    int L = 0, m = 0, p = 0;
+    bool singular = false;
+    amg_options opt{};
+    amg::Level lev[amg::kMaxLevels];
+    double* Minv = nullptr;
+    // outer FCG (level 0 own rows)
+    int n = 0, W = 5;
+    double *b = nullptr, *x = nullptr, *r = nullptr, *Z = nullptr, *D = nullptr, *Q = nullptr;
+    double* osc = nullptr;  // dq[kMaxWin], c[kMaxWin], dr, rr, bb, tmp, rr_true
+    int* flag = nullptr;
+    double* hsc = nullptr;  // pinned host mirror: rr, flag
+    amg::DotScratch ds;
+    int nu_ws = 0;          // nu the inner workspaces are sized for
+    int l_tail = 0;         // first level run by the coarse-tail kernel (L = none)
+    amg::TLevel* d_tlev = nullptr;
+    std::vector<cudaGraphExec_t> graphs;
+    int graph_nu = 0;
+    long long graph_launches = 0;
+    std::vector<void*> allocs;
+    std::vector<void*> ws_allocs;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;  // live profile of the level-0 smoother steps
+    bool prof_on = false;
+    int64_t bytes = 0;
+    amg_info info{};
+    // distributed handle (amg_setup_dist); comm == nullptr on one GPU
+    amg::Comm* comm = nullptr;
+    int g = 0;                       // first replicated level: levels < g are row-partitioned
+    int64_t n_global = 0, row_begin = 0;  // the caller's level-0 block
+    int n_local = 0;
+    double* ar_send = nullptr;       // batched dot allreduce scratch: [kArMax] and [kArMax * P]
+    double* ar_recv = nullptr;
+    double *bfull = nullptr, *xfull = nullptr;  // g == 0: gathered b and x
+};
+
+namespace amg {
+
+constexpr int kArMax = 40;  // scalars per batched allreduce
+
+// driver.cu
+template <class T>
+T* halloc(amg_hierarchy* h, size_t n, bool ws = false) {
+    T* p = dalloc<T>(n + 8, h->s);  // +8: padding for the 16-byte vector loads
+    (ws ? h->ws_allocs : h->allocs).push_back(p);
+    h->bytes += (int64_t)((n + 8) * sizeof(T));
+    return p;
+}
+uint64_t host_sm64(uint64_t z);
+double kappa_rule(int m);
+void poly_coeffs(double l1, double kappa, int m, double* a, double* b);
+// level loop (a1-a6) from h->lev[l0].A, which every rank holds whole (replicated); sets h->L
+void build_levels(amg_hierarchy* h, int l0);
+// coarsest inverse, SpMV formats, workspaces, tail (after all levels exist)
+void finish_build(amg_hierarchy* h);
+// vector of level l laid out for halo exchange: returns the pointer to its first own element
+double* valloc(amg_hierarchy* h, Level& Lv, int slots, bool ws);
+
+// dist.cu
+void build_dist(amg_hierarchy* h, int64_t n_global, int64_t row_begin, int n_local, const int64_t* rp,
+                const int32_t* ci_global, const double* v, const double* d);
+void halo_exchange(amg_hierarchy* h, int l, double* x);  // no-op unless level l is row-partitioned
+// sum the scalars at ptrs over the ranks (each rank's local partial; rank-order sum, identical on
+// every rank); no-op on one GPU
+void dot_allreduce(amg_hierarchy* h, const std::vector<double*>& ptrs);
+// own block (count_r elements at displ_r of `full`) of every rank gathered into `full` (device)
+void allgatherv_d(amg_hierarchy* h, double* full, const std::vector<int64_t>& offs);
+// warm every exchange pattern once outside graph capture (NCCL connects peers lazily)
+void warm_comm(amg_hierarchy* h);
+// export helpers for the parity hooks: relative columns -> global ids, own agg -> global coarse ids
+void export_dist_cols(amg_hierarchy* h, int l, int* out_dev);
+void export_dist_agg(amg_hierarchy* h, int l, int* out_dev);
+
+}  // namespace amg

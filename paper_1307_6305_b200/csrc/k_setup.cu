@@ -93,7 +93,10 @@ enum : int {
     VF_RANGE = 1, VF_UNSORTED = 2, VF_POSOFF = 4, VF_ASYM = 8, VF_DIAG = 16, VF_D = 32, VF_RP = 64
 };
 
-__global__ void k_validate(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+// Columns must lie in [cmin, cmax): [0, n) on one GPU; [-nlo, n + nhi) on a row-partitioned level
+// (columns relative to the first own row, halo outside [0, n)).  Symmetry is checked for pairs of
+// own rows (a cross-block pair is split between two ranks: the caller's contract).
+__global__ void k_validate(int n, int cmin, int cmax, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                            const double* __restrict__ v, const double* __restrict__ d, int* flags) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         int f = 0;
@@ -103,11 +106,12 @@ __global__ void k_validate(int n, const int64_t* __restrict__ rp, const int32_t*
         bool has = false;
         for (int64_t p = p0; p < p1; ++p) {
             const int c = ci[p];
-            if (c < 0 || c >= n) { f |= VF_RANGE; continue; }
+            if (c < cmin || c >= cmax) { f |= VF_RANGE; continue; }
             if (p > p0 && c <= ci[p - 1]) f |= VF_UNSORTED;
             if (c == i) { has = true; dv = v[p]; continue; }
             if (!(v[p] < 0.0)) f |= VF_POSOFF;
             off += -v[p];
+            if (c < 0 || c >= n) continue;
             int64_t lo = rp[c], hi = rp[c + 1];
             while (lo < hi) {
                 int64_t mid = (lo + hi) >> 1;
@@ -121,10 +125,11 @@ __global__ void k_validate(int n, const int64_t* __restrict__ rp, const int32_t*
     }
 }
 
-int validate_input(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s) {
+int validate_input(int n, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v, const double* d,
+                   cudaStream_t s) {
     int* fl = dalloc<int>(1, s);
     CK(cudaMemsetAsync(fl, 0, sizeof(int), s));
-    k_validate<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, v, d, fl);
+    k_validate<<<grid_for(n), kBlock, 0, s>>>(n, cmin, cmax, rp, ci, v, d, fl);
     ++g_launches;
     CK(cudaGetLastError());
     int f = read_scalar(fl, s);
@@ -233,7 +238,7 @@ double inf_norm(const Csr& A, cudaStream_t s) {
 __global__ void k_g0_count(int n, const int* __restrict__ rp, const int* __restrict__ ci, int* cnt) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         int c = 0;
-        for (int p = rp[i]; p < rp[i + 1]; ++p) c += (ci[p] != i);
+        for (int p = rp[i]; p < rp[i + 1]; ++p) c += (ci[p] != i && ci[p] >= 0 && ci[p] < n);
         cnt[i] = c;
     }
 }
@@ -243,7 +248,7 @@ __global__ void k_g0_fill(int n, const int* __restrict__ rp, const int* __restri
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         int q = grp[i];
         for (int p = rp[i]; p < rp[i + 1]; ++p)
-            if (ci[p] != i) { gci[q] = ci[p]; gw[q] = 1u; ++q; }
+            if (ci[p] != i && ci[p] >= 0 && ci[p] < n) { gci[q] = ci[p]; gw[q] = 1u; ++q; }
     }
 }
 
@@ -280,7 +285,12 @@ struct EKey {
     int lo, hi;
 };
 
-__device__ __forceinline__ EKey make_key(uint32_t w, int a, int b, uint64_t salt) {
+// a, b: local vertex ids of G_t; `off` = global id of local vertex 0 (row-partitioned levels:
+// docs/keys.md uses global ids; 0 on one GPU).  The order of keys is offset invariant except
+// through the hash, which must see the global ids.
+__device__ __forceinline__ EKey make_key(uint32_t w, int a, int b, uint64_t salt, int off) {
+    a += off;
+    b += off;
     EKey k;
     k.w = w;
     k.lo = a < b ? a : b;
@@ -299,7 +309,7 @@ __device__ __forceinline__ bool key_gt(const EKey& a, const EKey& b) {
 // handshake round, step 1: every free vertex proposes to its max-key free neighbour
 __global__ void k_propose(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                           const uint32_t* __restrict__ w, const int* __restrict__ mate, int* __restrict__ prop,
-                          uint64_t salt, int* any) {
+                          uint64_t salt, int off, int* any) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         int best = -1;
         if (mate[v] < 0) {
@@ -307,7 +317,7 @@ __global__ void k_propose(int n, const int* __restrict__ rp, const int* __restri
             for (int p = rp[v]; p < rp[v + 1]; ++p) {
                 const int u = ci[p];
                 if (mate[u] >= 0) continue;
-                EKey k = make_key(w[p], v, u, salt);
+                EKey k = make_key(w[p], v, u, salt, off);
                 if (best < 0 || key_gt(k, bk)) { bk = k; best = u; }
             }
         }
@@ -326,7 +336,7 @@ __global__ void k_accept(int n, int* __restrict__ mate, const int* __restrict__ 
 
 // attach (A3) + leader (A4)
 __global__ void k_leader(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                         const uint32_t* __restrict__ w, const int* __restrict__ mate, uint64_t salt,
+                         const uint32_t* __restrict__ w, const int* __restrict__ mate, uint64_t salt, int off,
                          int* __restrict__ leader, int* __restrict__ isl) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         const int m = mate[v];
@@ -337,7 +347,7 @@ __global__ void k_leader(int n, const int* __restrict__ rp, const int* __restric
             EKey bk{};
             int bu = -1;
             for (int p = rp[v]; p < rp[v + 1]; ++p) {
-                EKey k = make_key(w[p], v, ci[p], salt);
+                EKey k = make_key(w[p], v, ci[p], salt, off);
                 if (bu < 0 || key_gt(k, bk)) { bk = k; bu = ci[p]; }
             }
             const int mu = mate[bu];  // matched by maximality
@@ -354,7 +364,7 @@ __global__ void k_assign(int n, const int* __restrict__ leader, const int* __res
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) agg[v] = id[leader[v]];
 }
 
-int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* rounds, cudaStream_t s) {
+int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, int* nc, int* rounds, cudaStream_t s) {
     const int n = G.n;
     int* mate = dalloc<int>(n, s);
     int* prop = dalloc<int>(n, s);
@@ -370,7 +380,7 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* 
     for (;;) {
         for (int k = 0; k < kBatch; ++k) {
             CK(cudaMemsetAsync(any, 0, sizeof(int), s));
-            k_propose<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, prop, salt, any);
+            k_propose<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, prop, salt, id_off, any);
             ++g_launches;
             k_accept<<<g, kBlock, 0, s>>>(n, mate, prop);
             ++g_launches;
@@ -385,7 +395,7 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* 
     int* leader = prop;  // reuse
     int* isl = dalloc<int>((size_t)n + 1, s);
     CK(cudaMemsetAsync(isl + n, 0, sizeof(int), s));
-    k_leader<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, salt, leader, isl);
+    k_leader<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, salt, id_off, leader, isl);
     ++g_launches;
     CK(cudaGetLastError());
     int* id = dalloc<int>((size_t)n + 1, s);
@@ -406,13 +416,13 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int* agg_t, int* nc, int* 
 // keys for every stored entry of a CSR: (agg(i) << b) | agg(j); `drop` => self entries get the
 // sentinel (all ones in the low 2b bits) which sorts last.
 __global__ void k_pair_keys(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                            const int* __restrict__ agg, int b, bool drop, uint64_t* __restrict__ keys,
-                            int* __restrict__ idx) {
+                            const int* __restrict__ agg, const int* __restrict__ cmap, int b, bool drop,
+                            uint64_t* __restrict__ keys, int* __restrict__ idx) {
     const uint64_t sentinel = (b >= 32) ? ~0ULL : ((1ULL << (2 * b)) - 1ULL);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint64_t I = (uint64_t)agg[i];
         for (int p = rp[i]; p < rp[i + 1]; ++p) {
-            const uint64_t J = (uint64_t)agg[ci[p]];
+            const uint64_t J = (uint64_t)cmap[ci[p]];
             keys[p] = (drop && I == J) ? sentinel : ((I << b) | J);
             idx[p] = p;
         }
@@ -473,16 +483,17 @@ __global__ void k_lower_bound_u64(int64_t m, const uint64_t* keys, uint64_t x, i
 // Quotient of a CSR under agg: returns (rp, ci, val) of the nc x nc result.  VAL = uint32
 // multiplicities (pass graphs, drop self entries) or double values (Galerkin, keep all).
 template <class VAL>
-static void quotient_impl(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg, int nc,
-                          bool drop, int** orp, int** oci, VAL** oval, int64_t* onnz, cudaStream_t s) {
-    const int b = bits_for(nc);
+static void quotient_impl(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg,
+                          const int* cmap, int nc, int ncols, bool drop, int** orp, int** oci, VAL** oval,
+                          int64_t* onnz, cudaStream_t s) {
+    const int b = bits_for(std::max(nc, ncols));
     const uint64_t sentinel = (b >= 32) ? ~0ULL : ((1ULL << (2 * b)) - 1ULL);
     const int m = (int)nnz;
     uint64_t* k0 = dalloc<uint64_t>(m, s);
     uint64_t* k1 = dalloc<uint64_t>(m, s);
     int* i0 = dalloc<int>(m, s);
     int* i1 = dalloc<int>(m, s);
-    k_pair_keys<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, agg, b, drop, k0, i0);
+    k_pair_keys<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, agg, cmap, b, drop, k0, i0);
     ++g_launches;
     CK(cudaGetLastError());
     sort_pairs(k0, k1, i0, i1, m, 2 * b, s);  // stable: equal keys keep (row, position) order
@@ -836,18 +847,21 @@ PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStrea
         dfree(aptr, s);
         if (ok) return H;
     }
-    quotient_impl<uint32_t>(G.n, G.nnz, G.rp, G.ci, G.w, agg_t, nc, true, &H.rp, &H.ci, &H.w, &H.nnz, s);
+    quotient_impl<uint32_t>(G.n, G.nnz, G.rp, G.ci, G.w, agg_t, agg_t, nc, nc, true, &H.rp, &H.ci, &H.w, &H.nnz, s);
     return H;
 }
 
-Csr galerkin(const Csr& A, const int* agg, int nc, const int* perm, const int* aptr, cudaStream_t s) {
+Csr galerkin(const Csr& A, const int* agg, const int* cmap, int nc, int ncols, const int* perm, const int* aptr,
+             cudaStream_t s) {
     Csr H;
     H.n = nc;
+    if (!cmap) cmap = agg;
+    // the row merge reads the coarse column of every entry through `cmap` (rows come from perm/aptr)
     if (!getenv("AMG_RADIX_QUOTIENT") &&
-        quotient_rowmerge<double>(A.n, A.nnz, A.rp, A.ci, A.v, agg, nc, false, perm, aptr, &H.rp, &H.ci, &H.v, &H.nnz,
+        quotient_rowmerge<double>(A.n, A.nnz, A.rp, A.ci, A.v, cmap, nc, false, perm, aptr, &H.rp, &H.ci, &H.v, &H.nnz,
                                   s))
         return H;
-    quotient_impl<double>(A.n, A.nnz, A.rp, A.ci, A.v, agg, nc, false, &H.rp, &H.ci, &H.v, &H.nnz, s);
+    quotient_impl<double>(A.n, A.nnz, A.rp, A.ci, A.v, agg, cmap, nc, ncols, false, &H.rp, &H.ci, &H.v, &H.nnz, s);
     return H;
 }
 
@@ -977,6 +991,7 @@ __global__ void k_max_int(int n, const int* __restrict__ a, int* out) {
 Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s) {
     Sell S;
     S.n = A.n;
+    S.chi = A.n - 1;  // raised by the caller on a level with an upper halo
     S.nslices = (A.n + 31) / 32;
     int* width = dalloc<int>((size_t)S.nslices + 1, s);
     CK(cudaMemsetAsync(width + S.nslices, 0, sizeof(int), s));

@@ -18,7 +18,7 @@
 
 namespace amg {
 
-long long g_launches = 0;
+thread_local long long g_launches = 0;
 static int g_num_sms = 148;
 
 void init_device_props() {
@@ -273,7 +273,7 @@ struct SellOps {
     const double* sv;  // shared-memory value dictionary (VM = 1)
     const int* sc;     // shared-memory offset dictionary (CM = 1)
     int i;             // the lane's row
-    int nm1;           // n - 1
+    int chi;           // last valid column: n - 1, or n + nhi - 1 on a row-partitioned level (halo above)
     __device__ __forceinline__ void load_val(size_t e, double& v, int& vraw) const {
         if constexpr (CM == 3) vraw = ld_stream_u16(pcode + e);
         else if constexpr (VM == 0) v = ld_stream_d(val + e);
@@ -290,7 +290,7 @@ struct SellOps {
         if constexpr (CM == 0) return craw;
         else {
             const int c = i + ((CM == 1 || CM == 3) ? sc[craw] : craw);
-            return c < nm1 ? c : nm1;  // lanes past n (last slice) read a valid element
+            return c < chi ? c : chi;  // lanes past n (last slice) read a valid element
         }
     }
     __device__ __forceinline__ double value(double v, int vraw) const {
@@ -312,6 +312,8 @@ __device__ __forceinline__ double sell_row(const SellOps<VM, CM>& ops, size_t e0
     for (int u = 0; u < W; ++u) ops.load_val(e0 + (size_t)u * 32, v[u], vr[u]);
 #pragma unroll
     for (int u = 0; u < W; ++u) c[u] = ops.load_col(e0 + (size_t)u * 32, vr[u]);
+    // columns are >= -2^30 (halo below the own rows of a row-partitioned level; setup checks
+    // nlo < 2^30), so the OR of any set of them (and of the non-negative codes) is >= -2^30
     int all = 0, vdep = -1;
 #pragma unroll
     for (int u = 0; u < W; ++u) {
@@ -319,9 +321,9 @@ __device__ __forceinline__ double sell_row(const SellOps<VM, CM>& ops, size_t e0
         all |= c[u];
         if constexpr (VM == 0) vdep &= __double2hiint(v[u]); else all |= vr[u];
     }
-    // z == 0 always (columns and codes are >= 0; no stored value has the NaN high word 0x7ff80001),
+    // z == 0 always (the OR of columns and codes is >= -2^30; no stored value has the NaN high word 0x7ff80001),
     // but it depends on every column and value load, so every stream load is issued before any gather
-    const int z = (all < 0 || vdep == 0x7ff80001) ? 1 : 0;
+    const int z = (all < -(1 << 30) || vdep == 0x7ff80001) ? 1 : 0;
 #pragma unroll
     for (int u = 0; u < W; ++u) x[u] = ld_gather(xg + (c[u] | z));
     double s = 0.0;
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(kBlock) k_sell(Sell S, const double* __restric
         if (sn < S.nslices) { bn = __ldg(S.sptr + sn); en = __ldg(S.sptr + sn + 1); }
         const int i = sl * 32 + lane;
         const bool act = i < S.n;
-        const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, i, S.n - 1};
+        const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, i, S.chi};
         typename Epi::Pre pre{};
         double xi = 0.0;
         if (act) {  // independent row operands first (their latency overlaps the matrix stream)
@@ -741,16 +743,21 @@ void launch_dot(int n, const double* x, const double* y, double* out, const DotS
     ++g_launches;
 }
 
-__global__ void __launch_bounds__(kBlock) k_sub_scalar(int n, double* __restrict__ v, const double* __restrict__ sum) {
+__global__ void __launch_bounds__(kBlock) k_sub_scalar(int n, double ntot, double* __restrict__ v,
+                                                       const double* __restrict__ sum) {
     pdl_trigger();
     pdl_wait();
-    const double mu = (*sum) / (double)n;
+    const double mu = (*sum) / ntot;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] -= mu;
 }
 
 void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cudaStream_t s) {
     launch_dot(n, v, nullptr, tmp, ds, s);
-    launch_k(k_sub_scalar, dim3(vgrid(n)), dim3(kBlock), 0, s, n, v, (const double*)tmp);
+    launch_sub_mean(n, (double)n, v, tmp, s);
+}
+
+void launch_sub_mean(int n, double ntot, double* v, const double* sum, cudaStream_t s) {
+    launch_k(k_sub_scalar, dim3(vgrid(n)), dim3(kBlock), 0, s, n, ntot, v, sum);
     CK(cudaGetLastError());
     ++g_launches;
 }
