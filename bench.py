@@ -4,8 +4,10 @@
 A step = one pass of the whole hot path over the workload:
 amg_setup (validation, A_0, lambda_1, matching passes, Galerkin, coarsest inverse, tiles) +
 amg_solve (outer FCG + k-cycle to tol = 1e-8 from x_0 = 0) + amg_free, inputs resident in HBM.
-value = n * iters / (time per step), i.e. unknowns*iterations per second, whole job (sum over
-ranks / max-over-ranks time).  `e2e` repeats the step through the same C ABI with pinned HOST
+value = n * iters / (time per step), i.e. unknowns*iterations per second of the whole job.  With
+--gpus N > 1 (torchrun, one process per GPU) the SAME problem is row-partitioned over the N GPUs
+(amg_setup_dist over an NCCL communicator: halo exchange per SpMV-class pass, rank-order allreduce of
+the FCG dots, gathered coarse levels) -- strong scaling, time = max over ranks.  `e2e` repeats the step through the same C ABI with pinned HOST
 buffers (host<->device copies inside the timed region).  The dominant kernel (the fused
 three-term smoother step on level 0) is timed live with CUDA events inside the replayed graph.
 
@@ -45,6 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="use the row-partitioned path even on one GPU")
     return ap.parse_args()
 
 
@@ -159,12 +162,12 @@ def main_ours(a):
     import torch
 
     rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        dist.init_process_group("nccl", device_id=dev)
     from inputs import gen
     from paper_1307_6305_b200 import amg
 
@@ -176,14 +179,33 @@ def main_ours(a):
     stream = torch.cuda.current_stream(dev)
     opts = amg.amg_options_default(coarsest_size=prm["coarsest_size"], seed=prm["seed"],
                                    stream=stream.cuda_stream)
+    comm = None
+    beg, end = 0, n
+    arrs = (prob.rp, prob.ci, prob.val, prob.d)
+    if world > 1 or a.dist:  # row-partitioned over the ranks (NCCL communicator owned by the library)
+        from paper_1307_6305_b200 import dist as pdist
+
+        if world > 1:
+            comm = pdist.nccl_comm(rank, world, lambda buf: pdist.torch_broadcast_bytes(buf, device=dev))
+        else:  # --dist at N = 1: the distributed code path over a one-rank NCCL communicator
+            comm = pdist.nccl_comm(0, 1, lambda buf: buf)
+        offs = pdist.row_blocks(n, world)
+        beg, end = offs[rank], offs[rank + 1]
+        arrs = pdist.local_block(prob.rp, prob.ci, prob.val, prob.d, beg, end)
+    nl = end - beg
+
+    def setup(rp, ci, val, d):
+        if comm is None:
+            return amg.amg_setup(rp, ci, val, d, prm["passes"], prm["degree"], opts)
+        return amg.amg_setup_dist(comm, n, beg, rp, ci, val, d, prm["passes"], prm["degree"], opts)
+
     # device-resident inputs (value) and pinned host inputs (e2e)
-    d_arrs = [torch.from_numpy(x).to(dev) for x in (prob.rp, prob.ci, prob.val, prob.d)] if prob.d is not None else \
-        [torch.from_numpy(x).to(dev) for x in (prob.rp, prob.ci, prob.val)] + [None]
-    b_dev = torch.from_numpy(b_np).to(dev)
-    x_dev = torch.zeros(n, dtype=torch.float64, device=dev)
+    d_arrs = [None if x is None else torch.from_numpy(x).to(dev) for x in arrs]
+    b_dev = torch.from_numpy(b_np[beg:end].copy()).to(dev)
+    x_dev = torch.zeros(nl, dtype=torch.float64, device=dev)
 
     def step_device():
-        h = amg.amg_setup(*d_arrs, prm["passes"], prm["degree"], opts)
+        h = setup(*d_arrs)
         x_dev.zero_()
         st, it, rr = amg.amg_solve(h, b_dev, x_dev, prm["tol"], prm["k_inner"])
         info = amg.amg_get_info(h)
@@ -217,7 +239,7 @@ def main_ours(a):
     iters = [i[1] for i in infos]
     status = [i[0] for i in infos]
     last = infos[-1][3]
-    units = n * sum(iters) * world
+    units = n * sum(iters)  # the whole problem per iteration (strong scaling over the ranks)
     value = units / (ms / 1e3)
     setup_ms = statistics.mean(i[3]["setup_ms"] for i in infos)
     solve_ms = statistics.mean(i[3]["solve_ms"] for i in infos)
@@ -228,12 +250,12 @@ def main_ours(a):
     # ---- e2e: same step through the C ABI with pinned host buffers
     e2e = None
     if not a.no_e2e:
-        h_arrs = [torch.from_numpy(x).pin_memory() if x is not None else None for x in (prob.rp, prob.ci, prob.val, prob.d)]
-        b_h = torch.from_numpy(b_np).pin_memory()
-        x_h = torch.zeros(n, dtype=torch.float64).pin_memory()
+        h_arrs = [torch.from_numpy(x).pin_memory() if x is not None else None for x in arrs]
+        b_h = torch.from_numpy(b_np[beg:end].copy()).pin_memory()
+        x_h = torch.zeros(nl, dtype=torch.float64).pin_memory()
 
         def step_host():
-            h = amg.amg_setup(*h_arrs, prm["passes"], prm["degree"], opts)
+            h = setup(*h_arrs)
             x_h.zero_()
             st, it, rr = amg.amg_solve(h, b_h, x_h, prm["tol"], prm["k_inner"])
             amg.amg_free(h)
@@ -255,12 +277,17 @@ def main_ours(a):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ems = float(t.item())
         h2d = sum(x.numel() * x.element_size() for x in h_arrs if x is not None) + 2 * b_h.numel() * 8
-        e2e = {"value": n * sum(its) * world / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        if world > 1:  # bytes of the whole job
+            t = torch.tensor([float(h2d)], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t)
+            h2d = t.item()
+        e2e = {"value": n * sum(its) / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(n * 8), "ms_per_step": ems / ke, "steps": ke}
 
     if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
+        torch.distributed.barrier()
+        amg.amg_comm_free(comm)
+        torch.distributed.destroy_process_group()
         return
 
     # ---- roofline of the dominant kernel (level-0 fused smoother step), live CUDA-event timing
@@ -302,13 +329,16 @@ def main_ours(a):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[a.config], "config": a.config, "n": n, "nnz": nnz,
                    "levels": last["levels"], "n_levels": last["n"], "iters": iters, "status": status,
                    "grid_complexity": last["grid_complexity"], "operator_complexity": last["operator_complexity"],
                    "l2": "inputs larger than L2 (CSR+vectors >> 126 MB); no flush",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"row-partitioned x{world} over NCCL (decoupled aggregation, halo per SpMV pass, "
+                                   f"rank-order dot allreduce, levels < {opts.gather_rows} rows gathered; "
+                                   f"{last['dist_levels']} partitioned levels)") if comm is not None else "single GPU",
                    "step": "amg_setup + amg_solve(x0=0, tol 1e-8) + amg_free, inputs resident in HBM"},
         "setup_ms": setup_ms, "solve_ms": solve_ms,
         "solve_only": {"value": n * statistics.mean(iters) / (solve_ms / 1e3), "unit": UNIT,
@@ -318,7 +348,10 @@ def main_ours(a):
         "final_relres": infos[-1][2], "true_relres": last["last_true_relres"],
     }
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        amg.amg_comm_free(comm)
     if world > 1:
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 
 

@@ -123,6 +123,7 @@ struct ThreadComm final : Comm {
             return;
         }
         const bool ok = sh->cv.wait_for(lk, std::chrono::seconds(300), [&] { return sh->gen != g || sh->aborted; });
+        if (sh->gen != g) return;  // the barrier completed (an abort after it concerns later exchanges)
         if (!ok || sh->aborted) {
             sh->aborted = true;
             sh->cv.notify_all();

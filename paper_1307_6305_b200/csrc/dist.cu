@@ -263,15 +263,19 @@ static void finish_halo(amg_hierarchy* h, Level& Lv, const std::vector<std::vect
     Halo& H = Lv.H;
     H.send.clear();
     std::vector<int> sidx;
+    int bad = 0;
     for (int q = 0; q < (int)got.size(); ++q) {
         if (q == h->comm->rank || got[q].empty()) continue;
         H.send.push_back({q, (int)sidx.size(), (int)got[q].size()});
         for (int G : got[q]) {
-            if ((int64_t)G < Lv.gbeg || (int64_t)G >= Lv.gbeg + Lv.A.n)
-                throw Error(AMG_E_INPUT, "halo request outside the owner's block (asymmetric pattern across blocks)");
+            if ((int64_t)G < Lv.gbeg || (int64_t)G >= Lv.gbeg + Lv.A.n) bad = 1;
             sidx.push_back((int)(G - Lv.gbeg));
         }
     }
+    // collective decision: every rank fails together (no rank is left waiting in a later exchange)
+    const std::vector<int> bads = allgather_host<int>(h->comm, bad, s);
+    if (std::accumulate(bads.begin(), bads.end(), 0))
+        throw Error(AMG_E_INPUT, "halo request outside the owner's block (asymmetric pattern across blocks)");
     H.nsend = (int)sidx.size();
     H.sidx = halloc<int>(h, sidx.size());
     H.sbuf = halloc<double>(h, sidx.size());

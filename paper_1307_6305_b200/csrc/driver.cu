@@ -824,7 +824,10 @@ static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t 
     } catch (const Error& e) {
         g_last_error = e.what();
         cudaGetLastError();
-        if (h->comm && e.code != AMG_E_NCCL) h->comm->abort();
+        // argument, input and stagnation errors are collective decisions (every rank throws them);
+        // any other error is local: wake and fail the other ranks instead of leaving them waiting
+        if (h->comm && e.code != AMG_E_NCCL && e.code != AMG_E_ARG && e.code != AMG_E_INPUT && e.code != AMG_E_SETUP)
+            h->comm->abort();
         release(h);
         return e.code;
     } catch (const std::exception& e) {

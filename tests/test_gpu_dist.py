@@ -229,3 +229,34 @@ def test_dist_bad_blocks_fail_on_every_rank(amg, gen_mod):
         return 0
 
     assert run_ranks(amg, 2, fn) == [amg.AMG_E_ARG, amg.AMG_E_ARG]
+
+
+def test_nccl_one_rank_matches_single_gpu(amg, gen_mod):
+    """The NCCL backend (dlopen'd libnccl, grouped send/recv, allgather, CUDA-graph capture of the
+    exchanges) on a one-rank communicator: bitwise the single-GPU result."""
+    p = gen_mod.problem("C2", size=160)
+    from inputs import gen
+
+    b = gen.rhs(p.n, 0)
+    o = amg.amg_options_default(coarsest_size=1000, gather_rows=0)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 3, 3, o)
+    x1 = np.zeros(p.n)
+    st1, it1, _ = amg.amg_solve(h, b, x1, 1e-8, 2)
+    amg.amg_free(h)
+    uid = amg.amg_comm_unique_id()
+    comm = amg.amg_comm_init_nccl(uid, 1, 0)
+    try:
+        assert amg.amg_comm_rank(comm) == (0, 1)
+        hd = amg.amg_setup_dist(comm, p.n, 0, p.rp, p.ci, p.val, p.d, 3, 3, o)
+        info = amg.amg_get_info(hd)
+        assert info["nranks"] == 1 and info["dist_levels"] >= 1
+        x2 = np.zeros(p.n)
+        st2, it2, _ = amg.amg_solve(hd, b, x2, 1e-8, 2)
+        x3 = np.zeros(p.n)
+        amg.amg_solve(hd, b, x3, 1e-8, 2)  # replay of the captured graphs
+        amg.amg_free(hd)
+    finally:
+        amg.amg_comm_free(comm)
+    assert st1 == st2 == 0 and it1 == it2
+    assert np.linalg.norm(x1 - x2) <= 1e-12 * np.linalg.norm(x1)
+    assert np.array_equal(x2, x3)
