@@ -444,6 +444,358 @@ __global__ void __launch_bounds__(kBlock) k_sell(Sell S, const double* __restric
     if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
 }
 
+// Software-pipelined SELL-32 kernel for levels whose slices are all <= W wide (W = 5 or 8: the 2D / 3D
+// grid operators).  Each warp walks its slices s, s + nwarps, ...; while the dependent x gathers of
+// slice s are in flight, the stream loads (codes / values, f, x_{k-1}, x_i) of its NEXT slice are
+// already issued, so a slice costs one overlapped memory round trip instead of two dependent ones.
+// Same arithmetic as k_sell (fma chain in slice-entry order), so the results are bitwise equal.
+template <int W, int VM, int CM, class Pre>
+struct PipeBuf {
+    int vr[W];
+    double v[W];
+    int c[W];
+    Pre pre;
+    double xi;
+};
+
+template <class Epi, int W, int VM, int CM>
+__device__ __forceinline__ void pipe_load(const Sell& S, const SellOps<VM, CM>& ops, const Epi& epi, const double* xg,
+                                          int b, int w, int lane, int i,
+                                          PipeBuf<W, VM, CM, typename Epi::Pre>& B) {
+    const size_t e0 = (size_t)b * 32 + lane;
+#pragma unroll
+    for (int u = 0; u < W; ++u)
+        if (u < w) ops.load_val(e0 + (size_t)u * 32, B.v[u], B.vr[u]);
+#pragma unroll
+    for (int u = 0; u < W; ++u)
+        if (u < w) B.c[u] = ops.load_col(e0 + (size_t)u * 32, B.vr[u]);
+    if (i < S.n) {
+        B.pre = epi.load(i);
+        B.xi = ld_gather(xg + i);
+    }
+}
+
+template <class Epi, bool DOTS, int VM, int CM, int W>
+__global__ void __launch_bounds__(kBlock) k_sell_pipe(Sell S, const double* __restrict__ xg, Epi epi,
+                                                      double* partials, unsigned* ticket, DotOut dot_out) {
+    __shared__ double sv[VM ? 256 : 1];
+    __shared__ int sc[(CM == 1 || CM == 3) ? 256 : 1];
+    pdl_trigger();
+    if constexpr (VM == 1)
+        for (int k = threadIdx.x; k < S.nvdict; k += blockDim.x) sv[k] = S.vdict[k];
+    if constexpr (CM == 1 || CM == 3)
+        for (int k = threadIdx.x; k < S.ncdict; k += blockDim.x) sc[k] = S.cdict[k];
+    if constexpr (VM == 1 || CM == 1 || CM == 3) __syncthreads();
+    pdl_wait();
+    double acc[Epi::ND > 0 ? Epi::ND : 1];
+#pragma unroll
+    for (int k = 0; k < (Epi::ND > 0 ? Epi::ND : 1); ++k) acc[k] = 0.0;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    using Buf = PipeBuf<W, VM, CM, typename Epi::Pre>;
+    if (sl < S.nslices) {
+        int b = __ldg(S.sptr + sl), w = __ldg(S.sptr + sl + 1) - b;
+        Buf A{};
+        {
+            const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, sl * 32 + lane, S.chi};
+            pipe_load<Epi, W, VM, CM>(S, ops, epi, xg, b, w, lane, sl * 32 + lane, A);
+        }
+        int sn = sl + nwarps, bn = 0, wn = 0;
+        if (sn < S.nslices) { bn = __ldg(S.sptr + sn); wn = __ldg(S.sptr + sn + 1) - bn; }
+        for (;;) {
+            // issue the next slice's streams before this slice's gathers
+            Buf B{};
+            if (sn < S.nslices) {
+                const SellOps<VM, CM> opn{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, sn * 32 + lane, S.chi};
+                pipe_load<Epi, W, VM, CM>(S, opn, epi, xg, bn, wn, lane, sn * 32 + lane, B);
+            }
+            const int s2 = sn + nwarps;
+            int b2 = 0, w2 = 0;
+            if (s2 < S.nslices) { b2 = __ldg(S.sptr + s2); w2 = __ldg(S.sptr + s2 + 1) - b2; }
+            // this slice: gathers and the fma chain in entry order
+            const int i = sl * 32 + lane;
+            const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, i, S.chi};
+            double x[W];
+#pragma unroll
+            for (int u = 0; u < W; ++u)
+                if (u < w) x[u] = ld_gather(xg + ops.column(A.c[u]));
+            double sum = 0.0;
+#pragma unroll
+            for (int u = 0; u < W; ++u)
+                if (u < w) sum = fma(ops.value(A.v[u], A.vr[u]), x[u], sum);
+            if (i < S.n) epi.store(i, sum, A.xi, A.pre, acc);
+            if (sn >= S.nslices) break;
+            A = B;
+            sl = sn;
+            w = wn;
+            sn = s2;
+            bn = b2;
+            wn = w2;
+        }
+    }
+    if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
+}
+
+// ------------------------------------------------------------------ TMA-staged smoother step
+// The fused three-term step on a SELL level whose slices are all <= W wide, with every STREAM (the
+// slice's value/column code runs, f, x_{k-1} and the x_k tile of the chunk's own rows) moved by the
+// bulk-copy engine (cp.async.bulk global -> shared, completion on an mbarrier) through an NS-stage
+// ring in shared memory.  A chunk is 8 slices = 256 rows; warp w of the 8 consumer warps owns slice
+// 8c + w; a 9th warp (one lane) is the producer, NS - 1 chunks ahead.  The consumer warps only issue
+// the dependent x gathers (L1/L2), so the DRAM streams stay in flight without costing registers.
+// Same arithmetic as k_sell (fma chain in slice-entry order): bitwise-equal results.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MBW_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_u16(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s16(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_u8(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
+constexpr int kTmaWarps = 8;  // consumer warps per CTA (+1 producer warp)
+constexpr int kBndAhead = 4;  // producer fetches slice offsets this many chunks early
+constexpr int kBndRing = 8;   // ring of fetched offsets (> kBndAhead)
+
+template <int VM, int CM>
+struct TmaStreams {
+    static constexpr int ESA = CM == 3 ? 2 : (VM == 0 ? 8 : 1);              // value / pair stream
+    static constexpr int ESB = CM == 3 ? 0 : (CM == 0 ? 4 : (CM == 1 ? 1 : 2)); // column stream
+};
+
+__host__ __device__ constexpr int tma_align16(int x) { return (x + 15) & ~15; }
+
+// chunk = kTmaWarps * SPW slices (each consumer warp owns SPW slices of it); NS-stage ring
+template <int VM, int CM, int W, int SPW, int NS>
+struct TmaLayout {
+    static constexpr int CS = kTmaWarps * SPW;  // slices per chunk
+    static constexpr int ROWS = 32 * CS;
+    static constexpr int HDR = tma_align16(4 * (CS + 1));
+    static constexpr int A = tma_align16(CS * W * 32 * TmaStreams<VM, CM>::ESA);
+    static constexpr int B = tma_align16(CS * W * 32 * TmaStreams<VM, CM>::ESB);
+    static constexpr int V = ROWS * 8;
+    static constexpr int STAGE = HDR + A + B + 3 * V;
+    static constexpr int BYTES = NS * STAGE + 2 * NS * 8 + 16;
+};
+
+struct TmaSmoothArgs {
+    const double* f;
+    const double* xprev;
+    double* out;
+    double alpha, beta, cg, cp;
+};
+
+template <int VM, int CM, int W, int SPW, int NS>
+__global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth_tma(Sell S, const double* __restrict__ xg,
+                                                                     TmaSmoothArgs a) {
+    using Lay = TmaLayout<VM, CM, W, SPW, NS>;
+    using St = TmaStreams<VM, CM>;
+    constexpr int CS = Lay::CS;
+    extern __shared__ __align__(128) unsigned char tsm[];
+    __shared__ double sv[VM ? 256 : 1];
+    __shared__ int sc[(CM == 1 || CM == 3) ? 256 : 1];
+    __shared__ int bnd[kBndRing * (CS + 1)];
+    uint64_t* full = reinterpret_cast<uint64_t*>(tsm + NS * Lay::STAGE);
+    uint64_t* empty = full + NS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < NS; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kTmaWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (VM == 1)
+        for (int k = threadIdx.x; k < S.nvdict; k += blockDim.x) sv[k] = S.vdict[k];
+    if constexpr (CM == 1 || CM == 3)
+        for (int k = threadIdx.x; k < S.ncdict; k += blockDim.x) sc[k] = S.cdict[k];
+    __syncthreads();
+    pdl_wait();
+    const int nchunks = (S.nslices + CS - 1) / CS;
+    const int K = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const unsigned char* gA = CM == 3 ? reinterpret_cast<const unsigned char*>(S.pcode)
+                                      : (VM == 0 ? reinterpret_cast<const unsigned char*>(S.val) : S.vcode);
+    const unsigned char* gB = CM == 0 ? reinterpret_cast<const unsigned char*>(S.col)
+                                      : (CM == 1 ? S.ccode : reinterpret_cast<const unsigned char*>(S.coff));
+    if (warp == kTmaWarps) {  // producer: one lane
+        if (lane != 0) return;
+        // The chunk's slice offsets (sptr) are fetched kBndAhead chunks early with 4-byte cp.async into a
+        // shared ring, so the copy issue never waits on a dependent global load.
+        auto fetch_bounds = [&](int k) {
+            if (k < K) {
+                const int s0 = (blockIdx.x + k * gridDim.x) * CS, s1 = min(s0 + CS, S.nslices);
+                int* dst = bnd + (k % kBndRing) * (CS + 1);
+                for (int q = 0; q <= CS; ++q)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + q)),
+                                 "l"(S.sptr + min(s0 + q, s1))
+                                 : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        for (int k = 0; k < kBndAhead; ++k) fetch_bounds(k);
+        for (int k = 0; k < K; ++k) {
+            fetch_bounds(k + kBndAhead);
+            asm volatile("cp.async.wait_group %0;" ::"n"(kBndAhead) : "memory");
+            const int* hb = bnd + (k % kBndRing) * (CS + 1);
+            const int st = k % NS, j = k / NS;
+            if (j > 0) mbar_wait(&empty[st], (j - 1) & 1);
+            unsigned char* sb = tsm + st * Lay::STAGE;
+            int* hdr = reinterpret_cast<int*>(sb);
+            const int c = blockIdx.x + k * gridDim.x;
+            const int s0 = c * CS, s1 = min(s0 + CS, S.nslices);
+            for (int q = 0; q <= CS; ++q) hdr[q] = hb[q];
+            const int b0 = hdr[0], b1 = hdr[CS];
+            const int r0 = s0 * 32, r1 = min(s1 * 32, S.n);
+            const uint32_t vb = (uint32_t)tma_align16((r1 - r0) * 8);
+            const uint32_t ab = (uint32_t)(b1 - b0) * 32u * St::ESA;
+            const uint32_t bb = (uint32_t)(b1 - b0) * 32u * St::ESB;
+            mbar_expect_tx(&full[st], ab + bb + vb * (a.xprev ? 3u : 2u));
+            if (ab) bulk_g2s(sb + Lay::HDR, gA + (size_t)b0 * 32 * St::ESA, ab, &full[st]);
+            if (bb) bulk_g2s(sb + Lay::HDR + Lay::A, gB + (size_t)b0 * 32 * St::ESB, bb, &full[st]);
+            bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B, xg + r0, vb, &full[st]);
+            bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + Lay::V, a.f + r0, vb, &full[st]);
+            if (a.xprev) bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + 2 * Lay::V, a.xprev + r0, vb, &full[st]);
+        }
+        return;
+    }
+    // consumers: shared-window addresses are formed once (32-bit ld.shared below)
+    const uint32_t tsm_a = smem_u32(tsm), sv_a = smem_u32(sv), sc_a = smem_u32(sc);
+    const double* __restrict__ xgr = xg;
+    for (int k = 0; k < K; ++k) {
+        const int st = k % NS, j = k / NS;
+        mbar_wait(&full[st], j & 1);
+        const uint32_t sb = tsm_a + st * Lay::STAGE;
+        const int c = blockIdx.x + k * gridDim.x;
+        const int h0 = lds_s32(sb);
+        // this warp's SPW slices of the chunk: codes -> columns, then every gather, then the fma chains
+        int craw[SPW][W], w[SPW], col[SPW][W];
+        uint32_t aoff[SPW];
+#pragma unroll
+        for (int h = 0; h < SPW; ++h) {
+            const int q = warp + h * kTmaWarps;
+            const int s = c * CS + q;
+            const int hq = lds_s32(sb + 4 * q), hq1 = lds_s32(sb + 4 * (q + 1));
+            w[h] = s < S.nslices ? hq1 - hq : 0;
+            const uint32_t off = (uint32_t)(hq - h0);
+            aoff[h] = off;
+            const uint32_t A = sb + Lay::HDR + off * 32 * St::ESA + lane * St::ESA;
+            const uint32_t Bc = sb + Lay::HDR + Lay::A + off * 32 * St::ESB + lane * St::ESB;
+            const int i = s * 32 + lane;
+            auto entry = [&](int u) {
+                int cr;
+                if constexpr (CM == 3) {
+                    craw[h][u] = lds_u16(A + u * 64);
+                    cr = craw[h][u] >> 8;
+                } else {
+                    if constexpr (VM == 1) craw[h][u] = lds_u8(A + u * 32);
+                    if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
+                    else if constexpr (CM == 1) cr = lds_u8(Bc + u * 32);
+                    else cr = lds_s16(Bc + u * 64);
+                }
+                int cc;
+                if constexpr (CM == 0) cc = cr;
+                else {
+                    cc = i + ((CM == 1 || CM == 3) ? lds_s32(sc_a + 4 * cr) : cr);
+                    cc = cc < S.chi ? cc : S.chi;
+                }
+                col[h][u] = cc;
+            };
+            if (w[h] == W) {  // full-width slice (the common case): straight-line
+#pragma unroll
+                for (int u = 0; u < W; ++u) entry(u);
+            } else {
+#pragma unroll
+                for (int u = 0; u < W; ++u)
+                    if (u < w[h]) entry(u);
+            }
+        }
+        double x[SPW][W];
+#pragma unroll
+        for (int h = 0; h < SPW; ++h) {
+            if (w[h] == W) {
+#pragma unroll
+                for (int u = 0; u < W; ++u) x[h][u] = ld_gather(xgr + col[h][u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < W; ++u)
+                    if (u < w[h]) x[h][u] = ld_gather(xgr + col[h][u]);
+            }
+        }
+        const uint32_t vt = sb + Lay::HDR + Lay::A + Lay::B;
+#pragma unroll
+        for (int h = 0; h < SPW; ++h) {
+            const int q = warp + h * kTmaWarps;
+            const uint32_t A = sb + Lay::HDR + aoff[h] * 32 * St::ESA + lane * St::ESA;
+            double sum = 0.0;
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                if (u < w[h]) {
+                    double v;
+                    if constexpr (VM == 0) v = lds_f64(A + u * 256);
+                    else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[h][u] & 0xff) : craw[h][u]));
+                    sum = fma(v, x[h][u], sum);
+                }
+            }
+            const int i = (c * CS + q) * 32 + lane;
+            const uint32_t r8 = 8 * (q * 32 + lane);
+            if (w[h] > 0 && i < S.n) {
+                const double xi = lds_f64(vt + r8), fi = lds_f64(vt + Lay::V + r8);
+                const double prev = a.xprev ? lds_f64(vt + 2 * Lay::V + r8) : a.cp * fi;
+                a.out[i] = a.alpha * (a.cg * xi) + (1.0 - a.alpha) * prev + a.beta * (fi - a.cg * sum);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+}
+
 // resident grid of one kernel instance (cached per instance and dynamic smem size)
 template <class K>
 static int resident_grid(K kernel, size_t smem) {
@@ -475,12 +827,30 @@ int tiled_grid(int cap, int ntiles) {
     return g < 1 ? 1 : g;
 }
 
+// AMG_PIPE=1 selects the register-pipelined k_sell_pipe (measured slower on the compressed levels)
+static bool pipe_enabled() {
+    static int on = -1;
+    if (on < 0) on = getenv("AMG_PIPE") ? 1 : 0;
+    return on == 1;
+}
+
 template <class Epi, bool DOTS, int VM, int CM, int WMAX>
 static void launch_sell_w(const SpOp& op, const double* xg, const Epi& epi, double* part, unsigned* tk,
                           DotOut dot_out, cudaStream_t s) {
+    const int need = (op.S.nslices + (kBlock / 32) - 1) / (kBlock / 32);
+    if constexpr (WMAX == 5 || WMAX == 8) {
+        if (pipe_enabled()) {
+            static int res = 0;  // per instance
+            if (!res) res = resident_grid(k_sell_pipe<Epi, DOTS, VM, CM, WMAX>, 0);
+            int g = need < res ? need : res;
+            if (g < 1) g = 1;
+            launch_k(k_sell_pipe<Epi, DOTS, VM, CM, WMAX>, dim3(g), dim3(kBlock), 0, s, op.S, xg, epi, part, tk,
+                     dot_out);
+            return;
+        }
+    }
     static int res = 0;  // per instance
     if (!res) res = resident_grid(k_sell<Epi, DOTS, VM, CM, WMAX>, 0);
-    int need = (op.S.nslices + (kBlock / 32) - 1) / (kBlock / 32);
     int g = need < res ? need : res;
     if (g < 1) g = 1;
     launch_k(k_sell<Epi, DOTS, VM, CM, WMAX>, dim3(g), dim3(kBlock), 0, s, op.S, xg, epi, part, tk, dot_out);
@@ -524,8 +894,74 @@ static void launch_op(const SpOp& op, const double* xg, const Epi& epi, const Do
     ++g_launches;
 }
 
+
+static bool tma_enabled() {
+    static int on = -1;
+    if (on < 0) on = getenv("AMG_NO_TMA") ? 0 : 1;
+    return on == 1;
+}
+
+template <int VM, int CM, int W, int SPW, int NS>
+static void launch_smooth_tma_w(const SpOp& op, const double* xg, const TmaSmoothArgs& a, cudaStream_t s) {
+    using Lay = TmaLayout<VM, CM, W, SPW, NS>;
+    static int res = 0;  // resident grid per instance
+    if (!res) {
+        CK(cudaFuncSetAttribute(k_smooth_tma<VM, CM, W, SPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                Lay::BYTES));
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_smooth_tma<VM, CM, W, SPW, NS>,
+                                                         32 * (kTmaWarps + 1), Lay::BYTES));
+        res = g_num_sms * (bps < 1 ? 1 : bps);
+    }
+    const int nchunks = (op.S.nslices + Lay::CS - 1) / Lay::CS;
+    const int g = nchunks < res ? nchunks : res;
+    launch_k(k_smooth_tma<VM, CM, W, SPW, NS>, dim3(g < 1 ? 1 : g), dim3(32 * (kTmaWarps + 1)), (size_t)Lay::BYTES,
+             s, op.S, xg, a);
+}
+
+// compressed streams (few bytes per row): 2 slices per consumer warp keep twice the gathers in flight;
+// fp64/int32 streams are already bandwidth-bound with one slice per warp
+template <int VM, int CM, int W>
+static void launch_smooth_tma_v(const SpOp& op, const double* xg, const TmaSmoothArgs& a, cudaStream_t s) {
+    static int var = -1;  // AMG_TMA_VARIANT (experiments): 0 = 1 slice/warp 4 stages, 1 = 2 slices 3 stages,
+                          // 2 = 1 slice 2 stages, 3 = 2 slices 2 stages
+    if (var < 0) var = getenv("AMG_TMA_VARIANT") ? atoi(getenv("AMG_TMA_VARIANT")) : (VM == 1 ? 1 : 0);
+    switch (var) {
+        case 1: launch_smooth_tma_w<VM, CM, W, 2, 3>(op, xg, a, s); break;
+        case 2: launch_smooth_tma_w<VM, CM, W, 1, 2>(op, xg, a, s); break;
+        case 3: launch_smooth_tma_w<VM, CM, W, 2, 2>(op, xg, a, s); break;
+        default: launch_smooth_tma_w<VM, CM, W, 1, 4>(op, xg, a, s); break;
+    }
+}
+
+template <int VM, int CM>
+static void launch_smooth_tma(const SpOp& op, const double* xg, const TmaSmoothArgs& a, cudaStream_t s) {
+    if (op.S.wmax <= 5) launch_smooth_tma_v<VM, CM, 5>(op, xg, a, s);
+    else launch_smooth_tma_v<VM, CM, 8>(op, xg, a, s);
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f, const double* xprev, double cp,
                    double alpha, double beta, double* out, cudaStream_t s) {
+    // TMA-staged path: SELL level with slices <= 8 wide, large enough to be bandwidth bound, and
+    // 16-byte aligned streams (bulk copies move 16-byte multiples)
+    if (tma_enabled() && op.sell && op.S.wmax <= 8 && op.S.nslices >= 8 * 148 * kTmaWarps && aligned16(xg) &&
+        aligned16(f) && (!xprev || aligned16(xprev))) {
+        TmaSmoothArgs a{f, xprev, out, alpha, beta, cg, cp};
+        switch (op.S.vmode * 4 + op.S.cmode) {
+            case 0: launch_smooth_tma<0, 0>(op, xg, a, s); break;
+            case 1: launch_smooth_tma<0, 1>(op, xg, a, s); break;
+            case 2: launch_smooth_tma<0, 2>(op, xg, a, s); break;
+            case 4: launch_smooth_tma<1, 0>(op, xg, a, s); break;
+            case 5: launch_smooth_tma<1, 1>(op, xg, a, s); break;
+            case 6: launch_smooth_tma<1, 2>(op, xg, a, s); break;
+            default: launch_smooth_tma<1, 3>(op, xg, a, s); break;
+        }
+        CK(cudaGetLastError());
+        ++g_launches;
+        return;
+    }
     EpiSmooth e{f, xprev, out, alpha, beta, cg, cp};
     launch_op<EpiSmooth, false>(op, xg, e, nullptr, DotOut{}, s);
 }

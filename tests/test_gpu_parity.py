@@ -309,3 +309,28 @@ def test_coarse_tail_kernel_parity(amg, gen_mod, oracle_mod, tail_nnz):
         assert st == 0 and abs(it3 - ref3["iters"]) <= 1
     finally:
         amg.amg_free(h)
+
+
+def test_smoother_tma_path_parity(amg, gen_mod, oracle_mod):
+    """Level 0 of the C3 recipe at 1024^2 (1M rows, compressed SELL, > 9472 slices) runs the TMA-staged
+    smoother kernel; one whole smoother application and one B_0(r) against the oracle."""
+    p = gen_mod.problem("C3", size=1024)
+    hier = oracle_mod.setup_problem(p)
+    h = gpu_setup(amg, p)
+    try:
+        assert amg.amg_get_info(h)["level0_format"] == 2
+        rng = np.random.default_rng(3)
+        n = p.n
+        f = rng.uniform(-1, 1, n)
+        x0 = rng.uniform(-1, 1, n)
+        x = np.empty(n)
+        amg.amg_level_smooth(h, 0, f, x0, x)
+        ref = hier.smooth(0, f, x0)
+        assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+        r = rng.uniform(-1, 1, n)
+        z = np.empty(n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        zr = hier.precond(r, nu=2, level=0)
+        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+    finally:
+        amg.amg_free(h)

@@ -62,6 +62,7 @@ int main(int argc, char** argv) {
     S.nslices = nsl;
     S.padded = (int64_t)nsl * 160;
     S.wmax = 5;
+    S.chi = n - 1;
     double *xg, *f, *xp, *out, *vd;
     int* cd;
     CK(cudaMalloc(&S.sptr, sizeof(int) * (nsl + 1)));
