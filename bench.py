@@ -311,7 +311,7 @@ def main_ours(a):
     survey_bytes = 12 * nnz + 36 * n  # SURVEY 8(d) model: int32 idx + fp64 values
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": "k_sell<EpiSmooth> level-0 three-term smoother step",
+            "kernel": "k_sell_tma<TEpiSmooth> level-0 fused three-term smoother step (TMA-staged SELL-32)",
             "format": fmt.get(last.get("level0_format", 1)),
             "bytes_per_launch": bytes_launch, "avg_launch_us": avg_launch_ms * 1e3, "launches_timed": prof_n,
             "peak_source": peak_src, "frac_of_8TBs": (achieved / 8000.0) if achieved else None,

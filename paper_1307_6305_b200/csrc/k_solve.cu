@@ -624,16 +624,47 @@ struct TmaLayout {
     static constexpr int BYTES = NS * STAGE + 2 * NS * 8 + 16;
 };
 
-struct TmaSmoothArgs {
+// Epilogues of the TMA path: NV row vectors are staged besides the x tile (vec(k) = their global
+// pointers, null = not staged), store() combines them with the row sum.
+struct TEpiSmooth {  // three-term recurrence step; prev = xprev ? xprev_i : cp * f_i
     const double* f;
     const double* xprev;
     double* out;
     double alpha, beta, cg, cp;
+    static constexpr int ND = 0;
+    __device__ __forceinline__ const double* vec(int k) const { return k == 0 ? f : xprev; }
+    __device__ __forceinline__ void store(int i, double s, double xi, double v0, double v1, double*) const {
+        const double prev = xprev ? v1 : cp * v0;
+        out[i] = alpha * (cg * xi) + (1.0 - alpha) * prev + beta * (v0 - cg * s);
+    }
+};
+struct TEpiResid {  // out = f - A x; acc[0] += out^2
+    const double* f;
+    double* out;
+    static constexpr int ND = 1;
+    __device__ __forceinline__ const double* vec(int k) const { return k == 0 ? f : nullptr; }
+    __device__ __forceinline__ void store(int i, double s, double, double v0, double, double* acc) const {
+        const double r = v0 - s;
+        out[i] = r;
+        acc[0] += r * r;
+    }
+};
+struct TEpiSpmvDots {  // q = A d; acc = (d.q, d.rho)
+    const double* rho;
+    double* q;
+    static constexpr int ND = 2;
+    __device__ __forceinline__ const double* vec(int k) const { return k == 0 ? rho : nullptr; }
+    __device__ __forceinline__ void store(int i, double s, double di, double v0, double, double* acc) const {
+        q[i] = s;
+        acc[0] += di * s;
+        acc[1] += di * v0;
+    }
 };
 
-template <int VM, int CM, int W, int SPW, int NS>
-__global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth_tma(Sell S, const double* __restrict__ xg,
-                                                                     TmaSmoothArgs a) {
+template <class Epi, bool DOTS, int VM, int CM, int W, int SPW, int NS>
+__global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const double* __restrict__ xg, Epi epi,
+                                                                   double* partials, unsigned* ticket,
+                                                                   DotOut dot_out) {
     using Lay = TmaLayout<VM, CM, W, SPW, NS>;
     using St = TmaStreams<VM, CM>;
     constexpr int CS = Lay::CS;
@@ -644,6 +675,9 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth_tma(Sell S, con
     uint64_t* full = reinterpret_cast<uint64_t*>(tsm + NS * Lay::STAGE);
     uint64_t* empty = full + NS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc[Epi::ND > 0 ? Epi::ND : 1];
+#pragma unroll
+    for (int k = 0; k < (Epi::ND > 0 ? Epi::ND : 1); ++k) acc[k] = 0.0;
     pdl_trigger();
     if (threadIdx.x == 0) {
         for (int k = 0; k < NS; ++k) {
@@ -660,140 +694,145 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth_tma(Sell S, con
     pdl_wait();
     const int nchunks = (S.nslices + CS - 1) / CS;
     const int K = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const unsigned char* gA = CM == 3 ? reinterpret_cast<const unsigned char*>(S.pcode)
-                                      : (VM == 0 ? reinterpret_cast<const unsigned char*>(S.val) : S.vcode);
-    const unsigned char* gB = CM == 0 ? reinterpret_cast<const unsigned char*>(S.col)
-                                      : (CM == 1 ? S.ccode : reinterpret_cast<const unsigned char*>(S.coff));
+    const double* v0g = epi.vec(0);
+    const double* v1g = epi.vec(1);
     if (warp == kTmaWarps) {  // producer: one lane
-        if (lane != 0) return;
-        // The chunk's slice offsets (sptr) are fetched kBndAhead chunks early with 4-byte cp.async into a
-        // shared ring, so the copy issue never waits on a dependent global load.
-        auto fetch_bounds = [&](int k) {
-            if (k < K) {
-                const int s0 = (blockIdx.x + k * gridDim.x) * CS, s1 = min(s0 + CS, S.nslices);
-                int* dst = bnd + (k % kBndRing) * (CS + 1);
-                for (int q = 0; q <= CS; ++q)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + q)),
-                                 "l"(S.sptr + min(s0 + q, s1))
-                                 : "memory");
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        for (int k = 0; k < kBndAhead; ++k) fetch_bounds(k);
-        for (int k = 0; k < K; ++k) {
-            fetch_bounds(k + kBndAhead);
-            asm volatile("cp.async.wait_group %0;" ::"n"(kBndAhead) : "memory");
-            const int* hb = bnd + (k % kBndRing) * (CS + 1);
-            const int st = k % NS, j = k / NS;
-            if (j > 0) mbar_wait(&empty[st], (j - 1) & 1);
-            unsigned char* sb = tsm + st * Lay::STAGE;
-            int* hdr = reinterpret_cast<int*>(sb);
-            const int c = blockIdx.x + k * gridDim.x;
-            const int s0 = c * CS, s1 = min(s0 + CS, S.nslices);
-            for (int q = 0; q <= CS; ++q) hdr[q] = hb[q];
-            const int b0 = hdr[0], b1 = hdr[CS];
-            const int r0 = s0 * 32, r1 = min(s1 * 32, S.n);
-            const uint32_t vb = (uint32_t)tma_align16((r1 - r0) * 8);
-            const uint32_t ab = (uint32_t)(b1 - b0) * 32u * St::ESA;
-            const uint32_t bb = (uint32_t)(b1 - b0) * 32u * St::ESB;
-            mbar_expect_tx(&full[st], ab + bb + vb * (a.xprev ? 3u : 2u));
-            if (ab) bulk_g2s(sb + Lay::HDR, gA + (size_t)b0 * 32 * St::ESA, ab, &full[st]);
-            if (bb) bulk_g2s(sb + Lay::HDR + Lay::A, gB + (size_t)b0 * 32 * St::ESB, bb, &full[st]);
-            bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B, xg + r0, vb, &full[st]);
-            bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + Lay::V, a.f + r0, vb, &full[st]);
-            if (a.xprev) bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + 2 * Lay::V, a.xprev + r0, vb, &full[st]);
-        }
-        return;
-    }
-    // consumers: shared-window addresses are formed once (32-bit ld.shared below)
-    const uint32_t tsm_a = smem_u32(tsm), sv_a = smem_u32(sv), sc_a = smem_u32(sc);
-    const double* __restrict__ xgr = xg;
-    for (int k = 0; k < K; ++k) {
-        const int st = k % NS, j = k / NS;
-        mbar_wait(&full[st], j & 1);
-        const uint32_t sb = tsm_a + st * Lay::STAGE;
-        const int c = blockIdx.x + k * gridDim.x;
-        const int h0 = lds_s32(sb);
-        // this warp's SPW slices of the chunk: codes -> columns, then every gather, then the fma chains
-        int craw[SPW][W], w[SPW], col[SPW][W];
-        uint32_t aoff[SPW];
-#pragma unroll
-        for (int h = 0; h < SPW; ++h) {
-            const int q = warp + h * kTmaWarps;
-            const int s = c * CS + q;
-            const int hq = lds_s32(sb + 4 * q), hq1 = lds_s32(sb + 4 * (q + 1));
-            w[h] = s < S.nslices ? hq1 - hq : 0;
-            const uint32_t off = (uint32_t)(hq - h0);
-            aoff[h] = off;
-            const uint32_t A = sb + Lay::HDR + off * 32 * St::ESA + lane * St::ESA;
-            const uint32_t Bc = sb + Lay::HDR + Lay::A + off * 32 * St::ESB + lane * St::ESB;
-            const int i = s * 32 + lane;
-            auto entry = [&](int u) {
-                int cr;
-                if constexpr (CM == 3) {
-                    craw[h][u] = lds_u16(A + u * 64);
-                    cr = craw[h][u] >> 8;
-                } else {
-                    if constexpr (VM == 1) craw[h][u] = lds_u8(A + u * 32);
-                    if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
-                    else if constexpr (CM == 1) cr = lds_u8(Bc + u * 32);
-                    else cr = lds_s16(Bc + u * 64);
+        if (lane == 0) {
+            const unsigned char* gA = CM == 3 ? reinterpret_cast<const unsigned char*>(S.pcode)
+                                              : (VM == 0 ? reinterpret_cast<const unsigned char*>(S.val) : S.vcode);
+            const unsigned char* gB = CM == 0 ? reinterpret_cast<const unsigned char*>(S.col)
+                                              : (CM == 1 ? S.ccode : reinterpret_cast<const unsigned char*>(S.coff));
+            // The chunk's slice offsets (sptr) are fetched kBndAhead chunks early with 4-byte cp.async into a
+            // shared ring, so the copy issue never waits on a dependent global load.
+            auto fetch_bounds = [&](int k) {
+                if (k < K) {
+                    const int s0 = (blockIdx.x + k * gridDim.x) * CS, s1 = min(s0 + CS, S.nslices);
+                    int* dst = bnd + (k % kBndRing) * (CS + 1);
+                    for (int q = 0; q <= CS; ++q)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + q)),
+                                     "l"(S.sptr + min(s0 + q, s1))
+                                     : "memory");
                 }
-                int cc;
-                if constexpr (CM == 0) cc = cr;
-                else {
-                    cc = i + ((CM == 1 || CM == 3) ? lds_s32(sc_a + 4 * cr) : cr);
-                    cc = cc < S.chi ? cc : S.chi;
-                }
-                col[h][u] = cc;
+                asm volatile("cp.async.commit_group;" ::: "memory");
             };
-            if (w[h] == W) {  // full-width slice (the common case): straight-line
-#pragma unroll
-                for (int u = 0; u < W; ++u) entry(u);
-            } else {
-#pragma unroll
-                for (int u = 0; u < W; ++u)
-                    if (u < w[h]) entry(u);
+            for (int k = 0; k < kBndAhead; ++k) fetch_bounds(k);
+            for (int k = 0; k < K; ++k) {
+                fetch_bounds(k + kBndAhead);
+                asm volatile("cp.async.wait_group %0;" ::"n"(kBndAhead) : "memory");
+                const int* hb = bnd + (k % kBndRing) * (CS + 1);
+                const int st = k % NS, j = k / NS;
+                if (j > 0) mbar_wait(&empty[st], (j - 1) & 1);
+                unsigned char* sb = tsm + st * Lay::STAGE;
+                int* hdr = reinterpret_cast<int*>(sb);
+                const int c = blockIdx.x + k * gridDim.x;
+                const int s0 = c * CS, s1 = min(s0 + CS, S.nslices);
+                for (int q = 0; q <= CS; ++q) hdr[q] = hb[q];
+                const int b0 = hdr[0], b1 = hdr[CS];
+                const int r0 = s0 * 32, r1 = min(s1 * 32, S.n);
+                const uint32_t vb = (uint32_t)tma_align16((r1 - r0) * 8);
+                const uint32_t ab = (uint32_t)(b1 - b0) * 32u * St::ESA;
+                const uint32_t bb = (uint32_t)(b1 - b0) * 32u * St::ESB;
+                mbar_expect_tx(&full[st], ab + bb + vb * (1u + (v0g ? 1u : 0u) + (v1g ? 1u : 0u)));
+                if (ab) bulk_g2s(sb + Lay::HDR, gA + (size_t)b0 * 32 * St::ESA, ab, &full[st]);
+                if (bb) bulk_g2s(sb + Lay::HDR + Lay::A, gB + (size_t)b0 * 32 * St::ESB, bb, &full[st]);
+                bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B, xg + r0, vb, &full[st]);
+                if (v0g) bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + Lay::V, v0g + r0, vb, &full[st]);
+                if (v1g) bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + 2 * Lay::V, v1g + r0, vb, &full[st]);
             }
         }
-        double x[SPW][W];
+    } else {
+        // consumers: shared-window addresses are formed once (32-bit ld.shared below)
+        const uint32_t tsm_a = smem_u32(tsm), sv_a = smem_u32(sv), sc_a = smem_u32(sc);
+        const double* __restrict__ xgr = xg;
+        for (int k = 0; k < K; ++k) {
+            const int st = k % NS, j = k / NS;
+            mbar_wait(&full[st], j & 1);
+            const uint32_t sb = tsm_a + st * Lay::STAGE;
+            const int c = blockIdx.x + k * gridDim.x;
+            const int h0 = lds_s32(sb);
+            // this warp's SPW slices of the chunk: codes -> columns, then every gather, then the fma chains
+            int craw[SPW][W], w[SPW], col[SPW][W];
+            uint32_t aoff[SPW];
 #pragma unroll
-        for (int h = 0; h < SPW; ++h) {
-            if (w[h] == W) {
+            for (int h = 0; h < SPW; ++h) {
+                const int q = warp + h * kTmaWarps;
+                const int s = c * CS + q;
+                const int hq = lds_s32(sb + 4 * q), hq1 = lds_s32(sb + 4 * (q + 1));
+                w[h] = s < S.nslices ? hq1 - hq : 0;
+                const uint32_t off = (uint32_t)(hq - h0);
+                aoff[h] = off;
+                const uint32_t A = sb + Lay::HDR + off * 32 * St::ESA + lane * St::ESA;
+                const uint32_t Bc = sb + Lay::HDR + Lay::A + off * 32 * St::ESB + lane * St::ESB;
+                const int i = s * 32 + lane;
+                auto entry = [&](int u) {
+                    int cr;
+                    if constexpr (CM == 3) {
+                        craw[h][u] = lds_u16(A + u * 64);
+                        cr = craw[h][u] >> 8;
+                    } else {
+                        if constexpr (VM == 1) craw[h][u] = lds_u8(A + u * 32);
+                        if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
+                        else if constexpr (CM == 1) cr = lds_u8(Bc + u * 32);
+                        else cr = lds_s16(Bc + u * 64);
+                    }
+                    int cc;
+                    if constexpr (CM == 0) cc = cr;
+                    else {
+                        cc = i + ((CM == 1 || CM == 3) ? lds_s32(sc_a + 4 * cr) : cr);
+                        cc = cc < S.chi ? cc : S.chi;
+                    }
+                    col[h][u] = cc;
+                };
+                if (w[h] == W) {  // full-width slice (the common case): straight-line
 #pragma unroll
-                for (int u = 0; u < W; ++u) x[h][u] = ld_gather(xgr + col[h][u]);
-            } else {
+                    for (int u = 0; u < W; ++u) entry(u);
+                } else {
 #pragma unroll
-                for (int u = 0; u < W; ++u)
-                    if (u < w[h]) x[h][u] = ld_gather(xgr + col[h][u]);
-            }
-        }
-        const uint32_t vt = sb + Lay::HDR + Lay::A + Lay::B;
-#pragma unroll
-        for (int h = 0; h < SPW; ++h) {
-            const int q = warp + h * kTmaWarps;
-            const uint32_t A = sb + Lay::HDR + aoff[h] * 32 * St::ESA + lane * St::ESA;
-            double sum = 0.0;
-#pragma unroll
-            for (int u = 0; u < W; ++u) {
-                if (u < w[h]) {
-                    double v;
-                    if constexpr (VM == 0) v = lds_f64(A + u * 256);
-                    else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[h][u] & 0xff) : craw[h][u]));
-                    sum = fma(v, x[h][u], sum);
+                    for (int u = 0; u < W; ++u)
+                        if (u < w[h]) entry(u);
                 }
             }
-            const int i = (c * CS + q) * 32 + lane;
-            const uint32_t r8 = 8 * (q * 32 + lane);
-            if (w[h] > 0 && i < S.n) {
-                const double xi = lds_f64(vt + r8), fi = lds_f64(vt + Lay::V + r8);
-                const double prev = a.xprev ? lds_f64(vt + 2 * Lay::V + r8) : a.cp * fi;
-                a.out[i] = a.alpha * (a.cg * xi) + (1.0 - a.alpha) * prev + a.beta * (fi - a.cg * sum);
+            double x[SPW][W];
+#pragma unroll
+            for (int h = 0; h < SPW; ++h) {
+                if (w[h] == W) {
+#pragma unroll
+                    for (int u = 0; u < W; ++u) x[h][u] = ld_gather(xgr + col[h][u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < W; ++u)
+                        if (u < w[h]) x[h][u] = ld_gather(xgr + col[h][u]);
+                }
             }
+            const uint32_t vt = sb + Lay::HDR + Lay::A + Lay::B;
+#pragma unroll
+            for (int h = 0; h < SPW; ++h) {
+                const int q = warp + h * kTmaWarps;
+                const uint32_t A = sb + Lay::HDR + aoff[h] * 32 * St::ESA + lane * St::ESA;
+                double sum = 0.0;
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    if (u < w[h]) {
+                        double v;
+                        if constexpr (VM == 0) v = lds_f64(A + u * 256);
+                        else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[h][u] & 0xff) : craw[h][u]));
+                        sum = fma(v, x[h][u], sum);
+                    }
+                }
+                const int i = (c * CS + q) * 32 + lane;
+                const uint32_t r8 = 8 * (q * 32 + lane);
+                if (w[h] > 0 && i < S.n) {
+                    const double xi = lds_f64(vt + r8);
+                    const double a0 = v0g ? lds_f64(vt + Lay::V + r8) : 0.0;
+                    const double a1 = v1g ? lds_f64(vt + 2 * Lay::V + r8) : 0.0;
+                    epi.store(i, sum, xi, a0, a1, acc);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
     }
+    if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
 }
 
 // resident grid of one kernel instance (cached per instance and dynamic smem size)
@@ -901,82 +940,102 @@ static bool tma_enabled() {
     return on == 1;
 }
 
-template <int VM, int CM, int W, int SPW, int NS>
-static void launch_smooth_tma_w(const SpOp& op, const double* xg, const TmaSmoothArgs& a, cudaStream_t s) {
+template <class Epi, bool DOTS, int VM, int CM, int W, int SPW, int NS>
+static void launch_tma_w(const SpOp& op, const double* xg, const Epi& e, double* part, unsigned* tk, DotOut dot_out,
+                         cudaStream_t s) {
     using Lay = TmaLayout<VM, CM, W, SPW, NS>;
     static int res = 0;  // resident grid per instance
     if (!res) {
-        CK(cudaFuncSetAttribute(k_smooth_tma<VM, CM, W, SPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(k_sell_tma<Epi, DOTS, VM, CM, W, SPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 Lay::BYTES));
         int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_smooth_tma<VM, CM, W, SPW, NS>,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_sell_tma<Epi, DOTS, VM, CM, W, SPW, NS>,
                                                          32 * (kTmaWarps + 1), Lay::BYTES));
         res = g_num_sms * (bps < 1 ? 1 : bps);
     }
     const int nchunks = (op.S.nslices + Lay::CS - 1) / Lay::CS;
-    const int g = nchunks < res ? nchunks : res;
-    launch_k(k_smooth_tma<VM, CM, W, SPW, NS>, dim3(g < 1 ? 1 : g), dim3(32 * (kTmaWarps + 1)), (size_t)Lay::BYTES,
-             s, op.S, xg, a);
+    int g = nchunks < res ? nchunks : res;
+    if (g < 1) g = 1;
+    if constexpr (DOTS) g = g < 4096 ? g : 4096;  // partials buffer (DotScratch) holds 4096 blocks per dot
+    launch_k(k_sell_tma<Epi, DOTS, VM, CM, W, SPW, NS>, dim3(g), dim3(32 * (kTmaWarps + 1)), (size_t)Lay::BYTES, s,
+             op.S, xg, e, part, tk, dot_out);
 }
 
-// compressed streams (few bytes per row): 2 slices per consumer warp keep twice the gathers in flight;
-// fp64/int32 streams are already bandwidth-bound with one slice per warp
-template <int VM, int CM, int W>
-static void launch_smooth_tma_v(const SpOp& op, const double* xg, const TmaSmoothArgs& a, cudaStream_t s) {
-    static int var = -1;  // AMG_TMA_VARIANT (experiments): 0 = 1 slice/warp 4 stages, 1 = 2 slices 3 stages,
-                          // 2 = 1 slice 2 stages, 3 = 2 slices 2 stages
-    if (var < 0) var = getenv("AMG_TMA_VARIANT") ? atoi(getenv("AMG_TMA_VARIANT")) : (VM == 1 ? 1 : 0);
-    switch (var) {
-        case 1: launch_smooth_tma_w<VM, CM, W, 2, 3>(op, xg, a, s); break;
-        case 2: launch_smooth_tma_w<VM, CM, W, 1, 2>(op, xg, a, s); break;
-        case 3: launch_smooth_tma_w<VM, CM, W, 2, 2>(op, xg, a, s); break;
-        default: launch_smooth_tma_w<VM, CM, W, 1, 4>(op, xg, a, s); break;
+// compressed streams (few bytes per row): 2 slices per consumer warp keep twice the gathers in
+// flight (3 stages); fp64/int32 streams are bandwidth-bound with one slice per warp (4 stages).
+// AMG_TMA_VARIANT (experiments): 0 = 1 slice/warp 4 stages, 1 = 2 slices 3 stages, 2 = 1 slice 2 stages,
+// 3 = 2 slices 2 stages.
+template <class Epi, bool DOTS, int VM, int CM, int W>
+static void launch_tma_v(const SpOp& op, const double* xg, const Epi& e, double* part, unsigned* tk, DotOut d,
+                         cudaStream_t s) {
+    static int var = -2;
+    if (var == -2) var = getenv("AMG_TMA_VARIANT") ? atoi(getenv("AMG_TMA_VARIANT")) : -1;
+    const int v = var >= 0 ? var : (VM == 1 ? 1 : 0);
+    switch (v) {
+        case 1: launch_tma_w<Epi, DOTS, VM, CM, W, 2, 3>(op, xg, e, part, tk, d, s); break;
+        case 2: launch_tma_w<Epi, DOTS, VM, CM, W, 1, 2>(op, xg, e, part, tk, d, s); break;
+        case 3: launch_tma_w<Epi, DOTS, VM, CM, W, 2, 2>(op, xg, e, part, tk, d, s); break;
+        default: launch_tma_w<Epi, DOTS, VM, CM, W, 1, 4>(op, xg, e, part, tk, d, s); break;
     }
 }
 
-template <int VM, int CM>
-static void launch_smooth_tma(const SpOp& op, const double* xg, const TmaSmoothArgs& a, cudaStream_t s) {
-    if (op.S.wmax <= 5) launch_smooth_tma_v<VM, CM, 5>(op, xg, a, s);
-    else launch_smooth_tma_v<VM, CM, 8>(op, xg, a, s);
+template <class Epi, bool DOTS, int VM, int CM>
+static void launch_tma_fmt(const SpOp& op, const double* xg, const Epi& e, double* part, unsigned* tk, DotOut d,
+                           cudaStream_t s) {
+    if (op.S.wmax <= 5) launch_tma_v<Epi, DOTS, VM, CM, 5>(op, xg, e, part, tk, d, s);
+    else launch_tma_v<Epi, DOTS, VM, CM, 8>(op, xg, e, part, tk, d, s);
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+// TMA-staged path: SELL level with slices <= 8 wide, large enough to be bandwidth bound, and 16-byte
+// aligned streams (bulk copies move 16-byte multiples).  Returns false if not eligible.
+template <class Epi, bool DOTS>
+static bool launch_tma(const SpOp& op, const double* xg, const Epi& e, const double* v0, const double* v1,
+                       const DotScratch* ds, DotOut d, cudaStream_t s) {
+    if (!(tma_enabled() && op.sell && op.S.wmax <= 8 && op.S.nslices >= 8 * 148 * kTmaWarps && aligned16(xg) &&
+          (!v0 || aligned16(v0)) && (!v1 || aligned16(v1))))
+        return false;
+    double* part = ds ? ds->partials : nullptr;
+    unsigned* tk = ds ? ds->ticket : nullptr;
+    switch (op.S.vmode * 4 + op.S.cmode) {
+        case 0: launch_tma_fmt<Epi, DOTS, 0, 0>(op, xg, e, part, tk, d, s); break;
+        case 1: launch_tma_fmt<Epi, DOTS, 0, 1>(op, xg, e, part, tk, d, s); break;
+        case 2: launch_tma_fmt<Epi, DOTS, 0, 2>(op, xg, e, part, tk, d, s); break;
+        case 4: launch_tma_fmt<Epi, DOTS, 1, 0>(op, xg, e, part, tk, d, s); break;
+        case 5: launch_tma_fmt<Epi, DOTS, 1, 1>(op, xg, e, part, tk, d, s); break;
+        case 6: launch_tma_fmt<Epi, DOTS, 1, 2>(op, xg, e, part, tk, d, s); break;
+        default: launch_tma_fmt<Epi, DOTS, 1, 3>(op, xg, e, part, tk, d, s); break;
+    }
+    CK(cudaGetLastError());
+    ++g_launches;
+    return true;
+}
+
 void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f, const double* xprev, double cp,
                    double alpha, double beta, double* out, cudaStream_t s) {
-    // TMA-staged path: SELL level with slices <= 8 wide, large enough to be bandwidth bound, and
-    // 16-byte aligned streams (bulk copies move 16-byte multiples)
-    if (tma_enabled() && op.sell && op.S.wmax <= 8 && op.S.nslices >= 8 * 148 * kTmaWarps && aligned16(xg) &&
-        aligned16(f) && (!xprev || aligned16(xprev))) {
-        TmaSmoothArgs a{f, xprev, out, alpha, beta, cg, cp};
-        switch (op.S.vmode * 4 + op.S.cmode) {
-            case 0: launch_smooth_tma<0, 0>(op, xg, a, s); break;
-            case 1: launch_smooth_tma<0, 1>(op, xg, a, s); break;
-            case 2: launch_smooth_tma<0, 2>(op, xg, a, s); break;
-            case 4: launch_smooth_tma<1, 0>(op, xg, a, s); break;
-            case 5: launch_smooth_tma<1, 1>(op, xg, a, s); break;
-            case 6: launch_smooth_tma<1, 2>(op, xg, a, s); break;
-            default: launch_smooth_tma<1, 3>(op, xg, a, s); break;
-        }
-        CK(cudaGetLastError());
-        ++g_launches;
+    if (launch_tma<TEpiSmooth, false>(op, xg, TEpiSmooth{f, xprev, out, alpha, beta, cg, cp}, f, xprev, nullptr,
+                                      DotOut{}, s))
         return;
-    }
     EpiSmooth e{f, xprev, out, alpha, beta, cg, cp};
     launch_op<EpiSmooth, false>(op, xg, e, nullptr, DotOut{}, s);
 }
 
 void launch_resid(const SpOp& op, const double* xg, const double* f, double* out, double* dot_rr, const DotScratch& ds,
                   cudaStream_t s) {
-    EpiResid e{f, out};
-    if (dot_rr)
-        launch_op<EpiResid, true>(op, xg, e, &ds, DotOut{{dot_rr}}, s);
-    else
-        launch_op<EpiResid, false>(op, xg, e, nullptr, DotOut{}, s);
+    if (dot_rr) {
+        if (launch_tma<TEpiResid, true>(op, xg, TEpiResid{f, out}, f, nullptr, &ds, DotOut{{dot_rr}}, s)) return;
+        launch_op<EpiResid, true>(op, xg, EpiResid{f, out}, &ds, DotOut{{dot_rr}}, s);
+    } else {
+        if (launch_tma<TEpiResid, false>(op, xg, TEpiResid{f, out}, f, nullptr, nullptr, DotOut{}, s)) return;
+        launch_op<EpiResid, false>(op, xg, EpiResid{f, out}, nullptr, DotOut{}, s);
+    }
 }
 
 void launch_spmv_dots(const SpOp& op, const double* d, const double* rho, double* q, double* dot_dq, double* dot_dr,
                       const DotScratch& ds, cudaStream_t s) {
+    if (launch_tma<TEpiSpmvDots, true>(op, d, TEpiSpmvDots{rho, q}, rho, nullptr, &ds, DotOut{{dot_dq, dot_dr}}, s))
+        return;
     EpiSpmvDots e{rho, q};
     launch_op<EpiSpmvDots, true>(op, d, e, &ds, DotOut{{dot_dq, dot_dr}}, s);
 }
