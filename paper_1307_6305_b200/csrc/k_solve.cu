@@ -970,7 +970,9 @@ static void launch_tma_v(const SpOp& op, const double* xg, const Epi& e, double*
                          cudaStream_t s) {
     static int var = -2;
     if (var == -2) var = getenv("AMG_TMA_VARIANT") ? atoi(getenv("AMG_TMA_VARIANT")) : -1;
-    const int v = var >= 0 ? var : (VM == 1 ? 1 : 0);
+    // measured: 2 slices per warp win for the narrow compressed 2D level (C3: 113.7 vs
+    // 116.0 us), one slice per warp for the 7-wide 3D level (C4: 138.6 vs 158.4 us)
+    const int v = var >= 0 ? var : ((VM == 1 && W <= 5) ? 1 : 0);
     switch (v) {
         case 1: launch_tma_w<Epi, DOTS, VM, CM, W, 2, 3>(op, xg, e, part, tk, d, s); break;
         case 2: launch_tma_w<Epi, DOTS, VM, CM, W, 1, 2>(op, xg, e, part, tk, d, s); break;
@@ -982,8 +984,17 @@ static void launch_tma_v(const SpOp& op, const double* xg, const Epi& e, double*
 template <class Epi, bool DOTS, int VM, int CM>
 static void launch_tma_fmt(const SpOp& op, const double* xg, const Epi& e, double* part, unsigned* tk, DotOut d,
                            cudaStream_t s) {
-    if (op.S.wmax <= 5) launch_tma_v<Epi, DOTS, VM, CM, 5>(op, xg, e, part, tk, d, s);
-    else launch_tma_v<Epi, DOTS, VM, CM, 8>(op, xg, e, part, tk, d, s);
+    // exact-width instances up to 8 (the straight-line path then covers every full-width slice)
+    switch (op.S.wmax) {
+        case 1: case 2: case 3: case 4: launch_tma_v<Epi, DOTS, VM, CM, 4>(op, xg, e, part, tk, d, s); break;
+        case 5: launch_tma_v<Epi, DOTS, VM, CM, 5>(op, xg, e, part, tk, d, s); break;
+        case 6: launch_tma_v<Epi, DOTS, VM, CM, 6>(op, xg, e, part, tk, d, s); break;
+        case 7: launch_tma_v<Epi, DOTS, VM, CM, 7>(op, xg, e, part, tk, d, s); break;
+        case 8: launch_tma_v<Epi, DOTS, VM, CM, 8>(op, xg, e, part, tk, d, s); break;
+        default:
+            if (op.S.wmax <= 12) launch_tma_w<Epi, DOTS, VM, CM, 12, 1, 3>(op, xg, e, part, tk, d, s);
+            else launch_tma_w<Epi, DOTS, VM, CM, 16, 1, 3>(op, xg, e, part, tk, d, s);
+    }
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -993,7 +1004,11 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 template <class Epi, bool DOTS>
 static bool launch_tma(const SpOp& op, const double* xg, const Epi& e, const double* v0, const double* v1,
                        const DotScratch* ds, DotOut d, cudaStream_t s) {
-    if (!(tma_enabled() && op.sell && op.S.wmax <= 8 && op.S.nslices >= 8 * 148 * kTmaWarps && aligned16(xg) &&
+    static int min_slices = -1;  // AMG_TMA_MIN_SLICES (experiments)
+    if (min_slices < 0) min_slices = getenv("AMG_TMA_MIN_SLICES") ? atoi(getenv("AMG_TMA_MIN_SLICES")) : 8 * 148 * kTmaWarps;
+    static int max_w = -1;  // AMG_TMA_MAX_W (experiments)
+    if (max_w < 0) max_w = getenv("AMG_TMA_MAX_W") ? atoi(getenv("AMG_TMA_MAX_W")) : 16;
+    if (!(tma_enabled() && op.sell && op.S.wmax <= max_w && op.S.nslices >= min_slices && aligned16(xg) &&
           (!v0 || aligned16(v0)) && (!v1 || aligned16(v1))))
         return false;
     double* part = ds ? ds->partials : nullptr;
