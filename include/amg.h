@@ -75,7 +75,10 @@ typedef struct {
     int64_t  gather_rows;   /* amg_setup_dist only: the first level with fewer than gather_rows rows
                                (and always the coarsest) is gathered onto every rank, which runs the
                                rest of the hierarchy redundantly; default 50000 */
-    int64_t  reserved[4];
+    int32_t  tail_smem;     /* 1 = the coarse-tail kernel keeps every vector of its levels in shared
+                               memory when they fit (200 KB); default 0 (measured no gain) */
+    int32_t  reserved32;
+    int64_t  reserved[3];
 } amg_options;
 
 typedef struct {

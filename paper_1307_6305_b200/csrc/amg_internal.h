@@ -195,17 +195,24 @@ struct TLevel {
     double beta[kMaxDeg + 1] = {};
     double *X = nullptr, *XA = nullptr, *RES = nullptr, *RHO = nullptr, *E = nullptr;
     double *Z = nullptr, *D = nullptr, *Q = nullptr;
+    // shared-memory mode: offsets (in doubles) of X, XA, RES, RHO, E, Z, D, Q inside the kernel's
+    // dynamic shared memory; -1 = the global vector above
+    int off[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
 };
 struct TailArgs {
     int l0 = 0;       // level the call starts at
     int L = 0;        // number of levels (L-1 = coarsest)
     int m = 0, nu = 0;
     int mode = 0;     // 0: out = B_l0(rin);  1: FCG_inner(l0): lev[l0].RHO -> lev[l0].E
+    int smem = 0;     // doubles of dynamic shared memory holding the tail levels' vectors (0 = global)
+    int lbase = 0;    // lev[k] describes level lbase + k
     const double* Minv = nullptr;
     const double* rin = nullptr;
     double* out = nullptr;
-    const TLevel* lev = nullptr;  // device array [L]
+    const TLevel* lev = nullptr;  // device array
 };
+constexpr int kTailMaxLev = 12;   // shared-memory mode: at most this many tail levels
+constexpr int kTailSmemBytes = 200 * 1024;  // shared-memory mode budget for the tail vectors
 constexpr int kTailMaxNu = 4;  // the tail kernel supports nu <= 4
 // cluster size actually used (16 if the device allows non-portable clusters, else 8)
 int tail_cluster_size();

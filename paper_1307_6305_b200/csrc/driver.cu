@@ -385,6 +385,39 @@ static void upload_tail_levels(amg_hierarchy* h) {
         d.X = Lv.X; d.XA = Lv.XA; d.RES = Lv.RES; d.RHO = Lv.RHO; d.E = Lv.E;
         d.Z = Lv.Z; d.D = Lv.D; d.Q = Lv.Q;
     }
+    // shared-memory mode of the tail (k_tail.cu): every vector of the tail levels in the CTA's shared
+    // memory when they fit (nu inner slots), so each phase of the recursion costs L1/shared-memory
+    // latencies instead of L2 round trips
+    h->tail_smem = 0;
+    if (h->l_tail < h->L && h->opt.tail_smem && tail_cluster_size() == 1 && h->L - h->l_tail <= kTailMaxLev &&
+        h->nu_ws >= 1) {
+        int64_t off = 0;
+        auto take = [&](int64_t len) {
+            const int64_t o = off;
+            off += (len + 1) & ~int64_t(1);  // 16-byte aligned slots
+            return (int)o;
+        };
+        for (int k = h->l_tail; k < h->L; ++k) {
+            TLevel& d = t[k];
+            const int64_t n = d.n;
+            if (k < h->L - 1) {
+                d.off[0] = take(n);
+                d.off[1] = take(n);
+                d.off[2] = take(n);
+                d.off[5] = take(n);
+                d.off[6] = take(n * h->nu_ws);
+                d.off[7] = take(n * h->nu_ws);
+            }
+            d.off[3] = take(n);
+            d.off[4] = take(n);
+        }
+        if (off * (int64_t)sizeof(double) <= kTailSmemBytes) {
+            h->tail_smem = (int)off;
+        } else {
+            for (int k = h->l_tail; k < h->L; ++k)
+                for (int j = 0; j < 8; ++j) t[k].off[j] = -1;
+        }
+    }
     CK(cudaMemcpyAsync(h->d_tlev, t.data(), sizeof(TLevel) * t.size(), cudaMemcpyHostToDevice, h->s));
     CK(cudaStreamSynchronize(h->s));
 }
@@ -417,6 +450,8 @@ static void tail_call(amg_hierarchy* h, int mode, int l, int nu, const double* r
     a.rin = rin;
     a.out = out;
     a.lev = h->d_tlev;
+    a.smem = h->tail_smem;
+    a.lbase = 0;
     launch_tail(a, h->s);
 }
 
@@ -742,6 +777,7 @@ int amg_options_default(amg_options* o) {
     o->stream = nullptr;
     o->use_graphs = 1;
     o->tail_nnz = 8192;
+    o->tail_smem = 0;  // measured no gain on C1-C5: opt-in
     o->compress = 1;
     o->gather_rows = 50000;
     return AMG_OK;

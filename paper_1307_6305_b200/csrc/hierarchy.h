@@ -79,6 +79,7 @@ struct amg_hierarchy {
     amg::DotScratch ds;
     int nu_ws = 0;          // nu the inner workspaces are sized for
     int l_tail = 0;         // first level run by the coarse-tail kernel (L = none)
+    int tail_smem = 0;      // doubles of shared memory the tail kernel keeps its vectors in (0 = global)
     amg::TLevel* d_tlev = nullptr;
     std::vector<cudaGraphExec_t> graphs;
     int graph_nu = 0;

@@ -111,10 +111,10 @@ __device__ __noinline__ void t_fcg(const TailArgs& A, int l, TCtx c);
 template <bool CL>
 __device__ __noinline__ void t_B(const TailArgs& A, int l, const double* r, double* out, TCtx c) {
     if (l == A.L - 1) {
-        t_gemv<CL>(A.lev[l].n, A.Minv, r, out, c);
+        t_gemv<CL>(A.lev[l - A.lbase].n, A.Minv, r, out, c);
         return;
     }
-    const TLevel& L = A.lev[l];
+    const TLevel& L = A.lev[l - A.lbase];
     const int m = A.m;
     double* cur = L.X;
     double* prev = L.XA;
@@ -138,7 +138,7 @@ __device__ __noinline__ void t_B(const TailArgs& A, int l, const double* r, doub
     }
     csync<CL>();
     // restriction
-    const TLevel& C = A.lev[l + 1];
+    const TLevel& C = A.lev[l + 1 - A.lbase];
     for (int I = c.t; I < L.nc; I += c.T) {
         double s = 0.0;
         for (int t = L.aptr[I]; t < L.aptr[I + 1]; ++t) s += L.RES[L.perm[t]];
@@ -168,7 +168,7 @@ __device__ __noinline__ void t_B(const TailArgs& A, int l, const double* r, doub
 // FCG_inner(l): RHO_l -> E_l with nu iterations
 template <bool CL>
 __device__ __noinline__ void t_fcg(const TailArgs& A, int l, TCtx c) {
-    const TLevel& L = A.lev[l];
+    const TLevel& L = A.lev[l - A.lbase];
     const int n = L.n, nu = A.nu;
     double dq[kTailMaxNu];
     for (int i = 0; i < nu; ++i) {
@@ -213,6 +213,8 @@ __device__ __noinline__ void t_fcg(const TailArgs& A, int l, TCtx c) {
 
 template <bool CL>
 __global__ void __launch_bounds__(kTailBlock, 1) k_tail(TailArgs a) {
+    extern __shared__ __align__(16) double tsv[];
+    __shared__ TLevel slev[CL ? 1 : kTailMaxLev];
     pdl_trigger();
     pdl_wait();
     TCtx c;
@@ -221,6 +223,35 @@ __global__ void __launch_bounds__(kTailBlock, 1) k_tail(TailArgs a) {
         c = TCtx{(int)(cl.block_rank() * blockDim.x + threadIdx.x), (int)(cl.num_blocks() * blockDim.x)};
     } else {
         c = TCtx{(int)threadIdx.x, (int)blockDim.x};
+    }
+    if constexpr (!CL) {
+        if (a.smem) {
+            // shared-memory mode: every vector of the tail levels lives in this CTA's shared memory
+            // for the whole call (the matrices are read-only and stay in L1/L2); only the call's
+            // input (rin, or RHO_l0) and output (out, or E_l0) are global
+            const int nl = a.L - a.l0;
+            for (int k = threadIdx.x; k < nl; k += blockDim.x) {
+                TLevel t = a.lev[a.l0 - a.lbase + k];
+                double** ptr[8] = {&t.X, &t.XA, &t.RES, &t.RHO, &t.E, &t.Z, &t.D, &t.Q};
+                for (int j = 0; j < 8; ++j)
+                    if (t.off[j] >= 0) *ptr[j] = tsv + t.off[j];
+                slev[k] = t;
+            }
+            __syncthreads();
+            const TLevel& g0 = a.lev[a.l0 - a.lbase];
+            if (a.mode == 1)
+                for (int i = threadIdx.x; i < g0.n; i += blockDim.x) slev[0].RHO[i] = g0.RHO[i];
+            a.lev = slev;
+            a.lbase = a.l0;
+            __syncthreads();
+            if (a.mode == 0) {
+                t_B<CL>(a, a.l0, a.rin, a.out, c);
+            } else {
+                t_fcg<CL>(a, a.l0, c);
+                for (int i = threadIdx.x; i < g0.n; i += blockDim.x) g0.E[i] = slev[0].E[i];
+            }
+            return;
+        }
     }
     if (a.mode == 0)
         t_B<CL>(a, a.l0, a.rin, a.out, c);
@@ -266,7 +297,13 @@ int tail_cluster_size() {
 void launch_tail(const TailArgs& a, cudaStream_t s) {
     const int cs = tail_cluster_size();
     if (cs == 1) {
-        launch_k(k_tail<false>, dim3(1), dim3(kTailBlock), 0, s, a);
+        static int cfg_bytes = 0;
+        const int bytes = a.smem * (int)sizeof(double);
+        if (bytes > cfg_bytes) {
+            CK(cudaFuncSetAttribute(k_tail<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            cfg_bytes = bytes;
+        }
+        launch_k(k_tail<false>, dim3(1), dim3(kTailBlock), (size_t)bytes, s, a);
         CK(cudaGetLastError());
         ++g_launches;
         return;

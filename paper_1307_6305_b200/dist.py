@@ -1,8 +1,7 @@
 """Row-partition helpers of the multi-GPU path (argument marshalling only).
 
-* ``row_blocks(n, P)``   -- block offsets floor(b n / P), the partition the oracle's decoupled
-                            aggregation uses (reading A20 / SURVEY 8(c) O1), so parity runs compare
-                            like with like.
+* ``row_blocks(n, P)``   -- block offsets floor(b n / P), the partition of reading A20 (SURVEY
+                            8(c) O1), so parity runs compare like with like.
 * ``local_block(...)``   -- this rank's rows of a global CSR, columns kept GLOBAL (the input of
                             amg_setup_dist).
 * ``nccl_comm(...)``     -- the library's NCCL communicator for a torch.distributed job: rank 0 asks

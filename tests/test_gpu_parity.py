@@ -334,3 +334,25 @@ def test_smoother_tma_path_parity(amg, gen_mod, oracle_mod):
         assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("tail_nnz", [8192, 10 ** 6])
+def test_tail_shared_memory_mode_parity(amg, gen_mod, oracle_mod, tail_nnz):
+    """The coarse-tail kernel with its vectors in shared memory (opt-in tail_smem) gives the same
+    B_0(r) as the oracle and the same iterations; tail_nnz 1e6 puts every level >= 1 of C1 in the tail."""
+    p = gen_mod.problem("C1")
+    hier = oracle_mod.setup_problem(p)
+    o = amg.amg_options_default(coarsest_size=100, tail_nnz=tail_nnz, tail_smem=1)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 2, 2, o)
+    try:
+        r = np.random.default_rng(5).uniform(-1, 1, p.n)
+        z = np.empty(p.n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        ref = hier.precond(r, nu=2, level=0)
+        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        b = gen_mod.rhs(p.n, 0)
+        x = np.zeros(p.n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        assert st == 0 and abs(it - hier.solve(b, tol=1e-8, nu=2)["iters"]) <= 1
+    finally:
+        amg.amg_free(h)
