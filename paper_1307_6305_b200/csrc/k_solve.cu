@@ -661,6 +661,73 @@ struct TEpiSpmvDots {  // q = A d; acc = (d.q, d.rho)
     }
 };
 
+// One slice of exact width K (straight-line): decode the K codes of this lane's row from the stage,
+// issue the K gathers, run the fma chain in entry order, apply the epilogue (variable-width levels).
+template <class Epi, int VM, int CM, int K, int ESA, int ESB, int LA, int LB, int LV, int ROWS>
+__device__ __forceinline__ void tma_slice(const Epi& epi, uint32_t sb, int q, uint32_t off, int i, int lane, int n,
+                                          int chi, uint32_t sv_a, uint32_t sc_a, const double* __restrict__ xg,
+                                          bool v0, bool v1, double* acc) {
+    constexpr int HDR = 0;
+    const uint32_t A = sb + LA + off * 32 * ESA + lane * ESA;
+    const uint32_t Bc = sb + LB + off * 32 * ESB + lane * ESB;
+    int craw[K], col[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+        int cr;
+        if constexpr (CM == 3) {
+            craw[u] = lds_u16(A + u * 64);
+            cr = craw[u] >> 8;
+        } else {
+            if constexpr (VM == 1) craw[u] = lds_u8(A + u * 32);
+            if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
+            else if constexpr (CM == 1) cr = lds_u8(Bc + u * 32);
+            else cr = lds_s16(Bc + u * 64);
+        }
+        int cc;
+        if constexpr (CM == 0) cc = cr;
+        else {
+            cc = i + ((CM == 1 || CM == 3) ? lds_s32(sc_a + 4 * cr) : cr);
+            cc = cc < chi ? cc : chi;
+        }
+        col[u] = cc;
+    }
+    double x[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) x[u] = ld_gather(xg + col[u]);
+    double sum = 0.0;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+        double v;
+        if constexpr (VM == 0) v = lds_f64(A + u * 256);
+        else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[u] & 0xff) : craw[u]));
+        sum = fma(v, x[u], sum);
+    }
+    (void)HDR;
+    if (i < n) {
+        const uint32_t r8 = 8 * (q * 32 + lane);
+        const uint32_t vt = sb + LV;
+        const double xi = lds_f64(vt + r8);
+        const double a0 = v0 ? lds_f64(vt + 8 * ROWS + r8) : 0.0;
+        const double a1 = v1 ? lds_f64(vt + 16 * ROWS + r8) : 0.0;
+        epi.store(i, sum, xi, a0, a1, acc);
+    }
+}
+
+template <class Epi, int VM, int CM, int W, class Lay, int K = W>
+__device__ __forceinline__ void tma_slice_dispatch(int w, const Epi& epi, uint32_t sb, int q, uint32_t off, int i,
+                                                   int lane, int n, int chi, uint32_t sv_a, uint32_t sc_a,
+                                                   const double* __restrict__ xg, bool v0, bool v1, double* acc) {
+    if constexpr (K >= 1) {
+        if (w == K)
+            tma_slice<Epi, VM, CM, K, TmaStreams<VM, CM>::ESA, TmaStreams<VM, CM>::ESB, Lay::HDR, Lay::HDR + Lay::A,
+                      Lay::HDR + Lay::A + Lay::B, Lay::ROWS>(epi, sb, q, off, i, lane, n, chi, sv_a, sc_a, xg, v0, v1,
+                                                             acc);
+        else
+            tma_slice_dispatch<Epi, VM, CM, W, Lay, K - 1>(w, epi, sb, q, off, i, lane, n, chi, sv_a, sc_a, xg, v0,
+                                                          v1, acc);
+    }
+}
+
 template <class Epi, bool DOTS, int VM, int CM, int W, int SPW, int NS>
 __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const double* __restrict__ xg, Epi epi,
                                                                    double* partials, unsigned* ticket,
@@ -750,6 +817,15 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
             const uint32_t sb = tsm_a + st * Lay::STAGE;
             const int c = blockIdx.x + k * gridDim.x;
             const int h0 = lds_s32(sb);
+            if constexpr (W > 8 && SPW == 1) {  // variable slice widths: exact-width straight-line bodies
+                const int s = c * CS + warp;
+                if (s < S.nslices) {
+                    const int hq = lds_s32(sb + 4 * warp), wq = lds_s32(sb + 4 * (warp + 1)) - hq;
+                    tma_slice_dispatch<Epi, VM, CM, W, Lay>(wq, epi, sb, warp, (uint32_t)(hq - h0), s * 32 + lane,
+                                                            lane, S.n, S.chi, sv_a, sc_a, xgr, v0g != nullptr,
+                                                            v1g != nullptr, acc);
+                }
+            } else {
             // this warp's SPW slices of the chunk: codes -> columns, then every gather, then the fma chains
             int craw[SPW][W], w[SPW], col[SPW][W];
             uint32_t aoff[SPW];
@@ -828,6 +904,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
                     epi.store(i, sum, xi, a0, a1, acc);
                 }
             }
+            }  // fixed-width path
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
         }
