@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nc, const int* _
                                                             const int* __restrict__ perm, const int* __restrict__ aptr,
                                                             const int* __restrict__ eoff, bool drop,
                                                             int* __restrict__ tcol, VAL* __restrict__ tval,
-                                                            int* __restrict__ ucount) {
+                                                            int* __restrict__ ucount, int emin) {
     __shared__ unsigned long long skey[kRMWarps][kRM];
     __shared__ VAL sval[kRMWarps][kRM];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nc, const int* _
     const int nwarp = gridDim.x * kRMWarps;
     for (int I = blockIdx.x * kRMWarps + wib; I < nc; I += nwarp) {
         const int e0 = eoff[I], E = eoff[I + 1] - e0;
-        if (E > kRM) continue;  // wide rows: k_rm_merge_block
+        if (E > kRM || E <= emin) continue;  // wide rows: k_rm_merge_block; rows <= emin: k_rm_small
         // gather in (member, position) order, k = running rank; members are spread over the lanes
         // (one member per lane, a warp prefix sum of their row lengths gives each its first k)
         const int t0 = aptr[I], t1 = aptr[I + 1];
@@ -759,6 +759,88 @@ __global__ void k_rm_compact(int nc, const int* __restrict__ eoff, const int* __
     }
 }
 
+// Coarse rows with E <= G entries, G lanes per row (32 / G rows per warp), no sort: lane t holds
+// entry k = t of the (member, CSR position) order; an entry is a run head if no earlier entry has the
+// same J; the head sums its run in increasing k (the sequential order: bit-exact); its output slot
+// is the number of heads with a smaller J (columns come out sorted).  Rows with E > G are skipped.
+template <class VAL, int G>
+__global__ void __launch_bounds__(256) k_rm_small(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                  const VAL* __restrict__ src, const int* __restrict__ agg,
+                                                  const int* __restrict__ perm, const int* __restrict__ aptr,
+                                                  const int* __restrict__ eoff, bool drop, int* __restrict__ tcol,
+                                                  VAL* __restrict__ tval, int* __restrict__ ucount, int emin) {
+    constexpr int GPW = 32 / G;  // rows per warp
+    const int lane = threadIdx.x & 31;
+    const int t = lane & (G - 1);
+    const unsigned NONE = 0xFFFFFFFFu;
+    const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int wstride = ((gridDim.x * blockDim.x) >> 5) * GPW;
+    // the warp's rows share one trip count (full-mask shuffles below)
+    for (int wb = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW; wb < nc; wb += wstride) {
+        const int I = wb + lane / G;
+        const bool rowok = I < nc;
+        const int e0 = rowok ? eoff[I] : 0;
+        const int E = rowok ? eoff[I + 1] - e0 : 0;
+        const bool mine = rowok && E > emin && E <= G;
+        // members of the aggregate: lane t < M holds member t's first position and row length
+        const int t0 = mine ? aptr[I] : 0;
+        const int M = mine ? aptr[I + 1] - t0 : 0;
+        int p0 = 0, len = 0;
+        if (t < M) {
+            const int v = perm[t0 + t];
+            p0 = rp[v];
+            len = rp[v + 1] - p0;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o, G);
+            if (t >= o) incl += y;
+        }
+        const int kb = incl - len;
+        // entry k = t: its member and CSR position
+        int pos = -1;
+#pragma unroll
+        for (int m = 0; m < G; ++m) {
+            const int kbm = __shfl_sync(0xffffffffu, kb, m, G);
+            const int lnm = __shfl_sync(0xffffffffu, len, m, G);
+            const int pm = __shfl_sync(0xffffffffu, p0, m, G);
+            if (m < M && t >= kbm && t < kbm + lnm) pos = pm + (t - kbm);
+        }
+        unsigned J = NONE;
+        VAL val = VAL(0);
+        if (mine && pos >= 0) {
+            const unsigned j = (unsigned)agg[ci[pos]];
+            val = src[pos];
+            J = (drop && j == (unsigned)I) ? NONE : j;
+        }
+        // run head = first entry (in k order) of its J; the head sums its run in increasing k
+        bool head = J != NONE;
+        VAL acc = val;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const unsigned Jr = __shfl_sync(0xffffffffu, J, r, G);
+            const VAL vr = __shfl_sync(0xffffffffu, val, r, G);
+            if (Jr == J && r < t) head = false;
+            if (Jr == J && r > t) acc += vr;
+        }
+        // output slot = number of heads with a smaller J (columns sorted)
+        int rank = 0;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            const unsigned Jr = __shfl_sync(0xffffffffu, J, r, G);
+            const int hr = __shfl_sync(0xffffffffu, (int)head, r, G);
+            if (hr && Jr < J) ++rank;
+        }
+        const unsigned hb = __ballot_sync(0xffffffffu, head && mine);
+        if (head && mine) {
+            tcol[e0 + rank] = (int)J;
+            tval[e0 + rank] = acc;
+        }
+        if (mine && t == 0) ucount[I] = __popc(hb & gm);
+    }
+}
+
 // returns false (nothing allocated) if some coarse row has more than kRM entries
 template <class VAL>
 static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg, int nc,
@@ -785,8 +867,30 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
     VAL* tval = dalloc<VAL>((size_t)tot + 8, s);
     int* uc = E;  // reuse: unique counts
     CK(cudaMemsetAsync(uc + nc, 0, sizeof(int), s));
+    // rows of <= 8 / <= 32 entries: sort-free shuffle merges (4 rows per warp / 1 row per warp);
+    // larger rows: the warp bitonic merge (and the CTA merge above kRM entries)
+    static int small_on = -1;
+    if (small_on < 0) small_on = getenv("AMG_RM_NO_SMALL") ? 0 : 1;
+    int emin = 0;
+    if (small_on) {
+        const int gb = (int)std::min<int64_t>((nc + 31) / 32, 148LL * 32);
+        k_rm_small<VAL, 8><<<gb, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, 0);
+        ++g_launches;
+        emin = 8;
+        static int g16 = -1;
+        if (g16 < 0) g16 = getenv("AMG_RM_16") ? 1 : 0;  // measured a wash on C3: opt-in
+        if (mx > 8 && g16) {
+            const int gw = (int)std::min<int64_t>((nc + 15) / 16, 148LL * 32);
+            k_rm_small<VAL, 16><<<gw, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, 8);
+            ++g_launches;
+            emin = 16;
+        }
+        CK(cudaGetLastError());
+    }
     const int nb = (int)std::min<int64_t>((nc + kRMWarps - 1) / kRMWarps, 148LL * 16);
-    k_rm_merge<VAL><<<nb, 32 * kRMWarps, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
+    if (mx > emin)
+        k_rm_merge<VAL><<<nb, 32 * kRMWarps, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc,
+                                                     emin);
     ++g_launches;
     CK(cudaGetLastError());
     if (mx > kRM) {  // list the wide rows, one CTA each
