@@ -377,6 +377,7 @@ typedef struct {
     int64_t coarsest_size;
     double kappa_opt;
     int restart, max_iter, rule, cycle, nparts;
+    double amli_kappa; /* cycle 2: 1/theta of the AMLI polynomial interval; 0 = reading A23 */
     int64_t gather_rows;
     uint64_t seed;
     olevel lev[ORC_MAXLEV];
@@ -621,6 +622,38 @@ static void ofcg_inner(const orc_h *h, int l, int nu, const double *b, double *e
  * readings A10-A12):  x = S_l(r, 0); rho_H = P^T(r - A x);
  * e = A_L^{-1/dagger} rho_H if l+1 is the coarsest, else FCG_inner(l+1, rho_H, nu)
  * (cycle=1: B_{l+1}(rho_H), the linear test-only V-cycle); x += P e; x = S_l(r, x). */
+/* Stationary AMLI coarse correction (cycle 2; "we use the polynomial based on the best
+ * approximation to x^{-1} in the uniform norm to form the preconditioner between any two successive
+ * levels"; reading A23):  e = q(B_l A_l) B_l rho, q = the degree-(nu-1) best uniform
+ * approximation to 1/t on [1/kappa_A, 1] (the smoother's family, on the preconditioned
+ * operator), evaluated by the smoother's three-term recurrence applied to B_l A_l y = B_l rho:
+ *   y_0 = 0,  y_{k+1} = alpha_k y_k + (1 - alpha_k) y_{k-1} + beta_k B_l(rho - A_l y_k),  k = 0..nu-1,
+ * i.e. nu applications of B_l and nu-1 SpMVs; kappa_A = rule R1 (A8) for degree nu-1 unless set.
+ * nu = 1: e = B_l rho (no polynomial: the V-cycle). */
+static void oamli(const orc_h *h, int l, int nu, const double *rho, double *e) {
+    const ocsr *A = &h->lev[l].A;
+    int64_t n = A->n;
+    if (nu == 1) { oB(h, l, nu, rho, e); return; }
+    int m = nu - 1;
+    double kap = h->amli_kappa > 1.0 ? h->amli_kappa : orc_kappa_rule(m);
+    double alpha[ORC_MAXDEG + 1], beta[ORC_MAXDEG + 1];
+    orc_poly_coeffs(1.0, kap, m, alpha, beta);
+    double *ym1 = calloc((size_t)n, sizeof(double)), *yk = calloc((size_t)n, sizeof(double));
+    double *t = malloc(sizeof(double) * n), *z = malloc(sizeof(double) * n);
+    for (int k = 0; k <= m; ++k) {
+        ospmv(A, yk, t);
+        for (int64_t i = 0; i < n; ++i) t[i] = rho[i] - t[i];
+        oB(h, l, nu, t, z);
+        for (int64_t i = 0; i < n; ++i) {
+            double yn = alpha[k] * yk[i] + (1.0 - alpha[k]) * ym1[i] + beta[k] * z[i];
+            ym1[i] = yk[i];
+            yk[i] = yn;
+        }
+    }
+    memcpy(e, yk, sizeof(double) * n);
+    free(ym1); free(yk); free(t); free(z);
+}
+
 static void oB(const orc_h *h, int l, int nu, const double *r, double *x) {
     if (l == h->nlev - 1) { ocoarse_solve(h, r, x); return; }
     const olevel *L = &h->lev[l];
@@ -632,6 +665,7 @@ static void oB(const orc_h *h, int l, int nu, const double *r, double *x) {
     for (int64_t i = 0; i < n; ++i) rH[L->agg[i]] += r[i] - t[i]; /* P^T, i increasing */
     if (l + 1 == h->nlev - 1) ocoarse_solve(h, rH, eH);
     else if (h->cycle == 1) oB(h, l + 1, nu, rH, eH);
+    else if (h->cycle == 2) oamli(h, l + 1, nu, rH, eH);
     else ofcg_inner(h, l + 1, nu, rH, eH);
     for (int64_t i = 0; i < n; ++i) x[i] += eH[L->agg[i]];
     osmooth(&L->A, h->m, L->alpha, L->beta, r, x, x);
@@ -704,6 +738,8 @@ int orc_solve(const orc_h *h, const double *b_in, double *x, double tol, int nu,
 
 /* ================================================= exported accessors / pieces */
 int orc_num_levels(const orc_h *h) { return h->nlev; }
+/* cycle 2 (stationary AMLI): 1/theta of the coarse polynomial interval (0 = reading A23) */
+void orc_set_amli_kappa(orc_h *h, double kappa) { h->amli_kappa = kappa; }
 int orc_is_singular(const orc_h *h) { return h->singular; }
 
 void orc_level_info(const orc_h *h, int l, int64_t *n, int64_t *nnz, double *lambda1, double *kappa, int64_t *nc,

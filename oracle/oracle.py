@@ -44,6 +44,7 @@ def _L():
         "orc_free": (None, [vp]),
         "orc_solve": (i32, [vp, vp, vp, dbl, i32, vp, vp, vp]),
         "orc_num_levels": (i32, [vp]),
+        "orc_set_amli_kappa": (None, [vp, dbl]),
         "orc_is_singular": (i32, [vp]),
         "orc_level_info": (None, [vp, i32, vp, vp, vp, vp, vp, vp]),
         "orc_level_csr": (None, [vp, i32, vp, vp, vp]),
@@ -162,7 +163,7 @@ class Hierarchy:
     """Oracle setup + solve (O5-O8)."""
 
     def __init__(self, rp, ci, val, d, passes, degree, coarsest_size=100, kappa=0.0, restart=5,
-                 max_iter=500, seed=0, nparts=1, gather_rows=0, rule=0, cycle=0):
+                 max_iter=500, seed=0, nparts=1, gather_rows=0, rule=0, cycle=0, amli_kappa=0.0):
         self._keep = [_c(rp, np.int64), _c(ci, np.int32), _c(val, np.float64), _c(d, np.float64)]
         rp, ci, val, d = self._keep
         self.m = degree
@@ -174,6 +175,8 @@ class Hierarchy:
         if st != 0:
             raise OracleError(st)
         self.h = h
+        if amli_kappa:
+            _L().orc_set_amli_kappa(h, amli_kappa)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -252,5 +255,5 @@ def setup_problem(prob, **over) -> Hierarchy:
     p = dict(prob.params)
     p.update(over)
     kw = {k: p[k] for k in ("coarsest_size", "kappa", "restart", "max_iter", "seed", "nparts", "gather_rows",
-                            "rule", "cycle") if k in p}
+                            "rule", "cycle", "amli_kappa") if k in p}
     return Hierarchy(prob.rp, prob.ci, prob.val, prob.d, p["passes"], p["degree"], **kw)

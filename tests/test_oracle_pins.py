@@ -561,3 +561,61 @@ def test_decoupled_aggregation(oracle_mod, gen_mod):
     h1 = oracle_mod.setup_problem(gen_mod.problem("C1", size=40), nparts=1)
     h1b = oracle_mod.setup_problem(gen_mod.problem("C1", size=40))
     assert np.array_equal(h1.level_agg(0), h1b.level_agg(0))
+
+
+def _poly_of_matrix(M, q, m, l0, l1):
+    """q(M) for the degree-m polynomial q (exact monomial fit on m+1 Chebyshev points of [l0, l1])."""
+    t = 0.5 * (l0 + l1) + 0.5 * (l1 - l0) * np.cos(np.pi * (np.arange(m + 1) + 0.5) / (m + 1))
+    c = np.linalg.solve(np.vander(t, m + 1, increasing=True), q(t))
+    out = c[m] * np.eye(M.shape[0])
+    for k in range(m - 1, -1, -1):  # Horner
+        out = out @ M + c[k] * np.eye(M.shape[0])
+    return out
+
+
+@pytest.mark.parametrize("nu", [2, 3])
+def test_amli_cycle_pins(oracle_mod, gen_mod, nu):
+    """Stationary AMLI cycle (cycle=2, reading A23): a fixed LINEAR symmetric operator
+    (S:406-408); equals the dense recursion B_l = Rbar + (I-RA) P M_{l+1} P^T (I-AR) with
+    M_{l+1} = q(B_{l+1} A_{l+1}) B_{l+1} (q = degree-(nu-1) best approximation to 1/t on [1/kappa_A, 1],
+    evaluated here as an explicit matrix polynomial), M = A_L^{-1} on the coarsest; SPD."""
+    p = gen_mod.grid2d(18)
+    h = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=10, cycle=2)
+    assert h.nlev >= 4
+    rng = np.random.default_rng(nu)
+    r, s = rng.standard_normal(p.n), rng.standard_normal(p.n)
+    z = h.precond(r, nu=nu)
+    assert np.allclose(h.precond(3.5 * r, nu=nu), 3.5 * z, rtol=1e-13, atol=1e-13)
+    assert (z @ s) == pytest.approx(r @ h.precond(s, nu=nu), rel=1e-10)
+    mats = []
+    for l in range(h.nlev):
+        rp, ci, v = h.level_csr(l)
+        mats.append(H.dense(rp, ci, v))
+    kapA = oracle_mod.kappa_rule(nu - 1)
+    q = H.q_closed_form(1.0 / kapA, 1.0, nu - 1)
+    M = np.linalg.inv(mats[-1])  # coarse operator seen by level L-2: exact solve (A12)
+    for l in range(h.nlev - 2, -1, -1):
+        A = mats[l]
+        l1 = h.level_info(l)["lambda1"]
+        kap = h.level_info(l)["kappa"]
+        R = H.matfun_sym(A, H.q_closed_form(l1 / kap, l1, 3))
+        P = H.P_dense(h.level_agg(l), h.level_info(l)["nc"])
+        B = H.two_level_B(A, P, R, M)
+        if l >= 1:
+            M = _poly_of_matrix(B @ A, q, nu - 1, 1.0 / kapA, 1.0) @ B
+    assert np.linalg.norm(z - B @ r) <= 1e-10 * np.linalg.norm(B @ r)
+    ev = np.linalg.eigvals(B @ mats[0]).real
+    assert ev.min() > 0
+    # nu = 1: the AMLI cycle is the V-cycle (one B application per coarse level)
+    hv = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=10, cycle=1)
+    assert np.array_equal(h.precond(r, nu=1), hv.precond(r, nu=1))
+
+
+def test_amli_solve_converges(oracle_mod, gen_mod):
+    """CG (the outer FCG with a linear preconditioner) with the AMLI cycle solves C1."""
+    p = gen_mod.problem("C1")
+    h = oracle_mod.setup_problem(p, cycle=2)
+    b = gen_mod.rhs(p.n, 0)
+    res = h.solve(b, tol=1e-8, nu=2)
+    assert res["status"] == 0 and res["true_relres"] <= 2e-8
+    assert res["iters"] <= 40
