@@ -77,8 +77,13 @@ typedef struct {
                                rest of the hierarchy redundantly; default 50000 */
     int32_t  tail_smem;     /* 1 = the coarse-tail kernel keeps every vector of its levels in shared
                                memory when they fit (200 KB); default 0 (measured no gain) */
-    int32_t  reserved32;
-    int64_t  reserved[3];
+    int32_t  cycle;         /* coarse-level correction: 0 = N-AMLI / k-cycle, nu inner
+                               FCG iterations (the paper's NPCG column; default); 2 = stationary AMLI:
+                               e = q(B A) B rho with q the degree-(nu-1) best uniform approximation to
+                               1/t on [1/amli_kappa, 1] (reading A23), a linear SPD preconditioner */
+    double   amli_kappa;    /* cycle 2: 1/theta of the AMLI polynomial interval; 0 => rule R1 (A8) for
+                               degree nu-1 (4 for nu = 2); default 0 */
+    int64_t  reserved[2];
 } amg_options;
 
 typedef struct {

@@ -175,6 +175,9 @@ void launch_fcg_update(int n, const double* dr, const double* dq, const double* 
 void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cudaStream_t s);
 // v -= (*sum) / ntot  (the second half of a mean projection whose sum was allreduced)
 void launch_sub_mean(int n, double ntot, double* v, const double* sum, cudaStream_t s);
+// out = a x + b y + c z  (y, z nullable; out may alias any input: elementwise)
+void launch_lincomb3(int n, double a, const double* x, double b, const double* y, double c, const double* z,
+                     double* out, cudaStream_t s);
 // y = x (device copy kernel)
 void launch_copy(int n, const double* x, double* y, cudaStream_t s);
 // dot = x.y (deterministic)

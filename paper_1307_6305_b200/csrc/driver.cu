@@ -437,7 +437,10 @@ static int64_t smoother_bytes(const Level& Lv) {
     return per * nnz + 32 * n;
 }
 
-static bool use_tail(const amg_hierarchy* h, int l, int nu) { return l >= h->l_tail && nu <= kTailMaxNu; }
+// the coarse-tail kernel implements the k-cycle only
+static bool use_tail(const amg_hierarchy* h, int l, int nu) {
+    return l >= h->l_tail && nu <= kTailMaxNu && h->opt.cycle == 0;
+}
 
 static void tail_call(amg_hierarchy* h, int mode, int l, int nu, const double* rin, double* out) {
     TailArgs a;
@@ -515,6 +518,38 @@ static void fcg_inner(amg_hierarchy* h, int l, int nu) {
     }
 }
 
+// Stationary AMLI coarse correction at level l (cycle 2; reading A23):
+// E_l = q(B_l A_l) B_l RHO_l, q the degree-(nu-1) best uniform approximation to 1/t on [1/kappa_A, 1]
+// by the smoother's three-term recurrence on the preconditioned operator:
+//   y_0 = 0, y_{k+1} = a_k y_k + (1 - a_k) y_{k-1} + b_k B_l(RHO - A_l y_k), k = 0..nu-1.
+// nu applications of B_l, nu-1 residual passes; nu = 1: E = B_l RHO.
+static void amli_correction(amg_hierarchy* h, int l, int nu) {
+    Level& Lv = h->lev[l];
+    cudaStream_t s = h->s;
+    if (nu == 1) {
+        apply_B(h, l, nu, Lv.RHO, Lv.E);
+        return;
+    }
+    const int m = nu - 1, n = Lv.A.n;
+    const double kap = h->opt.amli_kappa > 1.0 ? h->opt.amli_kappa : kappa_rule(m);
+    double a[kMaxDeg + 1], b[kMaxDeg + 1];
+    poly_coeffs(1.0, kap, m, a, b);
+    double* T = Lv.Q;   // residual RHO - A y_k (vector layout of the level: its halo is exchanged by B)
+    double* cur = Lv.E;
+    double* prev = Lv.D;
+    apply_B(h, l, nu, Lv.RHO, Lv.Z);
+    launch_lincomb3(n, b[0], Lv.Z, 0.0, nullptr, 0.0, nullptr, cur, s);  // y_1 = b_0 B rho
+    for (int k = 1; k <= m; ++k) {
+        halo_exchange(h, l, cur);
+        launch_resid(Lv.op, cur, Lv.RHO, T, nullptr, h->ds, s);
+        apply_B(h, l, nu, T, Lv.Z);
+        // y_{k+1} = a_k y_k + (1 - a_k) y_{k-1} + b_k z  (y_0 = 0) into the y_{k-1} buffer
+        launch_lincomb3(n, a[k], cur, 1.0 - a[k], k >= 2 ? prev : nullptr, b[k], Lv.Z, prev, s);
+        std::swap(cur, prev);
+    }
+    if (cur != Lv.E) launch_copy(n, cur, Lv.E, s);
+}
+
 // z = B_l(r): pre-smoothing from 0, residual, restriction, coarse correction,
 // prolongation, post-smoothing; the last smoothing step writes `out` (distinct from rin and the
 // level buffers).  `rin` must be a vector of level l's layout (it is the first step's SpMV input).
@@ -561,6 +596,8 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     // coarse correction (A12: exact solve when the next level is the coarsest)
     if (l + 1 == h->L - 1)
         launch_gemv(C.A.n, h->Minv, C.RHO, C.E, s);
+    else if (h->opt.cycle == 2)
+        amli_correction(h, l + 1, nu);
     else
         fcg_inner(h, l + 1, nu);
     launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
@@ -801,6 +838,8 @@ static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t 
     if (opt) o = *opt;
     if (o.coarsest_size < 1 || o.restart < 1 || o.restart > kMaxWin || o.max_iter < 0 || o.gather_rows < 0)
         return fail(AMG_E_ARG, "amg_setup: bad options");
+    if (o.cycle != 0 && o.cycle != 2) return fail(AMG_E_ARG, "amg_setup: cycle must be 0 (k-cycle) or 2 (AMLI)");
+    if (o.amli_kappa != 0.0 && !(o.amli_kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: amli_kappa must be 0 or > 1");
     if (comm && !comm->c) return fail(AMG_E_ARG, "amg_setup_dist: invalid communicator");
     if (o.kappa != 0.0 && !(o.kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: kappa must be 0 or > 1");
     if (o.kappa > 1.0 && !(Em_of(poly_degree, o.kappa) < 1.0))

@@ -1349,6 +1349,25 @@ void launch_sub_mean(int n, double ntot, double* v, const double* sum, cudaStrea
     ++g_launches;
 }
 
+__global__ void __launch_bounds__(kBlock) k_lincomb3(int n, double a, const double* x, double b, const double* y,
+                                                     double c, const double* z, double* out) {
+    pdl_trigger();
+    pdl_wait();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double v = a * x[i];
+        if (y) v += b * y[i];
+        if (z) v += c * z[i];
+        out[i] = v;
+    }
+}
+
+void launch_lincomb3(int n, double a, const double* x, double b, const double* y, double c, const double* z,
+                     double* out, cudaStream_t s) {
+    launch_k(k_lincomb3, dim3(vgrid(n)), dim3(kBlock), 0, s, n, a, x, b, y, c, z, out);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
 __global__ void __launch_bounds__(kBlock) k_copy(int n, const double* __restrict__ x, double* __restrict__ y) {
     pdl_trigger();
     pdl_wait();

@@ -58,13 +58,13 @@ def run_ranks(amg, P, fn):
     return out
 
 
-def dist_case(amg, p, P, gather_rows, oracle_mod, nu=2, check_solve=True, exact_values=True):
+def dist_case(amg, p, P, gather_rows, oracle_mod, nu=2, check_solve=True, exact_values=True, cycle=0):
     from paper_1307_6305_b200 import dist
 
     prm = p.params
     m = prm["degree"]
     offs = dist.row_blocks(p.n, P)
-    hier = oracle_mod.setup_problem(p, nparts=P, gather_rows=gather_rows)
+    hier = oracle_mod.setup_problem(p, nparts=P, gather_rows=gather_rows, cycle=cycle)
     rng = np.random.default_rng(11)
     r0 = rng.uniform(-1, 1, p.n)
     from inputs import gen
@@ -75,7 +75,7 @@ def dist_case(amg, p, P, gather_rows, oracle_mod, nu=2, check_solve=True, exact_
         beg, end = offs[rank], offs[rank + 1]
         lrp, lci, lv, ld = dist.local_block(p.rp, p.ci, p.val, p.d, beg, end)
         o = amg.amg_options_default(coarsest_size=prm.get("coarsest_size", 100), seed=prm.get("seed", 0),
-                                    gather_rows=gather_rows)
+                                    gather_rows=gather_rows, cycle=cycle)
         h = amg.amg_setup_dist(comm, p.n, beg, lrp, lci, lv, ld, prm["passes"], m, o)
         try:
             info = amg.amg_get_info(h)
@@ -181,6 +181,13 @@ def test_dist_singular_rgg(amg, gen_mod, oracle_mod):
     p = gen_mod.rgg(12000, seed=7)
     p.params = dict(passes=3, degree=4, coarsest_size=60, seed=0)
     dist_case(amg, p, 2, 1000, oracle_mod)
+
+
+def test_dist_amli_cycle(amg, gen_mod, oracle_mod):
+    """The stationary AMLI cycle on the row-partitioned path (halo-exchanged residual passes of the
+    coarse polynomial)."""
+    p = gen_mod.problem("C1")
+    dist_case(amg, p, 2, 0, oracle_mod, cycle=2)
 
 
 def test_dist_fully_replicated(amg, gen_mod, oracle_mod):

@@ -356,3 +356,45 @@ def test_tail_shared_memory_mode_parity(amg, gen_mod, oracle_mod, tail_nnz):
         assert st == 0 and abs(it - hier.solve(b, tol=1e-8, nu=2)["iters"]) <= 1
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C4s", "rgg"])
+def test_amli_cycle_parity(amg, gen_mod, oracle_mod, name):
+    """Stationary AMLI cycle (cycle=2, reading A23) on the GPU against the
+    oracle: B_l(r) on every level (nu = 2, and nu = 3 on level 0) <= 1e-10, linearity, and the
+    solve's iteration count within +-1."""
+    p = {"C1": lambda: gen_mod.problem("C1"), "C2s": lambda: gen_mod.problem("C2", size=128),
+         "C4s": lambda: gen_mod.problem("C4", size=16)}.get(name, None)
+    if p is None:
+        p = gen_mod.rgg(6000, seed=5)
+        p.params = dict(passes=3, degree=3, coarsest_size=50, seed=0)
+    else:
+        p = p()
+    hier = oracle_mod.setup_problem(p, cycle=2)
+    prm = p.params
+    o = amg.amg_options_default(coarsest_size=prm.get("coarsest_size", 100), seed=prm.get("seed", 0), cycle=2)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, prm["passes"], prm["degree"], o)
+    rng = np.random.default_rng(2)
+    try:
+        for l in range(hier.nlev):
+            n = hier.level_info(l)["n"]
+            r = rng.uniform(-1, 1, n)
+            z = np.empty(n)
+            amg.amg_level_precond(h, l, 2, r, z)
+            ref = hier.precond(r, nu=2, level=l)
+            assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref), f"AMLI B_{l}(r)"
+        r = rng.uniform(-1, 1, p.n)
+        z3 = np.empty(p.n)
+        amg.amg_level_precond(h, 0, 3, r, z3)
+        ref3 = hier.precond(r, nu=3, level=0)
+        assert np.linalg.norm(z3 - ref3) <= 1e-10 * np.linalg.norm(ref3), "AMLI nu=3"
+        z4 = np.empty(p.n)
+        amg.amg_level_precond(h, 0, 3, 2.5 * r, z4)
+        assert np.linalg.norm(z4 - 2.5 * z3) <= 1e-12 * np.linalg.norm(z4)  # linear operator
+        b = gen_mod.rhs(p.n, 0)
+        x = np.zeros(p.n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        oref = hier.solve(b, tol=1e-8, nu=2)
+        assert st == 0 and rr <= 1e-8 and abs(it - oref["iters"]) <= 1, (it, oref["iters"])
+    finally:
+        amg.amg_free(h)
