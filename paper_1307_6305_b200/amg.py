@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libamg_b200.so")
+# AMG_B200_LIB overrides the in-tree library (A/B timing of another build of the same ABI)
+LIB_PATH = os.environ.get("AMG_B200_LIB") or os.path.join(_HERE, "lib", "libamg_b200.so")
 
 AMG_OK, AMG_NOT_CONVERGED = 0, 1
 AMG_E_ARG, AMG_E_INPUT, AMG_E_CUDA, AMG_E_NCCL, AMG_E_OOM, AMG_E_BREAKDOWN, AMG_E_SETUP = -1, -2, -3, -4, -5, -6, -7

@@ -53,6 +53,10 @@ struct Sell {          // SELL-32: 32-row slices, entries column-major inside a 
     int64_t padded = 0;    // 32 * sptr[nslices]
     int wmax = 0;          // maximum slice width (selects the kernel's width bucket)
     int chi = 0;           // largest valid column index (n-1; n+nhi-1 with an upper halo) -- decode clamp
+    // a VIEW of a contiguous slice range (halo overlap on a row-partitioned level runs the interior
+    // slices while the halo is in flight, then the boundary slices): sptr/nslices describe the
+    // view's slices and srow0 is the absolute first row of its first slice (0 for the whole level)
+    int srow0 = 0;
     // lossless compressed streams (same slice layout), chosen per level at setup:
     int vmode = 0;         // 0: val (fp64); 1: vcode (uint8) into vdict (<= 256 distinct values)
     int cmode = 0;         // 0: col (int32); 1: ccode (uint8) into cdict of offsets col-row; 2: coff (int16 col-row);

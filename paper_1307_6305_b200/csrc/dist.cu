@@ -130,10 +130,16 @@ struct ScalarPtrs {
     double* p[kArMax];
     int k;
 };
-__global__ void k_ar_pack(ScalarPtrs sp, double* __restrict__ buf) {
+// local partial = main (+ the boundary views' partials of a split pass, added in this fixed order)
+__global__ void k_ar_pack(ScalarPtrs sp, ScalarPtrs e1, ScalarPtrs e2, double* __restrict__ buf) {
     pdl_trigger();
     pdl_wait();
-    for (int j = threadIdx.x; j < sp.k; j += blockDim.x) buf[j] = *sp.p[j];
+    for (int j = threadIdx.x; j < sp.k; j += blockDim.x) {
+        double v = *sp.p[j];
+        if (j < e1.k) v += *e1.p[j];
+        if (j < e2.k) v += *e2.p[j];
+        buf[j] = v;
+    }
 }
 // rank-order sum of the gathered partials: identical bits on every rank
 __global__ void k_ar_sum(ScalarPtrs sp, const double* __restrict__ g, int P) {
@@ -307,13 +313,90 @@ void halo_exchange(amg_hierarchy* h, int l, double* x) {
     halo_exchange_t<double>(h, Lv, x);
 }
 
-void dot_allreduce(amg_hierarchy* h, const std::vector<double*>& ptrs) {
+void halo_start(amg_hierarchy* h, int l, double* x) {
+    Level& Lv = h->lev[l];
+    if (!Lv.dist) return;
+    const Halo& H = Lv.H;
+    double* buf = H.sbuf;
+    if (H.nsend) {
+        launch_k(k_pack<double>, dim3(gridn(H.nsend)), dim3(kBlock), 0, h->s, H.nsend, (const int*)H.sidx,
+                 (const double*)x, buf);
+        CK(cudaGetLastError());
+        ++g_launches;
+    }
+    CK(cudaEventRecord(h->ev_pack, h->s));
+    CK(cudaStreamWaitEvent(h->cs, h->ev_pack, 0));
+    std::vector<P2P> ss, rr;
+    for (const Seg& g : H.send) ss.push_back({g.peer, buf + g.off, sizeof(double) * (size_t)g.cnt});
+    for (const Seg& g : H.recv) rr.push_back({g.peer, x + g.off, sizeof(double) * (size_t)g.cnt});
+    h->comm->sendrecv(ss, rr, h->cs);
+    CK(cudaEventRecord(h->ev_halo, h->cs));
+}
+
+void halo_finish(amg_hierarchy* h, int l) {
+    if (!h->lev[l].dist) return;
+    CK(cudaStreamWaitEvent(h->s, h->ev_halo, 0));
+}
+
+__global__ void k_slice_flags(int n, const int* __restrict__ rp, const int* __restrict__ ci, unsigned char* flag) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        bool b = false;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) b |= (ci[p] < 0 || ci[p] >= n);
+        if (b) flag[i >> 5] = 1;
+    }
+}
+
+// The interior range is the longest run of slices without a halo column; the boundary ranges are
+// the slices before and after it (2D strips / 3D slabs: the first and last grid lines of the block).
+void build_split(amg_hierarchy* h, int l) {
+    Level& Lv = h->lev[l];
+    Lv.split = false;
+    if (!Lv.dist || !Lv.op.sell || getenv("AMG_NO_OVERLAP")) return;
+    const int ns = Lv.S.nslices;
+    unsigned char* f = dalloc<unsigned char>((size_t)ns + 1, h->s);
+    CK(cudaMemsetAsync(f, 0, (size_t)ns + 1, h->s));
+    k_slice_flags<<<gridn(Lv.A.n), kBlock, 0, h->s>>>(Lv.A.n, Lv.A.rp, Lv.A.ci, f);
+    ++g_launches;
+    CK(cudaGetLastError());
+    std::vector<unsigned char> hf((size_t)ns);
+    CK(cudaMemcpyAsync(hf.data(), f, (size_t)ns, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    dfree(f, h->s);
+    int best_b = 0, best_e = 0;
+    for (int s = 0; s < ns;) {
+        if (hf[s]) { ++s; continue; }
+        int e = s;
+        while (e < ns && !hf[e]) ++e;
+        if (e - s > best_e - best_b) { best_b = s; best_e = e; }
+        s = e;
+    }
+    if (best_b == 0 && best_e == ns) return;  // no boundary slice (no halo): nothing to overlap
+    if (best_e - best_b < ns / 4) return;     // too little interior to hide the messages behind
+    auto view = [&](int a, int b) {
+        SpOp v = Lv.op;
+        v.S.sptr = Lv.S.sptr + a;
+        v.S.nslices = b - a;
+        v.S.srow0 = 32 * a;
+        return v;
+    };
+    Lv.op_int = view(best_b, best_e);
+    Lv.op_lo = view(0, best_b);
+    Lv.op_hi = view(best_e, ns);
+    Lv.split = true;
+}
+
+void dot_allreduce(amg_hierarchy* h, const std::vector<double*>& ptrs, const std::vector<double*>& extra1,
+                   const std::vector<double*>& extra2) {
     if (!h->comm || ptrs.empty()) return;
     if ((int)ptrs.size() > kArMax) throw Error(AMG_E_ARG, "too many scalars in one allreduce");
-    ScalarPtrs sp{};
+    ScalarPtrs sp{}, e1{}, e2{};
     sp.k = (int)ptrs.size();
+    e1.k = (int)extra1.size();
+    e2.k = (int)extra2.size();
     for (int j = 0; j < sp.k; ++j) sp.p[j] = ptrs[j];
-    launch_k(k_ar_pack, dim3(1), dim3(64), 0, h->s, sp, h->ar_send);
+    for (int j = 0; j < e1.k; ++j) e1.p[j] = extra1[j];
+    for (int j = 0; j < e2.k; ++j) e2.p[j] = extra2[j];
+    launch_k(k_ar_pack, dim3(1), dim3(64), 0, h->s, sp, e1, e2, h->ar_send);
     CK(cudaGetLastError());
     h->comm->allgather(h->ar_send, h->ar_recv, sizeof(double) * (size_t)sp.k, h->s);
     launch_k(k_ar_sum, dim3(1), dim3(64), 0, h->s, sp, (const double*)h->ar_recv, h->comm->size);
@@ -614,6 +697,11 @@ void warm_comm(amg_hierarchy* h) {
     for (int l = 0; l < h->g; ++l)
         if (h->lev[l].X) halo_exchange(h, l, h->lev[l].X);
     dot_allreduce(h, {h->osc + 2 * kMaxWin + 4});
+    for (int l = 0; l < h->g; ++l)  // the split passes' message pattern (same messages, other stream)
+        if (h->lev[l].X && h->lev[l].split) {
+            halo_start(h, l, h->lev[l].X);
+            halo_finish(h, l);
+        }
     if (h->g >= 1) allgatherv_d(h, h->lev[h->g].RHO, h->lev[h->g].offs);
     else allgatherv_d(h, h->b, h->lev[0].offs);
     CK(cudaStreamSynchronize(h->s));

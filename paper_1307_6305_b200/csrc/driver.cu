@@ -147,6 +147,9 @@ static void release(amg_hierarchy* h) {
     if (h->e1) cudaEventDestroy(h->e1);
     if (h->pe0) cudaEventDestroy(h->pe0);
     if (h->pe1) cudaEventDestroy(h->pe1);
+    if (h->ev_pack) cudaEventDestroy(h->ev_pack);
+    if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+    if (h->cs) cudaStreamDestroy(h->cs);
     delete h;
 }
 
@@ -310,6 +313,7 @@ void amg::finish_build(amg_hierarchy* h) {
         Lv.op.T = Lv.T;
         Lv.op.S = Lv.S;
         Lv.op.sell = Lv.S.sptr != nullptr;
+        if (Lv.dist) build_split(h, k);
         // vector layout [pad | lower halo | own | upper halo]
         Lv.lo_pad = (Lv.H.nlo + 3) & ~3;
         Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : Lv.A.n;
@@ -349,6 +353,10 @@ void amg::finish_build(amg_hierarchy* h) {
     if (h->comm) {
         h->ar_send = halloc<double>(h, kArMax);
         h->ar_recv = halloc<double>(h, (size_t)kArMax * h->comm->size);
+        h->dsplit = halloc<double>(h, kArMax);
+        CK(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
     }
     // coarse tail: first replicated level l >= 1 with nnz(A_l) <= tail_nnz (one SM runs it from L1/L2)
     h->l_tail = h->L;
@@ -476,6 +484,44 @@ static void ensure_inner_ws(amg_hierarchy* h, int nu) {
 // ------------------------------------------------------------------ solve schedule
 static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* out);
 
+// One SpMV-class pass on level l that reads x at the halo columns: `run(op, part)` launches the pass
+// over the slices of `op`.  On a row-partitioned level with an interior/boundary split the interior
+// slices (part 0) run while the halo messages are in flight, then the boundary slices
+// before (part 1) and after (part 2) them; a dot-producing pass writes parts 1/2 into split slots.
+template <class F>
+static void spmv_pass(amg_hierarchy* h, int l, double* x, F&& run) {
+    Level& Lv = h->lev[l];
+    if (!Lv.dist) {
+        run(Lv.op, 0);
+        return;
+    }
+    if (!Lv.split) {
+        halo_exchange(h, l, x);
+        run(Lv.op, 0);
+        return;
+    }
+    halo_start(h, l, x);
+    run(Lv.op_int, 0);
+    halo_finish(h, l);
+    run(Lv.op_lo, 1);
+    run(Lv.op_hi, 2);
+}
+
+// q = A d with d.q and d.rho into dq, dr (allreduced over the ranks on a row-partitioned level)
+static void spmv_dots_pass(amg_hierarchy* h, int l, double* d, const double* rho, double* q, double* dq,
+                           double* dr) {
+    Level& Lv = h->lev[l];
+    spmv_pass(h, l, d, [&](const SpOp& op, int part) {
+        double* o0 = part == 0 ? dq : h->dsplit + 2 * (part - 1);
+        double* o1 = part == 0 ? dr : h->dsplit + 2 * (part - 1) + 1;
+        launch_spmv_dots(op, d, rho, q, o0, o1, h->ds, h->s);
+    });
+    if (Lv.dist) {
+        if (Lv.split) dot_allreduce(h, {dq, dr}, {h->dsplit, h->dsplit + 1}, {h->dsplit + 2, h->dsplit + 3});
+        else dot_allreduce(h, {dq, dr});
+    }
+}
+
 // FCG_inner(l, RHO_l, nu) -> E_l.  On a row-partitioned level every SpMV
 // input is halo-exchanged first and every batch of dot partials is summed over the ranks before the
 // kernels that consume it.
@@ -510,9 +556,7 @@ static void fcg_inner(amg_hierarchy* h, int l, int nu) {
             }
             launch_direction(n, Lv.Z, Dp, c, dq, i, Di, s);
         }
-        halo_exchange(h, l, Di);
-        launch_spmv_dots(Lv.op, Di, rho, Qi, dq + i, dr + i, h->ds, s);  // q = A d, d.q, d.rho
-        if (Lv.dist) dot_allreduce(h, {dq + i, dr + i});
+        spmv_dots_pass(h, l, Di, rho, Qi, dq + i, dr + i);  // q = A d, d.q, d.rho
         launch_fcg_update(n, dr + i, dq + i, Di, Qi, Lv.E, i == 0, (i < nu - 1) ? rho : nullptr, nullptr, nullptr,
                           h->ds, s);
     }
@@ -540,8 +584,7 @@ static void amli_correction(amg_hierarchy* h, int l, int nu) {
     apply_B(h, l, nu, Lv.RHO, Lv.Z);
     launch_lincomb3(n, b[0], Lv.Z, 0.0, nullptr, 0.0, nullptr, cur, s);  // y_1 = b_0 B rho
     for (int k = 1; k <= m; ++k) {
-        halo_exchange(h, l, cur);
-        launch_resid(Lv.op, cur, Lv.RHO, T, nullptr, h->ds, s);
+        spmv_pass(h, l, cur, [&](const SpOp& op, int) { launch_resid(op, cur, Lv.RHO, T, nullptr, h->ds, s); });
         apply_B(h, l, nu, T, Lv.Z);
         // y_{k+1} = a_k y_k + (1 - a_k) y_{k-1} + b_k z  (y_0 = 0) into the y_{k-1} buffer
         launch_lincomb3(n, a[k], cur, 1.0 - a[k], k >= 2 ? prev : nullptr, b[k], Lv.Z, prev, s);
@@ -570,22 +613,24 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     // pre-smoothing S(r, 0): step 0 is free (x_1 = b0 r implicit)
     double* cur = Lv.X;
     double* prev = Lv.XA;
-    halo_exchange(h, l, const_cast<double*>(rin));
-    launch_smooth(Lv.op, rin, b[0], rin, nullptr, 0.0, a[1], b[1], Lv.X, s);  // k = 1 (x_0 = 0)
+    spmv_pass(h, l, const_cast<double*>(rin), [&](const SpOp& op, int) {
+        launch_smooth(op, rin, b[0], rin, nullptr, 0.0, a[1], b[1], Lv.X, s);  // k = 1 (x_0 = 0)
+    });
     if (m >= 2) {
-        halo_exchange(h, l, Lv.X);
-        launch_smooth(Lv.op, Lv.X, 1.0, rin, nullptr, b[0], a[2], b[2], Lv.XA, s);  // k = 2 (x_1 = b0 r)
+        spmv_pass(h, l, Lv.X, [&](const SpOp& op, int) {
+            launch_smooth(op, Lv.X, 1.0, rin, nullptr, b[0], a[2], b[2], Lv.XA, s);  // k = 2 (x_1 = b0 r)
+        });
         cur = Lv.XA;
         prev = Lv.X;
         for (int k = 3; k <= m; ++k) {
-            halo_exchange(h, l, cur);
-            launch_smooth(Lv.op, cur, 1.0, rin, prev, 0.0, a[k], b[k], prev, s);
+            spmv_pass(h, l, cur, [&](const SpOp& op, int) {
+                launch_smooth(op, cur, 1.0, rin, prev, 0.0, a[k], b[k], prev, s);
+            });
             std::swap(cur, prev);
         }
     }
     // residual + restriction
-    halo_exchange(h, l, cur);
-    launch_resid(Lv.op, cur, rin, Lv.RES, nullptr, h->ds, s);
+    spmv_pass(h, l, cur, [&](const SpOp& op, int) { launch_resid(op, cur, rin, Lv.RES, nullptr, h->ds, s); });
     Level& C = h->lev[l + 1];
     // the level below the last row-partitioned one is replicated: restrict into this rank's block of
     // it and allgather the blocks (C-gather); prolong from the same block
@@ -603,16 +648,18 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
     // post-smoothing S(r, x): x_{-1} = x_0 = cur
     double* other = (cur == Lv.X) ? Lv.XA : Lv.X;
-    halo_exchange(h, l, cur);
-    launch_smooth(Lv.op, cur, 1.0, rin, cur, 0.0, 1.0, b[0], other, s);  // k = 0
+    spmv_pass(h, l, cur, [&](const SpOp& op, int) {
+        launch_smooth(op, cur, 1.0, rin, cur, 0.0, 1.0, b[0], other, s);  // k = 0
+    });
     prev = cur;
     cur = other;
     const bool prof = (l == 0 && h->prof_on);
     if (prof) record_event(h->pe0, s);
     for (int k = 1; k <= m; ++k) {
         double* target = (k == m) ? out : prev;
-        halo_exchange(h, l, cur);
-        launch_smooth(Lv.op, cur, 1.0, rin, prev, 0.0, a[k], b[k], target, s);
+        spmv_pass(h, l, cur, [&](const SpOp& op, int) {
+            launch_smooth(op, cur, 1.0, rin, prev, 0.0, a[k], b[k], target, s);
+        });
         prev = cur;
         cur = target;
     }
@@ -663,9 +710,7 @@ static void outer_iteration(amg_hierarchy* h, int pos, int nu) {
         }
         launch_direction(n, h->Z, Ds, c, dq, pos, Dp, s);
     }
-    halo_exchange(h, 0, Dp);
-    launch_spmv_dots(h->lev[0].op, Dp, h->r, Qp, dq + pos, dr, h->ds, s);
-    if (dist) dot_allreduce(h, {dq + pos, dr});
+    spmv_dots_pass(h, 0, Dp, h->r, Qp, dq + pos, dr);
     launch_fcg_update(n, dr, dq + pos, Dp, Qp, h->x, false, h->r, rr, h->flag, h->ds, s);
     if (dist) dot_allreduce(h, {rr});
 }

@@ -57,6 +57,10 @@ struct Level {
     std::vector<int64_t> offs;   // block offsets of all ranks (P+1): the partition this level's rows came in
     Halo H;
     int lo_pad = 0;              // own element offset inside a vector allocation (>= H.nlo, multiple of 4)
+    // halo overlap: the SELL slices that read no halo column (interior, one range) run while the halo
+    // is in flight; the boundary slices (the ranges around it) after it has arrived
+    bool split = false;
+    SpOp op_int, op_lo, op_hi;   // slice views: interior, boundary before it, boundary after it
     int ld = 0;                  // vector slot stride (lo_pad + n + nhi, rounded up to 4)
 };
 
@@ -99,6 +103,9 @@ struct amg_hierarchy {
     double* ar_send = nullptr;       // batched dot allreduce scratch: [kArMax] and [kArMax * P]
     double* ar_recv = nullptr;
     double *bfull = nullptr, *xfull = nullptr;  // g == 0: gathered b and x
+    cudaStream_t cs = nullptr;       // communication stream (halo messages overlap the interior rows)
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    double* dsplit = nullptr;        // boundary-view partial dots of a split pass [4]: lo (dq, dr), hi (dq, dr)
 };
 
 namespace amg {
@@ -129,7 +136,15 @@ void build_dist(amg_hierarchy* h, int64_t n_global, int64_t row_begin, int n_loc
 void halo_exchange(amg_hierarchy* h, int l, double* x);  // no-op unless level l is row-partitioned
 // sum the scalars at ptrs over the ranks (each rank's local partial; rank-order sum, identical on
 // every rank); no-op on one GPU
-void dot_allreduce(amg_hierarchy* h, const std::vector<double*>& ptrs);
+// (extra1/extra2: partials of the boundary views of a split pass, added to ptrs[j] in this order)
+void dot_allreduce(amg_hierarchy* h, const std::vector<double*>& ptrs, const std::vector<double*>& extra1 = {},
+                   const std::vector<double*>& extra2 = {});
+// split halo exchange: pack + messages on the communication stream (halo_start), then make the
+// compute stream wait for them (halo_finish); no-op pair unless level l is row-partitioned
+void halo_start(amg_hierarchy* h, int l, double* x);
+void halo_finish(amg_hierarchy* h, int l);
+// interior/boundary slice views of a row-partitioned SELL level (sets Lv.split, op_int, op_lo, op_hi)
+void build_split(amg_hierarchy* h, int l);
 // own block (count_r elements at displ_r of `full`) of every rank gathered into `full` (device)
 void allgatherv_d(amg_hierarchy* h, double* full, const std::vector<int64_t>& offs);
 // warm every exchange pattern once outside graph capture (NCCL connects peers lazily)

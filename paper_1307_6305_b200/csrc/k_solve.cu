@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kBlock) k_sell(Sell S, const double* __restric
         const int sn = sl + nwarps;
         int bn = 0, en = 0;
         if (sn < S.nslices) { bn = __ldg(S.sptr + sn); en = __ldg(S.sptr + sn + 1); }
-        const int i = sl * 32 + lane;
+        const int i = S.srow0 + sl * 32 + lane;
         const bool act = i < S.n;
         const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, i, S.chi};
         typename Epi::Pre pre{};
@@ -498,8 +498,9 @@ __global__ void __launch_bounds__(kBlock) k_sell_pipe(Sell S, const double* __re
         int b = __ldg(S.sptr + sl), w = __ldg(S.sptr + sl + 1) - b;
         Buf A{};
         {
-            const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, sl * 32 + lane, S.chi};
-            pipe_load<Epi, W, VM, CM>(S, ops, epi, xg, b, w, lane, sl * 32 + lane, A);
+            const int i0 = S.srow0 + sl * 32 + lane;
+            const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, i0, S.chi};
+            pipe_load<Epi, W, VM, CM>(S, ops, epi, xg, b, w, lane, i0, A);
         }
         int sn = sl + nwarps, bn = 0, wn = 0;
         if (sn < S.nslices) { bn = __ldg(S.sptr + sn); wn = __ldg(S.sptr + sn + 1) - bn; }
@@ -507,14 +508,15 @@ __global__ void __launch_bounds__(kBlock) k_sell_pipe(Sell S, const double* __re
             // issue the next slice's streams before this slice's gathers
             Buf B{};
             if (sn < S.nslices) {
-                const SellOps<VM, CM> opn{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, sn * 32 + lane, S.chi};
-                pipe_load<Epi, W, VM, CM>(S, opn, epi, xg, bn, wn, lane, sn * 32 + lane, B);
+                const int in = S.srow0 + sn * 32 + lane;
+                const SellOps<VM, CM> opn{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, in, S.chi};
+                pipe_load<Epi, W, VM, CM>(S, opn, epi, xg, bn, wn, lane, in, B);
             }
             const int s2 = sn + nwarps;
             int b2 = 0, w2 = 0;
             if (s2 < S.nslices) { b2 = __ldg(S.sptr + s2); w2 = __ldg(S.sptr + s2 + 1) - b2; }
             // this slice: gathers and the fma chain in entry order
-            const int i = sl * 32 + lane;
+            const int i = S.srow0 + sl * 32 + lane;
             const SellOps<VM, CM> ops{S.val, S.vcode, S.col, S.ccode, S.coff, S.pcode, sv, sc, i, S.chi};
             double x[W];
 #pragma unroll
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
                 const int s0 = c * CS, s1 = min(s0 + CS, S.nslices);
                 for (int q = 0; q <= CS; ++q) hdr[q] = hb[q];
                 const int b0 = hdr[0], b1 = hdr[CS];
-                const int r0 = s0 * 32, r1 = min(s1 * 32, S.n);
+                const int r0 = S.srow0 + s0 * 32, r1 = min(S.srow0 + s1 * 32, S.n);
                 const uint32_t vb = (uint32_t)tma_align16((r1 - r0) * 8);
                 const uint32_t ab = (uint32_t)(b1 - b0) * 32u * St::ESA;
                 const uint32_t bb = (uint32_t)(b1 - b0) * 32u * St::ESB;
@@ -821,7 +823,8 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
                 const int s = c * CS + warp;
                 if (s < S.nslices) {
                     const int hq = lds_s32(sb + 4 * warp), wq = lds_s32(sb + 4 * (warp + 1)) - hq;
-                    tma_slice_dispatch<Epi, VM, CM, W, Lay>(wq, epi, sb, warp, (uint32_t)(hq - h0), s * 32 + lane,
+                    tma_slice_dispatch<Epi, VM, CM, W, Lay>(wq, epi, sb, warp, (uint32_t)(hq - h0),
+                                                            S.srow0 + s * 32 + lane,
                                                             lane, S.n, S.chi, sv_a, sc_a, xgr, v0g != nullptr,
                                                             v1g != nullptr, acc);
                 }
@@ -839,7 +842,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
                 aoff[h] = off;
                 const uint32_t A = sb + Lay::HDR + off * 32 * St::ESA + lane * St::ESA;
                 const uint32_t Bc = sb + Lay::HDR + Lay::A + off * 32 * St::ESB + lane * St::ESB;
-                const int i = s * 32 + lane;
+                const int i = S.srow0 + s * 32 + lane;
                 auto entry = [&](int u) {
                     int cr;
                     if constexpr (CM == 3) {
@@ -895,7 +898,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
                         sum = fma(v, x[h][u], sum);
                     }
                 }
-                const int i = (c * CS + q) * 32 + lane;
+                const int i = S.srow0 + (c * CS + q) * 32 + lane;
                 const uint32_t r8 = 8 * (q * 32 + lane);
                 if (w[h] > 0 && i < S.n) {
                     const double xi = lds_f64(vt + r8);
