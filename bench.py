@@ -134,6 +134,27 @@ def sample_size(cfg_name: str, steps: int) -> int:
     return 1024 if steps <= 16 else 512
 
 
+def model_bytes_per_iter(n, nnz, m, nu, W=5):
+    """SURVEY.md 8(d) byte model of one outer iteration (int32 indices, fp64 values, x gathered once):
+    sum over levels l < L-1 of nu^l visits x [first pre-step + (m-1) steps + residual + SpMV/dots +
+    m post steps + transfers], the outer FCG vector work at the average window (W-1)/2, the inner FCG
+    vector work, and the dense coarsest GEMVs.  The uncompressed format, i.e. the SURVEY's ceiling
+    model; the kernels stream less (compressed codes)."""
+    L = len(n)
+    tot = 0.0
+    for l in range(L - 1):
+        z, k = nnz[l], n[l]
+        per = (12 * z + 20 * k) + (m - 1) * (12 * z + 36 * k) + 2 * (12 * z + 28 * k) + m * (12 * z + 36 * k) \
+            + 32 * k + 20 * n[l + 1]
+        tot += nu ** l * per
+        if l >= 1:  # FCG_inner(l): nu iterations, window i
+            tot += nu ** (l - 1) * sum(16 * (1 + i) + 40 for i in range(nu)) * k
+    w = (W - 1) / 2
+    tot += (16 * (1 + w) + 56) * n[0]
+    tot += nu ** (L - 2) * 8 * n[L - 1] ** 2
+    return tot
+
+
 def run_reference(a):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -327,6 +348,7 @@ def main_ours(a):
                "sample": f"{a.config} recipe at size {size} (n={r['n']}): oracle setup {r['setup_s']:.2f}s + "
                          f"solve {r['solve_s']:.2f}s, {r['iters']} iters, single thread; value = n*iters/total"}
 
+    mb = model_bytes_per_iter(last["n"], last["nnz"], prm["degree"], prm["k_inner"])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
@@ -343,6 +365,8 @@ def main_ours(a):
         "setup_ms": setup_ms, "solve_ms": solve_ms,
         "solve_only": {"value": n * statistics.mean(iters) / (solve_ms / 1e3), "unit": UNIT,
                        "ms_per_iter": solve_ms / max(1, statistics.mean(iters))},
+        "solve_model": {"bytes_per_iter": mb, "effective_GBps": mb * statistics.mean(iters) / (solve_ms / 1e3) / 1e9,
+                        "model": "SURVEY 8(d) uncompressed byte model (int32/fp64) of one outer iteration"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "launches_per_iter": last["launches_per_iter"], "clocks": clk,
         "final_relres": infos[-1][2], "true_relres": last["last_true_relres"],
