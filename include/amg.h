@@ -83,7 +83,11 @@ typedef struct {
                                1/t on [1/amli_kappa, 1] (reading A23), a linear SPD preconditioner */
     double   amli_kappa;    /* cycle 2: 1/theta of the AMLI polynomial interval; 0 => rule R1 (A8) for
                                degree nu-1 (4 for nu = 2); default 0 */
-    int64_t  reserved[2];
+    int32_t  lanczos_steps; /* 0 = lambda_1 = ||A_l||_inf (default); k > 0 = reading A24
+                               (SURVEY 8(f) item 3): lambda_1 = min(||A_l||_inf, 1.1 theta_k), theta_k the
+                               largest Ritz value of k Lanczos steps (smoothed levels; amg_setup only) */
+    int32_t  reserved32;
+    int64_t  reserved[1];
 } amg_options;
 
 typedef struct {

@@ -36,6 +36,7 @@
 
 #define ORC_MAXLEV 64
 #define ORC_MAXDEG 32
+#define ORC_MAXLANCZOS 64
 
 /* ========================================================== sparse matrix */
 typedef struct {
@@ -145,6 +146,67 @@ static uint64_t osm64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     return z ^ (z >> 31);
+}
+
+/* Largest eigenvalue of the symmetric tridiagonal T (diagonal a[0..k), off-diagonal b[1..k)) by
+ * bisection on the Sturm count (number of eigenvalues < x), to adjacent doubles. */
+static double otridiag_max(int k, const double *a, const double *b) {
+    double lo = a[0], hi = a[0];
+    for (int j = 0; j < k; ++j) { /* Gershgorin interval */
+        double r = (j > 0 ? fabs(b[j]) : 0.0) + (j + 1 < k ? fabs(b[j + 1]) : 0.0);
+        if (a[j] - r < lo) lo = a[j] - r;
+        if (a[j] + r > hi) hi = a[j] + r;
+    }
+    for (int it = 0; it < 200; ++it) {
+        double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        int cnt = 0; /* eigenvalues < mid: negative pivots of T - mid I */
+        double d = 1.0;
+        for (int j = 0; j < k; ++j) {
+            d = a[j] - mid - (j > 0 ? b[j] * b[j] / d : 0.0);
+            if (d == 0.0) d = -1e-300;
+            if (d < 0.0) cnt++;
+        }
+        if (cnt == k) hi = mid; else lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+/* Reading A24 ("tighter lambda_max"; opt-in, the paper's setting is
+ * lambda_1 = ||A||_inf): lambda_1 = min(||A||_inf, 1.1 theta_k) with theta_k the largest Ritz
+ * value of k plain Lanczos steps on A from v_0 = u/||u||, u_i = 2 U(z ^ i) - 1,
+ * U(y) = (splitmix64(y) >> 11) 2^-53, z = splitmix64(seed ^ 0x4C414E435A4F5300 ^ level):
+ *   w = A v_j - beta_j v_{j-1}; alpha_j = v_j.A v_j; w -= alpha_j v_j; beta_{j+1} = ||w||; v_{j+1} = w/beta_{j+1}
+ * (w formed as A v_j - alpha_j v_j - beta_j v_{j-1}; stops early if beta_{j+1} = 0). */
+static uint64_t osm64(uint64_t z);
+double orc_lanczos_max(const int64_t n, const int64_t *rp, const int32_t *ci, const double *v, int k, uint64_t seed,
+                       int level) {
+    ocsr A = {n, rp[n], (int64_t *)rp, (int32_t *)ci, (double *)v, NULL};
+    double *vj = malloc(sizeof(double) * n), *vm = calloc((size_t)n, sizeof(double));
+    double *w = malloc(sizeof(double) * n);
+    double al[ORC_MAXLANCZOS], be[ORC_MAXLANCZOS + 1];
+    uint64_t z = osm64(seed ^ 0x4C414E435A4F5300ULL ^ (uint64_t)level);
+    for (int64_t i = 0; i < n; ++i) vj[i] = 2.0 * ((double)(osm64(z ^ (uint64_t)i) >> 11) * 0x1.0p-53) - 1.0;
+    double nr = sqrt(odot(n, vj, vj));
+    for (int64_t i = 0; i < n; ++i) vj[i] /= nr;
+    be[0] = 0.0;
+    int steps = 0;
+    if (k > ORC_MAXLANCZOS) k = ORC_MAXLANCZOS;
+    for (int j = 0; j < k; ++j) {
+        ospmv(&A, vj, w);
+        al[j] = odot(n, vj, w);
+        for (int64_t i = 0; i < n; ++i) w[i] = w[i] - al[j] * vj[i] - be[j] * vm[i];
+        steps = j + 1;
+        be[j + 1] = sqrt(odot(n, w, w));
+        if (!(be[j + 1] > 0.0)) break;
+        for (int64_t i = 0; i < n; ++i) {
+            vm[i] = vj[i];
+            vj[i] = w[i] / be[j + 1];
+        }
+    }
+    double t = otridiag_max(steps, al, be);
+    free(vj); free(vm); free(w);
+    return t;
 }
 
 /* salt(seed, level, pass) = splitmix64(seed ^ ((level << 8) ^ pass))  (A2). */
@@ -378,6 +440,7 @@ typedef struct {
     double kappa_opt;
     int restart, max_iter, rule, cycle, nparts;
     double amli_kappa; /* cycle 2: 1/theta of the AMLI polynomial interval; 0 = reading A23 */
+    int lanczos;       /* reading A24: k Lanczos steps for lambda_1 (0 = ||A||_inf, the paper's) */
     int64_t gather_rows;
     uint64_t seed;
     olevel lev[ORC_MAXLEV];
@@ -499,6 +562,8 @@ void orc_free(orc_h *h) {
     free(h);
 }
 
+static int orc_get_lanczos(void);
+
 /* Setup: level loop while n_l > coarsest_size:
  * lambda_1, kappa rule (A8), coefficients, p matching passes composed
  * into agg_l, Galerkin A_{l+1} = P^T A_l P, then the dense coarsest. */
@@ -514,6 +579,7 @@ int orc_setup(int64_t n, const int64_t *rp, const int32_t *ci, const double *val
     h->m = degree; h->coarsest_size = coarsest_size; h->kappa_opt = kappa;
     h->restart = restart; h->max_iter = max_iter; h->seed = seed; h->nparts = nparts;
     h->gather_rows = gather_rows; h->rule = rule; h->cycle = cycle;
+    h->lanczos = orc_get_lanczos();
     int st = oform_A0(n, rp, ci, val, d, &h->lev[0].A);
     if (st) { free(h); return st; }
     h->singular = 1;
@@ -527,6 +593,10 @@ int orc_setup(int64_t n, const int64_t *rp, const int32_t *ci, const double *val
     for (;;) {
         olevel *L = &h->lev[l];
         L->lambda1 = oinf_norm(&L->A);
+        if (h->lanczos > 0 && L->A.n > coarsest_size) { /* reading A24 (smoothed levels only) */
+            double t = 1.1 * orc_lanczos_max(L->A.n, L->A.rp, L->A.ci, L->A.v, h->lanczos, seed, l);
+            if (t < L->lambda1) L->lambda1 = t;
+        }
         L->kappa = kappa > 1.0 ? kappa : orc_kappa_rule(degree);
         orc_poly_coeffs(L->lambda1, L->kappa, degree, L->alpha, L->beta);
         if (L->A.n <= coarsest_size) break;
@@ -738,6 +808,9 @@ int orc_solve(const orc_h *h, const double *b_in, double *x, double tol, int nu,
 
 /* ================================================= exported accessors / pieces */
 int orc_num_levels(const orc_h *h) { return h->nlev; }
+/* reading A24: k Lanczos steps for lambda_1 in subsequent orc_setup calls of this thread (0 = off) */
+static _Thread_local int g_lanczos = 0;
+void orc_set_lanczos(int k) { g_lanczos = k; }
 /* cycle 2 (stationary AMLI): 1/theta of the coarse polynomial interval (0 = reading A23) */
 void orc_set_amli_kappa(orc_h *h, double kappa) { h->amli_kappa = kappa; }
 int orc_is_singular(const orc_h *h) { return h->singular; }
@@ -851,3 +924,5 @@ void orc_csr_free(void *H) {
     ocsr_free((ocsr *)H);
     free(H);
 }
+
+static int orc_get_lanczos(void) { return g_lanczos; }

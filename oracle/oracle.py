@@ -45,6 +45,8 @@ def _L():
         "orc_solve": (i32, [vp, vp, vp, dbl, i32, vp, vp, vp]),
         "orc_num_levels": (i32, [vp]),
         "orc_set_amli_kappa": (None, [vp, dbl]),
+        "orc_set_lanczos": (None, [i32]),
+        "orc_lanczos_max": (dbl, [i64, vp, vp, vp, i32, u64, i32]),
         "orc_is_singular": (i32, [vp]),
         "orc_level_info": (None, [vp, i32, vp, vp, vp, vp, vp, vp]),
         "orc_level_csr": (None, [vp, i32, vp, vp, vp]),
@@ -132,6 +134,12 @@ def aggregate_pass(rp, ci, w, seed=0, level=0, pass_=0, rule=0):
     return agg, int(nc)
 
 
+def lanczos_max(rp, ci, v, k, seed=0, level=0) -> float:
+    """Largest Ritz value of k Lanczos steps from the counter-based start vector (reading A24)."""
+    rp, ci, v = _c(rp, np.int64), _c(ci, np.int32), _c(v, np.float64)
+    return _L().orc_lanczos_max(len(rp) - 1, _p(rp), _p(ci), _p(v), k, seed, level)
+
+
 def edge_hash(seed, level, pass_, a, b) -> int:
     return int(_L().orc_edge_hash(seed, level, pass_, a, b))
 
@@ -163,15 +171,17 @@ class Hierarchy:
     """Oracle setup + solve (O5-O8)."""
 
     def __init__(self, rp, ci, val, d, passes, degree, coarsest_size=100, kappa=0.0, restart=5,
-                 max_iter=500, seed=0, nparts=1, gather_rows=0, rule=0, cycle=0, amli_kappa=0.0):
+                 max_iter=500, seed=0, nparts=1, gather_rows=0, rule=0, cycle=0, amli_kappa=0.0, lanczos=0):
         self._keep = [_c(rp, np.int64), _c(ci, np.int32), _c(val, np.float64), _c(d, np.float64)]
         rp, ci, val, d = self._keep
         self.m = degree
         self.passes = passes
         h = vp()
+        _L().orc_set_lanczos(int(lanczos))
         st = _L().orc_setup(len(rp) - 1, _p(rp), _p(ci), _p(val), _p(d), passes, degree, coarsest_size, kappa,
                             restart, max_iter, seed, nparts, gather_rows, rule, cycle, ctypes.byref(h))
         self._keep = None
+        _L().orc_set_lanczos(0)
         if st != 0:
             raise OracleError(st)
         self.h = h
@@ -255,5 +265,5 @@ def setup_problem(prob, **over) -> Hierarchy:
     p = dict(prob.params)
     p.update(over)
     kw = {k: p[k] for k in ("coarsest_size", "kappa", "restart", "max_iter", "seed", "nparts", "gather_rows",
-                            "rule", "cycle", "amli_kappa") if k in p}
+                            "rule", "cycle", "amli_kappa", "lanczos") if k in p}
     return Hierarchy(prob.rp, prob.ci, prob.val, prob.d, p["passes"], p["degree"], **kw)

@@ -105,6 +105,8 @@ Csr form_A0(int n, const int64_t* rp, const int32_t* ci, const double* v, const 
 double inf_norm(const Csr& A, cudaStream_t s);
 // true if some d_i != 0
 bool any_nonzero(int n, const double* d, cudaStream_t s);
+// Lanczos start vector of reading A24: out_i = 2 U(z ^ i) - 1, U(y) = (splitmix64(y) >> 11) 2^-53
+void launch_lanczos_start(int n, uint64_t z, double* out, cudaStream_t s);
 
 struct PassGraph {     // matching pass graph G_t: CSR with integer multiplicities, no diagonal
     int n = 0;

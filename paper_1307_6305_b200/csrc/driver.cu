@@ -291,6 +291,72 @@ double* amg::valloc(amg_hierarchy* h, Level& Lv, int slots, bool ws) {
     return base + Lv.lo_pad;
 }
 
+// Largest eigenvalue of the symmetric tridiagonal (a[0..k), b[1..k)) by Sturm-count bisection.
+static double tridiag_max(int k, const double* a, const double* b) {
+    double lo = a[0], hi = a[0];
+    for (int j = 0; j < k; ++j) {
+        const double r = (j > 0 ? std::fabs(b[j]) : 0.0) + (j + 1 < k ? std::fabs(b[j + 1]) : 0.0);
+        lo = std::min(lo, a[j] - r);
+        hi = std::max(hi, a[j] + r);
+    }
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        int cnt = 0;
+        double d = 1.0;
+        for (int j = 0; j < k; ++j) {
+            d = a[j] - mid - (j > 0 ? b[j] * b[j] / d : 0.0);
+            if (d == 0.0) d = -1e-300;
+            if (d < 0.0) ++cnt;
+        }
+        if (cnt == k) hi = mid; else lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+// Reading A24 (opt-in): largest Ritz value of k plain Lanczos steps on A_l from
+// the counter-based start vector, every vector operation in the library's kernels (SpMV + dots,
+// linear combinations), the k x k tridiagonal on the host.
+static double lanczos_max(amg_hierarchy* h, int l, int k) {
+    Level& Lv = h->lev[l];
+    cudaStream_t s = h->s;
+    const int n = Lv.A.n;
+    double* buf = dalloc<double>(3 * ((size_t)n + 8), s);
+    double* vj = buf;
+    double* vm = buf + n + 8;
+    double* w = buf + 2 * (n + 8);
+    double* sc = dalloc<double>(4, s);
+    const uint64_t z = host_sm64(h->opt.seed ^ 0x4C414E435A4F5300ULL ^ (uint64_t)l);
+    launch_lanczos_start(n, z, vj, s);
+    CK(cudaMemsetAsync(vm, 0, sizeof(double) * n, s));
+    auto read = [&](const double* p) {
+        double v = 0.0;
+        CK(cudaMemcpyAsync(&v, p, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return v;
+    };
+    launch_dot(n, vj, vj, sc, h->ds, s);
+    launch_lincomb3(n, 1.0 / std::sqrt(read(sc)), vj, 0.0, nullptr, 0.0, nullptr, vj, s);
+    if (k > 64) k = 64;
+    double al[64] = {}, be[65] = {};
+    be[0] = 0.0;
+    int steps = 0;
+    for (int j = 0; j < k; ++j) {
+        launch_spmv_dots(Lv.op, vj, vj, w, sc, sc + 1, h->ds, s);  // w = A v_j, alpha_j = v_j.w
+        al[j] = read(sc);
+        launch_lincomb3(n, 1.0, w, -al[j], vj, -be[j], vm, w, s);
+        launch_dot(n, w, w, sc + 2, h->ds, s);
+        steps = j + 1;
+        be[j + 1] = std::sqrt(read(sc + 2));
+        if (!(be[j + 1] > 0.0)) break;
+        launch_lincomb3(n, 1.0 / be[j + 1], w, 0.0, nullptr, 0.0, nullptr, vm, s);  // v_{j+1} into v_{j-1}'s slot
+        std::swap(vj, vm);
+    }
+    dfree(buf, s);
+    dfree(sc, s);
+    return tridiag_max(steps, al, be);
+}
+
 void amg::finish_build(amg_hierarchy* h) {
     cudaStream_t s = h->s;
     PhaseTimer pt(s);
@@ -369,6 +435,16 @@ void amg::finish_build(amg_hierarchy* h) {
         CK(cudaDeviceGetLimit(&cur, cudaLimitStackSize));
         if (cur < 4096) CK(cudaDeviceSetLimit(cudaLimitStackSize, 4096));  // t_B/t_fcg recursion
         h->d_tlev = halloc<TLevel>(h, kMaxLevels);
+    }
+    // reading A24 (opt-in): tighter lambda_1 on the smoothed levels (needs the SpMV formats and the
+    // dot scratch above), coefficients recomputed
+    if (h->opt.lanczos_steps > 0) {
+        for (int k = 0; k < h->L - 1; ++k) {
+            Level& Lv = h->lev[k];
+            const double t = 1.1 * lanczos_max(h, k, h->opt.lanczos_steps);
+            if (t < Lv.lambda1) Lv.lambda1 = t;
+            poly_coeffs(Lv.lambda1, Lv.kappa, h->m, Lv.alpha, Lv.beta);
+        }
     }
     CK(cudaStreamSynchronize(s));
     pt.mark("workspaces");
@@ -886,6 +962,8 @@ static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t 
     if (o.cycle != 0 && o.cycle != 2) return fail(AMG_E_ARG, "amg_setup: cycle must be 0 (k-cycle) or 2 (AMLI)");
     if (o.amli_kappa != 0.0 && !(o.amli_kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: amli_kappa must be 0 or > 1");
     if (comm && !comm->c) return fail(AMG_E_ARG, "amg_setup_dist: invalid communicator");
+    if (o.lanczos_steps < 0 || o.lanczos_steps > 64 || (comm && o.lanczos_steps > 0))
+        return fail(AMG_E_ARG, "amg_setup: lanczos_steps must be in [0, 64] (single GPU only)");
     if (o.kappa != 0.0 && !(o.kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: kappa must be 0 or > 1");
     if (o.kappa > 1.0 && !(Em_of(poly_degree, o.kappa) < 1.0))
         return fail(AMG_E_ARG, "amg_setup: E_m(kappa) >= 1: the smoother would not converge (reading A9)");

@@ -207,6 +207,19 @@ bool any_nonzero(int n, const double* d, cudaStream_t s) {
     return f != 0;
 }
 
+// ------------------------------------------------------------------ Lanczos start vector (A24)
+__device__ __forceinline__ uint64_t sm64(uint64_t z);
+__global__ void k_lanczos_start(int n, uint64_t z, double* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = 2.0 * ((double)(sm64(z ^ (uint64_t)i) >> 11) * 0x1.0p-53) - 1.0;
+}
+
+void launch_lanczos_start(int n, uint64_t z, double* out, cudaStream_t s) {
+    k_lanczos_start<<<grid_for(n), kBlock, 0, s>>>(n, z, out);
+    ++g_launches;
+    CK(cudaGetLastError());
+}
+
 // ------------------------------------------------------------------ lambda_1 (a1)
 __global__ void k_rowabs_max(int n, const int* __restrict__ rp, const double* __restrict__ v,
                              unsigned long long* out) {
@@ -306,20 +319,24 @@ __device__ __forceinline__ bool key_gt(const EKey& a, const EKey& b) {
     return a.hi > b.hi;
 }
 
-// handshake round, step 1: every free vertex proposes to its max-key free neighbour
+// handshake round, step 1: every free vertex (mate -1) proposes to its max-key free neighbour.  A
+// free vertex with no free neighbour can never be matched (matches are never undone): it is marked
+// settled (mate -2, unmatched) so later rounds skip it.  Within one round only settled marks are
+// written, and a vertex is settled only if no neighbour is free, so no free vertex reads one.
 __global__ void k_propose(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                          const uint32_t* __restrict__ w, const int* __restrict__ mate, int* __restrict__ prop,
+                          const uint32_t* __restrict__ w, int* __restrict__ mate, int* __restrict__ prop,
                           uint64_t salt, int off, int* any) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         int best = -1;
-        if (mate[v] < 0) {
+        if (mate[v] == -1) {
             EKey bk{};
             for (int p = rp[v]; p < rp[v + 1]; ++p) {
                 const int u = ci[p];
-                if (mate[u] >= 0) continue;
+                if (mate[u] != -1) continue;
                 EKey k = make_key(w[p], v, u, salt, off);
                 if (best < 0 || key_gt(k, bk)) { bk = k; best = u; }
             }
+            if (best < 0) mate[v] = -2;
         }
         prop[v] = best;
         if (best >= 0) *any = 1;
@@ -330,7 +347,7 @@ __global__ void k_propose(int n, const int* __restrict__ rp, const int* __restri
 __global__ void k_accept(int n, int* __restrict__ mate, const int* __restrict__ prop) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         const int u = prop[v];
-        if (u >= 0 && mate[v] < 0 && prop[u] == v) mate[v] = u;
+        if (u >= 0 && mate[v] == -1 && prop[u] == v) mate[v] = u;
     }
 }
 
@@ -983,14 +1000,13 @@ __global__ void k_iota(int n, int* a) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
 }
 
+// aptr[I] = first position of aggregate I in the sorted order: every id in [0, nc) has a member (its
+// leader), so the heads of the sorted runs write every entry; aptr[nc] = n
 __global__ void k_aptr(int nc, int n, const int* __restrict__ sorted_agg, int* __restrict__ aptr) {
-    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I <= nc; I += gridDim.x * blockDim.x) {
-        int lo = 0, hi = n;
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (sorted_agg[mid] < I) lo = mid + 1; else hi = mid;
-        }
-        aptr[I] = lo;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int a = sorted_agg[t];
+        if (t == 0 || sorted_agg[t - 1] != a) aptr[a] = t;
+        if (t == n - 1) aptr[nc] = n;
     }
 }
 
@@ -1001,7 +1017,7 @@ void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaSt
     ++g_launches;
     CK(cudaGetLastError());
     sort_pairs(agg, sk, iota, perm, n, bits_for(nc), s);
-    k_aptr<<<grid_for(nc + 1), kBlock, 0, s>>>(nc, n, sk, aptr);
+    k_aptr<<<grid_for(n), kBlock, 0, s>>>(nc, n, sk, aptr);
     ++g_launches;
     CK(cudaGetLastError());
     dfree(iota, s);

@@ -398,3 +398,34 @@ def test_amli_cycle_parity(amg, gen_mod, oracle_mod, name):
         assert st == 0 and rr <= 1e-8 and abs(it - oref["iters"]) <= 1, (it, oref["iters"])
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("name", ["C1", "rgg"])
+def test_lanczos_lambda_parity(amg, gen_mod, oracle_mod, name):
+    """Reading A24 (opt-in lanczos_steps): the GPU's Lanczos lambda_1 on every smoothed level matches the
+    oracle's to 1e-12 (only the dots' summation order differs), B_0(r) <= 1e-10, iterations +-1."""
+    if name == "C1":
+        p = gen_mod.problem("C1")
+    else:
+        p = gen_mod.rgg(20000, seed=7)
+        p.params = dict(passes=4, degree=4, coarsest_size=100, seed=0)
+    hier = oracle_mod.setup_problem(p, lanczos=10)
+    prm = p.params
+    o = amg.amg_options_default(coarsest_size=prm.get("coarsest_size", 100), seed=prm.get("seed", 0), lanczos_steps=10)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, prm["passes"], prm["degree"], o)
+    try:
+        for l in range(hier.nlev):
+            s = amg.amg_level_sizes(h, l, prm["degree"])
+            assert s["lambda1"] == pytest.approx(hier.level_info(l)["lambda1"], rel=1e-12), l
+        r = np.random.default_rng(1).uniform(-1, 1, p.n)
+        z = np.empty(p.n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        ref = hier.precond(r, nu=2, level=0)
+        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        b = gen_mod.rhs(p.n, 0)
+        x = np.zeros(p.n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        oref = hier.solve(b, tol=1e-8, nu=2)
+        assert st == 0 and abs(it - oref["iters"]) <= 1, (it, oref["iters"])
+    finally:
+        amg.amg_free(h)

@@ -619,3 +619,31 @@ def test_amli_solve_converges(oracle_mod, gen_mod):
     res = h.solve(b, tol=1e-8, nu=2)
     assert res["status"] == 0 and res["true_relres"] <= 2e-8
     assert res["iters"] <= 40
+
+
+def test_lanczos_lambda_max_pins(oracle_mod, gen_mod):
+    """Reading A24 (opt-in): the Ritz value is a lower bound of lambda_max that
+    reaches it with k = n steps; 1.1 x the 10-step value bounds lambda_max from above on the test
+    graphs; the setup uses min(||A||_inf, 1.1 theta_10)."""
+    for seed, (n, weighted) in enumerate([(40, False), (60, True)]):
+        p = gen_mod.random_graph(n, 5, seed=seed + 3, weighted=weighted, dirichlet=True)
+        A = H.A0_dense(p)
+        lmax = np.linalg.eigvalsh(A).max()
+        rp, ci, v = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 1, 2, coarsest_size=n).level_csr(0)
+        for k in (2, 5, 10):
+            t = oracle_mod.lanczos_max(rp, ci, v, k)
+            assert t <= lmax * (1 + 1e-12)
+        assert oracle_mod.lanczos_max(rp, ci, v, n) == pytest.approx(lmax, rel=1e-8)
+    for p in (gen_mod.problem("C1"), gen_mod.rgg(3000, seed=2), gen_mod.random_graph(800, 7, seed=4, weighted=True)):
+        import scipy.sparse as sp
+        import scipy.sparse.linalg as sla
+
+        h0 = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=50)
+        rp, ci, v = h0.level_csr(0)
+        A = sp.csr_matrix((v, ci, rp))
+        lmax = sla.eigsh(A, k=1, which="LA", return_eigenvectors=False)[0]
+        t = oracle_mod.lanczos_max(rp, ci, v, 10)
+        assert t <= lmax * (1 + 1e-12) and 1.1 * t >= lmax
+        h = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=50, lanczos=10)
+        assert h.level_info(0)["lambda1"] == pytest.approx(min(h0.level_info(0)["lambda1"], 1.1 * t), rel=1e-15)
+        assert h.level_info(0)["lambda1"] >= lmax
