@@ -422,6 +422,105 @@ static void opass_graph0(const ocsr *A, const int32_t *blk, ocsr *G) {
     G->rp[n] = nnz;
 }
 
+/* ===================================================== MIS-k aggregation (A25) */
+/* The paper's own partitioner, reading A25:
+ *  (A) S = the maximal independent set of the graph of A^k (vertices at graph distance <= k are
+ *      adjacent) chosen greedily by decreasing key: v joins S iff no vertex of S with a larger key is
+ *      within distance k.  key(v) = (hi32(splitmix64(v ^ misalt)) << 32) | v, misalt =
+ *      splitmix64(seed ^ 0x4D49530000000000 ^ level) (distinct keys: v breaks ties).
+ *  (B) "collecting vertices and edges of the neighbors of vertices in S", layer by layer: every S
+ *      vertex roots its aggregate (layer 0); in layer d = 1..k every vertex not yet assigned takes,
+ *      among its neighbours assigned in layers < d, the root with the largest key.  By maximality of S
+ *      every vertex is assigned after k layers; aggregates are connected (each vertex joins through
+ *      a neighbour of its own aggregate).  Aggregate id = rank of its root in increasing vertex order.
+ * G is the level's pass graph G_0 (off-diagonal pattern). */
+static uint64_t omis_key(int64_t v, uint64_t misalt) {
+    return ((osm64((uint64_t)v ^ misalt) >> 32) << 32) | (uint64_t)(uint32_t)v;
+}
+
+static int64_t omis_aggregate(const ocsr *G, int k, uint64_t seed, int level, int32_t *agg, int8_t *roots_out);
+int64_t orc_mis_aggregate(const ocsr *G, int k, uint64_t seed, int level, int32_t *agg) {
+    return omis_aggregate(G, k, seed, level, agg, NULL);
+}
+static int64_t omis_aggregate(const ocsr *G, int k, uint64_t seed, int level, int32_t *agg, int8_t *roots_out) {
+    int64_t n = G->n;
+    uint64_t misalt = osm64(seed ^ 0x4D49530000000000ULL ^ (uint64_t)level);
+    uint64_t *key = malloc(sizeof(uint64_t) * (n ? n : 1));
+    int64_t *order = malloc(sizeof(int64_t) * (n ? n : 1));
+    for (int64_t v = 0; v < n; ++v) { key[v] = omis_key(v, misalt); order[v] = v; }
+    /* sort vertices by decreasing key (insertion into a heap-free merge: plain qsort with keys) */
+    for (int64_t w = 1; w < n; w *= 2) { /* bottom-up merge sort, descending key */
+        int64_t *tmp = malloc(sizeof(int64_t) * n);
+        for (int64_t lo = 0; lo < n; lo += 2 * w) {
+            int64_t mid = lo + w < n ? lo + w : n, hi = lo + 2 * w < n ? lo + 2 * w : n, a = lo, b = mid, o = lo;
+            while (a < mid && b < hi) tmp[o++] = key[order[a]] > key[order[b]] ? order[a++] : order[b++];
+            while (a < mid) tmp[o++] = order[a++];
+            while (b < hi) tmp[o++] = order[b++];
+        }
+        memcpy(order, tmp, sizeof(int64_t) * n);
+        free(tmp);
+    }
+    char *inS = calloc((size_t)n + 1, 1);
+    int64_t *dist = malloc(sizeof(int64_t) * (n ? n : 1)), *queue = malloc(sizeof(int64_t) * (n ? n : 1));
+    for (int64_t v = 0; v < n; ++v) dist[v] = -1;
+    for (int64_t t = 0; t < n; ++t) { /* (A): greedy by decreasing key; BFS of depth k from v */
+        int64_t v = order[t], qh = 0, qt = 0;
+        int blocked = 0;
+        queue[qt++] = v;
+        dist[v] = 0;
+        while (qh < qt && !blocked) {
+            int64_t u = queue[qh++];
+            if (inS[u]) { blocked = 1; break; }
+            if (dist[u] == k) continue;
+            for (int64_t p = G->rp[u]; p < G->rp[u + 1]; ++p) {
+                int64_t x = G->ci[p];
+                if (dist[x] < 0) { dist[x] = dist[u] + 1; queue[qt++] = x; }
+            }
+        }
+        for (int64_t q = 0; q < qt; ++q) dist[queue[q]] = -1;
+        if (!blocked) inS[v] = 1;
+    }
+    /* (B): layered growth */
+    int64_t *root = malloc(sizeof(int64_t) * (n ? n : 1)), *nroot = malloc(sizeof(int64_t) * (n ? n : 1));
+    for (int64_t v = 0; v < n; ++v) root[v] = inS[v] ? v : -1;
+    for (int d = 1; d <= k; ++d) {
+        for (int64_t v = 0; v < n; ++v) {
+            nroot[v] = root[v];
+            if (root[v] >= 0) continue;
+            int64_t best = -1;
+            for (int64_t p = G->rp[v]; p < G->rp[v + 1]; ++p) {
+                int64_t r = root[G->ci[p]];
+                if (r >= 0 && (best < 0 || key[r] > key[best])) best = r;
+            }
+            nroot[v] = best;
+        }
+        memcpy(root, nroot, sizeof(int64_t) * n);
+    }
+    if (roots_out) for (int64_t v = 0; v < n; ++v) roots_out[v] = inS[v];
+    int64_t nc = 0;
+    int32_t *id = malloc(sizeof(int32_t) * (n ? n : 1));
+    for (int64_t v = 0; v < n; ++v) id[v] = inS[v] ? (int32_t)nc++ : -1;
+    int64_t ok = nc;
+    for (int64_t v = 0; v < n; ++v) {
+        if (root[v] < 0) { ok = -1; agg[v] = -1; continue; } /* unreachable by maximality */
+        agg[v] = id[root[v]];
+    }
+    free(key); free(order); free(inS); free(dist); free(queue); free(root); free(nroot); free(id);
+    return ok;
+}
+
+/* test hook: MIS-k aggregation of a CSR pattern (off-diagonals) */
+int64_t orc_mis_aggregate_csr(int64_t n, const int64_t *rp, const int32_t *ci, int k, uint64_t seed, int level,
+                              int32_t *agg, int8_t *roots) {
+    ocsr A = {n, rp[n], (int64_t *)rp, (int32_t *)ci, NULL, NULL}, G;
+    int32_t *blk = calloc((size_t)n + 1, sizeof(int32_t));
+    opass_graph0(&A, blk, &G);
+    int64_t nc = omis_aggregate(&G, k, seed, level, agg, roots);
+    ocsr_free(&G);
+    free(blk);
+    return nc;
+}
+
 /* ================================================================ hierarchy */
 typedef struct {
     ocsr A;
@@ -441,6 +540,7 @@ typedef struct {
     int restart, max_iter, rule, cycle, nparts;
     double amli_kappa; /* cycle 2: 1/theta of the AMLI polynomial interval; 0 = reading A23 */
     int lanczos;       /* reading A24: k Lanczos steps for lambda_1 (0 = ||A||_inf, the paper's) */
+    int mis_k;         /* reading A25: 0 = repeated pairwise matching (A1-A5); k > 0 = MIS of A^k */
     int64_t gather_rows;
     uint64_t seed;
     olevel lev[ORC_MAXLEV];
@@ -511,7 +611,7 @@ static int oform_A0(int64_t n, const int64_t *rp, const int32_t *ci, const doubl
             if (ci[p] < 0 || ci[p] >= n) return ORC_E_INPUT;
             if (p > rp[i] && ci[p] <= ci[p - 1]) return ORC_E_INPUT;
             if (ci[p] == i) { has_diag = 1; dv = val[p]; continue; }
-            if (!(val[p] < 0.0)) return ORC_E_INPUT;
+            if (!(val[p] <= 0.0)) return ORC_E_INPUT; /* weights w_e >= 0: structural zeros allowed (A17) */
             off += -val[p];
             /* symmetry: (j,i) stored with equal value */
             int64_t j = ci[p], lo = rp[j], hi = rp[j + 1], f = -1;
@@ -563,6 +663,7 @@ void orc_free(orc_h *h) {
 }
 
 static int orc_get_lanczos(void);
+static int orc_get_mis_k(void);
 
 /* Setup: level loop while n_l > coarsest_size:
  * lambda_1, kappa rule (A8), coefficients, p matching passes composed
@@ -580,6 +681,7 @@ int orc_setup(int64_t n, const int64_t *rp, const int32_t *ci, const double *val
     h->restart = restart; h->max_iter = max_iter; h->seed = seed; h->nparts = nparts;
     h->gather_rows = gather_rows; h->rule = rule; h->cycle = cycle;
     h->lanczos = orc_get_lanczos();
+    h->mis_k = orc_get_mis_k();
     int st = oform_A0(n, rp, ci, val, d, &h->lev[0].A);
     if (st) { free(h); return st; }
     h->singular = 1;
@@ -611,7 +713,15 @@ int orc_setup(int64_t n, const int64_t *rp, const int32_t *ci, const double *val
         int32_t *gblk = malloc(sizeof(int32_t) * L->A.n);
         for (int64_t i = 0; i < L->A.n; ++i) { agg[i] = (int32_t)i; gblk[i] = L->blk[i]; }
         int64_t nc = L->A.n;
-        for (int t = 0; t < passes; ++t) {
+        if (h->mis_k > 0) { /* reading A25: one MIS-k aggregation replaces the matching passes */
+            int64_t ncm = orc_mis_aggregate(&G, h->mis_k, seed, l, agg);
+            if (ncm < 0) { ocsr_free(&G); free(agg); free(gblk); orc_free(h); return ORC_E_SETUP; }
+            int32_t *nblk = malloc(sizeof(int32_t) * (ncm ? ncm : 1));
+            for (int64_t v = 0; v < L->A.n; ++v) nblk[agg[v]] = gblk[v];
+            free(gblk); gblk = nblk;
+            nc = ncm;
+        }
+        for (int t = 0; t < (h->mis_k > 0 ? 0 : passes); ++t) {
             int32_t *aggt = malloc(sizeof(int32_t) * (G.n ? G.n : 1));
             int64_t nct;
             uint64_t salt = osalt(seed, l, t);
@@ -742,8 +852,21 @@ static void oB(const orc_h *h, int l, int nu, const double *r, double *x) {
     free(zero); free(t); free(rH); free(eH);
 }
 
+static const double *orc_get_xstar(void);
+/* ||x - x*||_A = sqrt((x - x*)^T A (x - x*)) */
+static double oanorm_err(const ocsr *A, const double *x, const double *xs) {
+    int64_t n = A->n;
+    double *e = malloc(sizeof(double) * n), *t = malloc(sizeof(double) * n);
+    for (int64_t i = 0; i < n; ++i) e[i] = x[i] - xs[i];
+    ospmv(A, e, t);
+    double v = odot(n, e, t);
+    free(e); free(t);
+    return sqrt(v > 0.0 ? v : 0.0);
+}
+
 /* Outer flexible CG (P:322-323 restart every 5; stopping
- * reading A14: ||r|| <= tol ||b|| on the recursive residual). */
+ * reading A14: ||r|| <= tol ||b|| on the recursive residual; or, when an exact solution x* is set
+ * (orc_set_xstar), the paper's rule: ||x - x*||_A <= tol ||x_0 - x*||_A). */
 int orc_solve(const orc_h *h, const double *b_in, double *x, double tol, int nu,
               int *iters_out, double *relres_out, double *true_relres_out) {
     if (!h || !(tol > 0.0) || nu < 1) return ORC_E_ARG;
@@ -761,6 +884,8 @@ int orc_solve(const orc_h *h, const double *b_in, double *x, double tol, int nu,
         for (int64_t i = 0; i < n; ++i) b[i] -= mu;
     }
     double bnorm = sqrt(odot(n, b, b));
+    const double *xstar = orc_get_xstar();
+    double e0A = xstar ? oanorm_err(A, x, xstar) : 0.0;
     int status = ORC_NOT_CONVERGED, k = 0, w = 0;
     if (bnorm == 0.0) {
         for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
@@ -769,7 +894,10 @@ int orc_solve(const orc_h *h, const double *b_in, double *x, double tol, int nu,
         ospmv(A, x, t);
         for (int64_t i = 0; i < n; ++i) r[i] = b[i] - t[i];
         for (k = 0;; ++k) {
-            if (sqrt(odot(n, r, r)) <= tol * bnorm) { status = ORC_OK; break; }
+            if (xstar ? oanorm_err(A, x, xstar) <= tol * e0A : sqrt(odot(n, r, r)) <= tol * bnorm) {
+                status = ORC_OK;
+                break;
+            }
             if (k >= h->max_iter) break;
             oB(h, 0, nu, r, z);
             if (h->singular) {
@@ -811,6 +939,13 @@ int orc_num_levels(const orc_h *h) { return h->nlev; }
 /* reading A24: k Lanczos steps for lambda_1 in subsequent orc_setup calls of this thread (0 = off) */
 static _Thread_local int g_lanczos = 0;
 void orc_set_lanczos(int k) { g_lanczos = k; }
+/* reading A25: MIS-k aggregation in subsequent orc_setup calls of this thread (0 = matching) */
+static _Thread_local int g_mis_k = 0;
+void orc_set_mis_k(int k) { g_mis_k = k; }
+/* A-norm stopping (the paper's protocol): when set, orc_solve stops on
+ * ||x - x*||_A <= tol ||x_0 - x*||_A instead of the residual (reading A14) */
+static _Thread_local const double *g_xstar = NULL;
+void orc_set_xstar(const double *xs) { g_xstar = xs; }
 /* cycle 2 (stationary AMLI): 1/theta of the coarse polynomial interval (0 = reading A23) */
 void orc_set_amli_kappa(orc_h *h, double kappa) { h->amli_kappa = kappa; }
 int orc_is_singular(const orc_h *h) { return h->singular; }
@@ -926,3 +1061,5 @@ void orc_csr_free(void *H) {
 }
 
 static int orc_get_lanczos(void) { return g_lanczos; }
+static int orc_get_mis_k(void) { return g_mis_k; }
+static const double *orc_get_xstar(void) { return g_xstar; }

@@ -46,6 +46,9 @@ def _L():
         "orc_num_levels": (i32, [vp]),
         "orc_set_amli_kappa": (None, [vp, dbl]),
         "orc_set_lanczos": (None, [i32]),
+        "orc_set_mis_k": (None, [i32]),
+        "orc_set_xstar": (None, [vp]),
+        "orc_mis_aggregate_csr": (i64, [i64, vp, vp, i32, u64, i32, vp, vp]),
         "orc_lanczos_max": (dbl, [i64, vp, vp, vp, i32, u64, i32]),
         "orc_is_singular": (i32, [vp]),
         "orc_level_info": (None, [vp, i32, vp, vp, vp, vp, vp, vp]),
@@ -134,6 +137,15 @@ def aggregate_pass(rp, ci, w, seed=0, level=0, pass_=0, rule=0):
     return agg, int(nc)
 
 
+def mis_aggregate(rp, ci, k, seed=0, level=0):
+    """MIS-k aggregation of a CSR pattern (reading A25); returns (agg, nc, roots)."""
+    rp, ci = _c(rp, np.int64), _c(ci, np.int32)
+    agg = np.empty(len(rp) - 1, np.int32)
+    roots = np.zeros(len(rp) - 1, np.int8)
+    nc = _L().orc_mis_aggregate_csr(len(rp) - 1, _p(rp), _p(ci), k, seed, level, _p(agg), _p(roots))
+    return agg, int(nc), roots.astype(bool)
+
+
 def lanczos_max(rp, ci, v, k, seed=0, level=0) -> float:
     """Largest Ritz value of k Lanczos steps from the counter-based start vector (reading A24)."""
     rp, ci, v = _c(rp, np.int64), _c(ci, np.int32), _c(v, np.float64)
@@ -171,17 +183,20 @@ class Hierarchy:
     """Oracle setup + solve (O5-O8)."""
 
     def __init__(self, rp, ci, val, d, passes, degree, coarsest_size=100, kappa=0.0, restart=5,
-                 max_iter=500, seed=0, nparts=1, gather_rows=0, rule=0, cycle=0, amli_kappa=0.0, lanczos=0):
+                 max_iter=500, seed=0, nparts=1, gather_rows=0, rule=0, cycle=0, amli_kappa=0.0, lanczos=0,
+                 mis_k=0):
         self._keep = [_c(rp, np.int64), _c(ci, np.int32), _c(val, np.float64), _c(d, np.float64)]
         rp, ci, val, d = self._keep
         self.m = degree
         self.passes = passes
         h = vp()
         _L().orc_set_lanczos(int(lanczos))
+        _L().orc_set_mis_k(int(mis_k))
         st = _L().orc_setup(len(rp) - 1, _p(rp), _p(ci), _p(val), _p(d), passes, degree, coarsest_size, kappa,
                             restart, max_iter, seed, nparts, gather_rows, rule, cycle, ctypes.byref(h))
         self._keep = None
         _L().orc_set_lanczos(0)
+        _L().orc_set_mis_k(0)
         if st != 0:
             raise OracleError(st)
         self.h = h
@@ -248,11 +263,17 @@ class Hierarchy:
         _L().orc_coarse_solve(self.h, _p(r), _p(e))
         return e
 
-    def solve(self, b, x0=None, tol=1e-8, nu=2):
+    def solve(self, b, x0=None, tol=1e-8, nu=2, xstar=None):
+        """xstar given: stop on the paper's relative A-norm error reduction."""
         b = _c(b, np.float64)
         x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
         it, rr, trr = i32(), dbl(), dbl()
-        st = _L().orc_solve(self.h, _p(b), _p(x), tol, nu, ctypes.byref(it), ctypes.byref(rr), ctypes.byref(trr))
+        xs = _c(xstar, np.float64)
+        _L().orc_set_xstar(_p(xs))
+        try:
+            st = _L().orc_solve(self.h, _p(b), _p(x), tol, nu, ctypes.byref(it), ctypes.byref(rr), ctypes.byref(trr))
+        finally:
+            _L().orc_set_xstar(None)
         return dict(status=st, x=x, iters=it.value, relres=rr.value, true_relres=trr.value)
 
     def complexities(self):
@@ -265,5 +286,5 @@ def setup_problem(prob, **over) -> Hierarchy:
     p = dict(prob.params)
     p.update(over)
     kw = {k: p[k] for k in ("coarsest_size", "kappa", "restart", "max_iter", "seed", "nparts", "gather_rows",
-                            "rule", "cycle", "amli_kappa", "lanczos") if k in p}
+                            "rule", "cycle", "amli_kappa", "lanczos", "mis_k") if k in p}
     return Hierarchy(prob.rp, prob.ci, prob.val, prob.d, p["passes"], p["degree"], **kw)

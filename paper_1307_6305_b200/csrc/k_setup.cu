@@ -109,7 +109,7 @@ __global__ void k_validate(int n, int cmin, int cmax, const int64_t* __restrict_
             if (c < cmin || c >= cmax) { f |= VF_RANGE; continue; }
             if (p > p0 && c <= ci[p - 1]) f |= VF_UNSORTED;
             if (c == i) { has = true; dv = v[p]; continue; }
-            if (!(v[p] < 0.0)) f |= VF_POSOFF;
+            if (!(v[p] <= 0.0)) f |= VF_POSOFF;  // weights w_e >= 0 (structural zeros allowed, A17)
             off += -v[p];
             if (c < 0 || c >= n) continue;
             int64_t lo = rp[c], hi = rp[c + 1];

@@ -429,3 +429,41 @@ def test_lanczos_lambda_parity(amg, gen_mod, oracle_mod, name):
         assert st == 0 and abs(it - oref["iters"]) <= 1, (it, oref["iters"])
     finally:
         amg.amg_free(h)
+
+
+def test_structural_zeros_fe_pattern(amg, oracle_mod):
+    """A P1-FE pattern with structural zeros (hypotenuse couplings of the right-triangle mesh, A17) is
+    accepted; hierarchy bit-exact and B_0(r) <= 1e-10 against the oracle."""
+    N = 48
+    n = N * N
+    rows = []
+    for y in range(N):
+        for x in range(N):
+            i = y * N + x
+            nb = [(i - 1, -1.0)] * (x > 0) + [(i + 1, -1.0)] * (x < N - 1) + [(i - N, -1.0)] * (y > 0) + \
+                [(i + N, -1.0)] * (y < N - 1) + [(i - N - 1, 0.0)] * (x > 0 and y > 0) + \
+                [(i + N + 1, 0.0)] * (x < N - 1 and y < N - 1)
+            rows.append(sorted(nb + [(i, -sum(v for _, v in nb) + (1.0 if x == 0 else 0.0))]))
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.array([c for r in rows for c, _ in r], np.int32)
+    v = np.array([w for r in rows for _, w in r])
+    d = np.zeros(n)
+    # the Dirichlet-like term added to the x = 0 diagonals above goes into d instead (Eq. (prob))
+    for y in range(N):
+        i = y * N
+        d[i] = 1.0
+        for p in range(rp[i], rp[i + 1]):
+            if ci[p] == i:
+                v[p] -= 1.0
+    hier = oracle_mod.Hierarchy(rp, ci, v, d, 2, 3, coarsest_size=40)
+    h = amg.amg_setup(rp, ci, v, d, 2, 3, amg.amg_options_default(coarsest_size=40))
+    try:
+        compare_hierarchy(amg, h, hier, 3, exact_values=True)
+        r = np.random.default_rng(0).uniform(-1, 1, n)
+        z = np.empty(n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        ref = hier.precond(r, nu=2, level=0)
+        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+    finally:
+        amg.amg_free(h)

@@ -647,3 +647,90 @@ def test_lanczos_lambda_max_pins(oracle_mod, gen_mod):
         h = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=50, lanczos=10)
         assert h.level_info(0)["lambda1"] == pytest.approx(min(h0.level_info(0)["lambda1"], 1.1 * t), rel=1e-15)
         assert h.level_info(0)["lambda1"] >= lmax
+
+
+def _bfs_dist(rp, ci, src, n):
+    d = np.full(n, -1)
+    d[src] = 0
+    q = [src]
+    for u in q:
+        for p in range(rp[u], rp[u + 1]):
+            x = ci[p]
+            if x != u and d[x] < 0:
+                d[x] = d[u] + 1
+                q.append(x)
+    return d
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_mis_aggregation_pins(oracle_mod, gen_mod, k):
+    """Reading A25 (the paper's partitioner; NEXT row f2, oracle only): the roots are an
+    independent set of the graph of A^k (pairwise distance > k) that is maximal (every vertex within
+    distance k of a root) and greedy by key; every vertex is assigned to a root at its distance to the
+    root set (the BFS layer), aggregates are connected and numbered by root order."""
+    for p in (gen_mod.problem("C1", size=20), gen_mod.random_graph(300, 5, seed=8)):
+        n = p.n
+        agg, nc, roots = oracle_mod.mis_aggregate(p.rp, p.ci, k, seed=3, level=1)
+        assert nc > 0 and agg.min() == 0 and agg.max() == nc - 1
+        dist = np.array([_bfs_dist(p.rp, p.ci, v, n) for v in range(n)])  # all-pairs hop distances
+        dist = np.where(dist < 0, 10 ** 9, dist)
+        S = np.flatnonzero(roots)
+        assert len(S) == nc and np.array_equal(agg[S], np.arange(nc))  # numbered by root order
+        DS = dist[:, S]
+        for a in range(len(S)):
+            for b in range(a + 1, len(S)):
+                assert DS[S[a], b] > k, "roots within distance k"
+        assert np.all(DS.min(axis=1) <= k), "not maximal"
+        # greedy by key (reading A25): v is a root iff no root with a larger key lies within distance k
+        misalt = H.splitmix64((3 ^ 0x4D49530000000000 ^ 1) & (2 ** 64 - 1))
+        key = np.array([((H.splitmix64(v ^ misalt) >> 32) << 32) | v for v in range(n)], dtype=object)
+        for v in range(n):
+            near = [u for u in S if dist[v, u] <= k and u != v]
+            assert roots[v] == all(key[u] < key[v] for u in near)
+        for v in range(n):  # assigned to a root at the vertex's distance to the root set (its layer)
+            assert DS[v, agg[v]] == DS[v].min()
+        for I in range(nc):  # connected
+            mem = np.flatnonzero(agg == I)
+            sub = set(mem.tolist())
+            seen, stack = {mem[0]}, [mem[0]]
+            while stack:
+                u = stack.pop()
+                for pp in range(p.rp[u], p.rp[u + 1]):
+                    x = p.ci[pp]
+                    if x in sub and x not in seen:
+                        seen.add(x)
+                        stack.append(x)
+            assert len(seen) == len(mem)
+
+
+def test_mis_hierarchy_paper_protocol(oracle_mod):
+    """The paper's protocol on the P1-FE pattern of a 128^2 Neumann problem (structural zeros on the
+    hypotenuse couplings kept, A17): MIS on A^4 coarsens by ~30 with complexities near the
+    paper's, and both cycles converge under the A-norm error stop."""
+    N = 128
+    n = N * N
+    rows = []
+    for y in range(N):
+        for x in range(N):
+            i = y * N + x
+            nb = [(i - 1, -1.0)] * (x > 0) + [(i + 1, -1.0)] * (x < N - 1) + [(i - N, -1.0)] * (y > 0) + \
+                [(i + N, -1.0)] * (y < N - 1) + [(i - N - 1, 0.0)] * (x > 0 and y > 0) + \
+                [(i + N + 1, 0.0)] * (x < N - 1 and y < N - 1)
+            rows.append(sorted(nb + [(i, -sum(v for _, v in nb))]))
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.array([c for r in rows for c, _ in r], np.int32)
+    v = np.array([w for r in rows for _, w in r])
+    h = oracle_mod.Hierarchy(rp, ci, v, None, 1, 4, coarsest_size=99, mis_k=4)
+    cf = h.level_info(0)["n"] / h.level_info(1)["n"]
+    gc, oc = h.complexities()
+    assert 25 < cf < 35 and gc < 1.05 and oc < 1.05
+    import scipy.sparse as sp
+
+    xs = np.random.default_rng(0).standard_normal(n)
+    xs -= xs.mean()
+    b = sp.csr_matrix((v, ci, rp)) @ xs
+    for cyc in (0, 2):
+        hc = oracle_mod.Hierarchy(rp, ci, v, None, 1, 4, coarsest_size=99, mis_k=4, cycle=cyc)
+        r = hc.solve(b, tol=1e-8, nu=2, xstar=xs)
+        assert r["status"] == 0 and r["iters"] <= 40
