@@ -57,6 +57,7 @@ struct Sell {          // SELL-32: 32-row slices, entries column-major inside a 
     // slices while the halo is in flight, then the boundary slices): sptr/nslices describe the
     // view's slices and srow0 is the absolute first row of its first slice (0 for the whole level)
     int srow0 = 0;
+    int maxoff = 0;        // max |col - row| over the stored entries (halo of the fused step pair)
     // lossless compressed streams (same slice layout), chosen per level at setup:
     int vmode = 0;         // 0: val (fp64); 1: vcode (uint8) into vdict (<= 256 distinct values)
     int cmode = 0;         // 0: col (int32); 1: ccode (uint8) into cdict of offsets col-row; 2: coff (int16 col-row);
@@ -105,6 +106,8 @@ Csr form_A0(int n, const int64_t* rp, const int32_t* ci, const double* v, const 
 double inf_norm(const Csr& A, cudaStream_t s);
 // true if some d_i != 0
 bool any_nonzero(int n, const double* d, cudaStream_t s);
+// max |col - row| over the stored entries (0 if only a diagonal)
+int max_col_offset(const Csr& A, cudaStream_t s);
 // Lanczos start vector of reading A24: out_i = 2 U(z ^ i) - 1, U(y) = (splitmix64(y) >> 11) 2^-53
 void launch_lanczos_start(int n, uint64_t z, double* out, cudaStream_t s);
 
@@ -154,6 +157,11 @@ extern thread_local long long g_launches;
 //          prev_i = xprev ? xprev_i : cp*f_i          (three-term recurrence step)
 void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f, const double* xprev,
                    double cp, double alpha, double beta, double* out, cudaStream_t s);
+//  two consecutive general steps in one launch (x_{k+1} into out1, x_{k+2} into out2; out2 may alias xk,
+//  out1 may alias xkm1); flags [>= slices/8 + 1] and sync [3] are zero-initialised level scratch.
+//  Returns false (nothing launched) when the level is not eligible.
+bool launch_smooth2(const SpOp& op, const double* xk, const double* xkm1, const double* f, double* out1, double* out2,
+                    double a1, double b1, double a2, double b2, int* flags, int* sync, cudaStream_t s);
 //  resid: out = f - A xg; optional dot r.r into dots[0]
 void launch_resid(const SpOp& op, const double* xg, const double* f, double* out, double* dot_rr,
                   const DotScratch& ds, cudaStream_t s);

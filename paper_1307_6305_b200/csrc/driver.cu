@@ -380,6 +380,14 @@ void amg::finish_build(amg_hierarchy* h) {
         Lv.op.S = Lv.S;
         Lv.op.sell = Lv.S.sptr != nullptr;
         if (Lv.dist) build_split(h, k);
+        if (Lv.op.sell && !Lv.dist && k < h->L - 1) {  // fused step pairs (k_smooth2_tma) scratch
+            Lv.S.maxoff = Lv.op.S.maxoff = max_col_offset(Lv.A, s);
+            const size_t nf = (size_t)Lv.S.nslices / 8 + 2;
+            Lv.fflags = halloc<int>(h, nf);
+            Lv.fsync = halloc<int>(h, 4);
+            CK(cudaMemsetAsync(Lv.fflags, 0, sizeof(int) * nf, s));
+            CK(cudaMemsetAsync(Lv.fsync, 0, sizeof(int) * 4, s));
+        }
         // vector layout [pad | lower halo | own | upper halo]
         Lv.lo_pad = (Lv.H.nlo + 3) & ~3;
         Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : Lv.A.n;
@@ -669,6 +677,49 @@ static void amli_correction(amg_hierarchy* h, int l, int nu) {
     if (cur != Lv.E) launch_copy(n, cur, Lv.E, s);
 }
 
+// A chain of general smoothing steps x_out = a x_g + (1 - a) x_prev + b (f - A x_g) on level l, each the
+// next one's x_prev / x_g.  Consecutive pairs are fused into one launch (k_smooth2_tma: the matrix
+// and f stream from HBM once per pair) on a non-partitioned level when eligible.  When `prof`, the
+// algorithmic bytes and launches are added to the live-profile window counters.
+struct SmStep {
+    const double* xg;
+    const double* xprev;
+    double a, b;
+    double* out;
+};
+static int64_t smoother_bytes(const Level& Lv);
+static int64_t pair_bytes(const Level& Lv) {  // fused pair: codes once, x_k, x_{k-1}, f read, 2 writes
+    const int64_t n = Lv.A.n;
+    return smoother_bytes(Lv) - 32 * n + 40 * n;
+}
+static void run_steps(amg_hierarchy* h, int l, const double* f, const std::vector<SmStep>& st, bool prof) {
+    Level& Lv = h->lev[l];
+    for (size_t q = 0; q < st.size();) {
+        const SmStep& s1 = st[q];
+        if (q + 1 < st.size() && !Lv.dist && Lv.fflags) {
+            const SmStep& s2 = st[q + 1];
+            if (s2.xg == s1.out && s2.xprev == s1.xg &&
+                launch_smooth2(Lv.op, s1.xg, s1.xprev, f, s1.out, s2.out, s1.a, s1.b, s2.a, s2.b, Lv.fflags, Lv.fsync,
+                               h->s)) {
+                if (prof) {
+                    h->prof_win_bytes += pair_bytes(Lv);
+                    h->prof_win_launches += 1;
+                }
+                q += 2;
+                continue;
+            }
+        }
+        spmv_pass(h, l, const_cast<double*>(s1.xg), [&](const SpOp& op, int) {
+            launch_smooth(op, s1.xg, 1.0, f, s1.xprev, 0.0, s1.a, s1.b, s1.out, h->s);
+        });
+        if (prof) {
+            h->prof_win_bytes += smoother_bytes(Lv);
+            h->prof_win_launches += 1;
+        }
+        ++q;
+    }
+}
+
 // z = B_l(r): pre-smoothing from 0, residual, restriction, coarse correction,
 // prolongation, post-smoothing; the last smoothing step writes `out` (distinct from rin and the
 // level buffers).  `rin` must be a vector of level l's layout (it is the first step's SpMV input).
@@ -698,12 +749,12 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
         });
         cur = Lv.XA;
         prev = Lv.X;
+        std::vector<SmStep> st;
         for (int k = 3; k <= m; ++k) {
-            spmv_pass(h, l, cur, [&](const SpOp& op, int) {
-                launch_smooth(op, cur, 1.0, rin, prev, 0.0, a[k], b[k], prev, s);
-            });
+            st.push_back({cur, prev, a[k], b[k], prev});
             std::swap(cur, prev);
         }
+        run_steps(h, l, rin, st, false);
     }
     // residual + restriction
     spmv_pass(h, l, cur, [&](const SpOp& op, int) { launch_resid(op, cur, rin, Lv.RES, nullptr, h->ds, s); });
@@ -724,21 +775,24 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
     // post-smoothing S(r, x): x_{-1} = x_0 = cur
     double* other = (cur == Lv.X) ? Lv.XA : Lv.X;
-    spmv_pass(h, l, cur, [&](const SpOp& op, int) {
-        launch_smooth(op, cur, 1.0, rin, cur, 0.0, 1.0, b[0], other, s);  // k = 0
-    });
+    std::vector<SmStep> st;
+    st.push_back({cur, cur, 1.0, b[0], other});  // k = 0
     prev = cur;
     cur = other;
-    const bool prof = (l == 0 && h->prof_on);
-    if (prof) record_event(h->pe0, s);
     for (int k = 1; k <= m; ++k) {
         double* target = (k == m) ? out : prev;
-        spmv_pass(h, l, cur, [&](const SpOp& op, int) {
-            launch_smooth(op, cur, 1.0, rin, prev, 0.0, a[k], b[k], target, s);
-        });
+        st.push_back({cur, prev, a[k], b[k], target});
         prev = cur;
         cur = target;
     }
+    // live profile of the dominant kernel: the level-0 post-smoothing launches (all m+1 steps)
+    const bool prof = (l == 0 && h->prof_on);
+    if (prof) {
+        h->prof_win_bytes = 0;
+        h->prof_win_launches = 0;
+        record_event(h->pe0, s);
+    }
+    run_steps(h, l, rin, st, prof);
     if (prof) record_event(h->pe1, s);
 }
 
@@ -859,7 +913,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     int status = AMG_NOT_CONVERGED, k = 0;
     long long graph_runs = 0;
     double prof_ms = 0.0;
-    int64_t prof_n = 0;
+    int64_t prof_n = 0, prof_bytes = 0;
     if (bnorm == 0.0) {
         CK(cudaMemsetAsync(h->x, 0, sizeof(double) * n, s));
         status = AMG_OK;
@@ -884,7 +938,8 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
                 float pm = 0.f;
                 CK(cudaEventElapsedTime(&pm, h->pe0, h->pe1));
                 prof_ms += pm;
-                prof_n += h->m;
+                prof_n += h->prof_win_launches;
+                prof_bytes += h->prof_win_bytes;
             }
             if (fl) { status = AMG_E_BREAKDOWN; ++k; break; }
             rnorm = std::sqrt(h->hsc[0]);
@@ -910,7 +965,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     h->info.launches_per_iter = h->graph_launches;
     h->info.prof_smoother_ms = prof_ms;
     h->info.prof_smoother_launches = prof_n;
-    h->info.prof_smoother_bytes = smoother_bytes(h->lev[0]);
+    h->info.prof_smoother_bytes = prof_n ? prof_bytes / prof_n : smoother_bytes(h->lev[0]);
     if (h->user) {  // order the caller's stream after this call's work
         CK(cudaEventRecord(h->e1, s));
         CK(cudaStreamWaitEvent(h->user, h->e1, 0));

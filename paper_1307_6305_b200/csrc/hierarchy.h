@@ -61,6 +61,8 @@ struct Level {
     // is in flight; the boundary slices (the ranges around it) after it has arrived
     bool split = false;
     SpOp op_int, op_lo, op_hi;   // slice views: interior, boundary before it, boundary after it
+    int* fflags = nullptr;       // fused step-pair scratch (k_smooth2_tma): per-chunk epochs, sync words
+    int* fsync = nullptr;
     int ld = 0;                  // vector slot stride (lo_pad + n + nhi, rounded up to 4)
 };
 
@@ -93,6 +95,8 @@ struct amg_hierarchy {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaEvent_t pe0 = nullptr, pe1 = nullptr;  // live profile of the level-0 smoother steps
     bool prof_on = false;
+    int64_t prof_win_bytes = 0;      // algorithmic bytes / launches inside the live-profile window
+    int64_t prof_win_launches = 0;
     int64_t bytes = 0;
     amg_info info{};
     // distributed handle (amg_setup_dist); comm == nullptr on one GPU

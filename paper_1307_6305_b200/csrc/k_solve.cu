@@ -1020,6 +1020,262 @@ static bool tma_enabled() {
     return on == 1;
 }
 
+// ------------------------------------------------------------------ two fused smoother steps
+// Two consecutive general three-term steps in ONE launch ("fused step pair"):
+//   stage 1: x_{k+1} = a1 x_k + (1 - a1) x_{k-1} + b1 (f - A x_k)        -> out1
+//   stage 2: x_{k+2} = a2 x_{k+1} + (1 - a2) x_k + b2 (f - A x_{k+1})    -> out2
+// Every CTA walks its chunks c_j = blockIdx + j G and, right after stage 1 of c_j, runs stage 2 of
+// c_{j-1}.  Stage 2 of chunk c needs x_{k+1} on the chunks c-h..c+h (h covers the level's widest
+// column offset): the producer waits (acquire) on their stage-1 flags, which the CTAs release after
+// their stores.  Stage 2 then re-reads the chunk's codes, f, x_k and x_{k+1} while they are still in
+// L2, so the pair streams the matrix and f from HBM once instead of twice.  Lag 1 with G > h is
+// deadlock free: a waiting stage 2 depends only on stage-1 tasks that precede it in every CTA's
+// order, and those never wait.  Stage-2 gathers use L2-coherent loads (x_{k+1} is written in this
+// launch).  Flags carry a per-launch epoch kept on the device (graph replays stay correct); a spin
+// that exceeds its bound sets *err instead of hanging.
+struct Smooth2Args {
+    const double* xk;
+    const double* xkm1;
+    const double* f;
+    double* out1;
+    double* out2;
+    double a1, b1, a2, b2;
+    int* flags;       // [nchunks] stage-1 completion epochs
+    int* sync;        // [0] epoch of the last completed launch, [1] CTA ticket, [2] error flag
+    int halo;         // chunks
+    int lag;          // stage 2 runs `lag` chunks behind stage 1
+    int gnc;          // experiment: stage-2 gathers through the read-only path (AMG_FUSE2_NC)
+};
+
+__device__ __forceinline__ double ld_cg(const double* p) {
+    double r;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int r;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int VM, int CM, int W, int SPW, int NS>
+__global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth2_tma(Sell S, Smooth2Args a) {
+    using Lay = TmaLayout<VM, CM, W, SPW, NS>;
+    using St = TmaStreams<VM, CM>;
+    constexpr int CS = Lay::CS;
+    extern __shared__ __align__(128) unsigned char tsm[];
+    __shared__ double sv[VM ? 256 : 1];
+    __shared__ int sc[(CM == 1 || CM == 3) ? 256 : 1];
+    __shared__ int bnd[kBndRing * (CS + 1)];
+    uint64_t* full = reinterpret_cast<uint64_t*>(tsm + NS * Lay::STAGE);
+    uint64_t* empty = full + NS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < NS; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kTmaWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (VM == 1)
+        for (int k = threadIdx.x; k < S.nvdict; k += blockDim.x) sv[k] = S.vdict[k];
+    if constexpr (CM == 1 || CM == 3)
+        for (int k = threadIdx.x; k < S.ncdict; k += blockDim.x) sc[k] = S.cdict[k];
+    __syncthreads();
+    pdl_wait();
+    const int epoch = ld_acquire(a.sync) + 1;
+    const int nchunks = (S.nslices + CS - 1) / CS;
+    const int G = gridDim.x;
+    const int K = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / G + 1 : 0;
+    // tasks: S1(0..LG-1), then S1(j) S2(j-LG) pairs, then the last S2: stage 2 runs LG chunks behind
+    // stage 1 (beyond the NS-deep copy pipeline), so its flags are normally set when it is issued
+    const int LG = K < a.lag ? K : a.lag;
+    const int T = 2 * K;
+    auto task = [&](int t, int& stage, int& c) {
+        int j;
+        const int pb = LG + 2 * (K - LG);
+        if (t < LG) { stage = 1; j = t; }
+        else if (t < pb) {
+            const int u = t - LG;
+            stage = (u & 1) ? 2 : 1;
+            j = (u & 1) ? LG + (u >> 1) - LG : LG + (u >> 1);
+        } else { stage = 2; j = K - LG + (t - pb); }
+        c = blockIdx.x + j * G;
+    };
+    const unsigned char* gA = CM == 3 ? reinterpret_cast<const unsigned char*>(S.pcode)
+                                      : (VM == 0 ? reinterpret_cast<const unsigned char*>(S.val) : S.vcode);
+    const unsigned char* gB = CM == 0 ? reinterpret_cast<const unsigned char*>(S.col)
+                                      : (CM == 1 ? S.ccode : reinterpret_cast<const unsigned char*>(S.coff));
+    if (warp == kTmaWarps) {  // producer warp: lane 0 issues the copies, all lanes check the flags
+        auto fetch_bounds = [&](int t) {
+            if (t < T) {
+                int stg, c;
+                task(t, stg, c);
+                const int s0 = c * CS, s1 = min(s0 + CS, S.nslices);
+                int* dst = bnd + (t % kBndRing) * (CS + 1);
+                for (int q = 0; q <= CS; ++q)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + q)),
+                                 "l"(S.sptr + min(s0 + q, s1))
+                                 : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (lane == 0)
+            for (int t = 0; t < kBndAhead; ++t) fetch_bounds(t);
+        for (int t = 0; t < T; ++t) {
+            int stage, c;
+            task(t, stage, c);
+            if (stage == 2) {  // x_{k+1} of the chunks c-h..c+h must be final (32 flags per round trip)
+                const int lo = max(0, c - a.halo), hi = min(nchunks - 1, c + a.halo);
+                long long spins = 0;
+                for (;;) {
+                    bool ok = true;
+                    for (int q = lo + lane; q <= hi; q += 32) ok = ok && ld_acquire(a.flags + q) >= epoch;
+                    if (__all_sync(0xffffffffu, ok)) break;
+                    __nanosleep(100);
+                    if (++spins > (1LL << 25)) {  // bounded: flag the error, do not hang
+                        if (lane == 0) atomicExch(a.sync + 2, 1);
+                        break;
+                    }
+                }
+            }
+            if (lane == 0) {
+                fetch_bounds(t + kBndAhead);
+                asm volatile("cp.async.wait_group %0;" ::"n"(kBndAhead) : "memory");
+                const int* hb = bnd + (t % kBndRing) * (CS + 1);
+                const int st = t % NS, j = t / NS;
+                if (j > 0) mbar_wait(&empty[st], (j - 1) & 1);
+                unsigned char* sb = tsm + st * Lay::STAGE;
+                int* hdr = reinterpret_cast<int*>(sb);
+                for (int q = 0; q <= CS; ++q) hdr[q] = hb[q];
+                const int s0 = c * CS, s1 = min(s0 + CS, S.nslices);
+                const int b0 = hdr[0], b1 = hdr[CS];
+                const int r0 = S.srow0 + s0 * 32, r1 = min(S.srow0 + s1 * 32, S.n);
+                const uint32_t vb = (uint32_t)tma_align16((r1 - r0) * 8);
+                const uint32_t ab = (uint32_t)(b1 - b0) * 32u * St::ESA;
+                const uint32_t bb = (uint32_t)(b1 - b0) * 32u * St::ESB;
+                const double* xg = stage == 1 ? a.xk : a.out1;
+                const double* xp = stage == 1 ? a.xkm1 : a.xk;
+                mbar_expect_tx(&full[st], ab + bb + 3u * vb);
+                if (ab) bulk_g2s(sb + Lay::HDR, gA + (size_t)b0 * 32 * St::ESA, ab, &full[st]);
+                if (bb) bulk_g2s(sb + Lay::HDR + Lay::A, gB + (size_t)b0 * 32 * St::ESB, bb, &full[st]);
+                bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B, xg + r0, vb, &full[st]);
+                bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + Lay::V, a.f + r0, vb, &full[st]);
+                bulk_g2s(sb + Lay::HDR + Lay::A + Lay::B + 2 * Lay::V, xp + r0, vb, &full[st]);
+            }
+            __syncwarp();
+        }
+    } else {
+        const uint32_t tsm_a = smem_u32(tsm), sv_a = smem_u32(sv), sc_a = smem_u32(sc);
+        for (int t = 0; t < T; ++t) {
+            int stage, c;
+            task(t, stage, c);
+            const int st = t % NS, j = t / NS;
+            mbar_wait(&full[st], j & 1);
+            const uint32_t sb = tsm_a + st * Lay::STAGE;
+            const int h0 = lds_s32(sb);
+            const double* __restrict__ xg = stage == 1 ? a.xk : a.out1;
+            // this warp's SPW slices: decode, then every gather, then the fma chains and epilogues
+            int craw[SPW][W], col[SPW][W], w[SPW];
+            uint32_t Aoff[SPW];
+#pragma unroll
+            for (int hh = 0; hh < SPW; ++hh) {
+                const int q = warp + hh * kTmaWarps;
+                const int s = c * CS + q;
+                const int hq = lds_s32(sb + 4 * q);
+                w[hh] = s < S.nslices ? lds_s32(sb + 4 * (q + 1)) - hq : 0;
+                const uint32_t off = (uint32_t)(hq - h0);
+                const uint32_t A = sb + Lay::HDR + off * 32 * St::ESA + lane * St::ESA;
+                const uint32_t Bc = sb + Lay::HDR + Lay::A + off * 32 * St::ESB + lane * St::ESB;
+                Aoff[hh] = A;
+                const int i = S.srow0 + s * 32 + lane;
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    if (u < w[hh]) {
+                        int cr;
+                        if constexpr (CM == 3) {
+                            craw[hh][u] = lds_u16(A + u * 64);
+                            cr = craw[hh][u] >> 8;
+                        } else {
+                            if constexpr (VM == 1) craw[hh][u] = lds_u8(A + u * 32);
+                            if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
+                            else if constexpr (CM == 1) cr = lds_u8(Bc + u * 32);
+                            else cr = lds_s16(Bc + u * 64);
+                        }
+                        int cc;
+                        if constexpr (CM == 0) cc = cr;
+                        else {
+                            cc = i + ((CM == 1 || CM == 3) ? lds_s32(sc_a + 4 * cr) : cr);
+                            cc = cc < S.chi ? cc : S.chi;
+                        }
+                        col[hh][u] = cc;
+                    }
+                }
+            }
+            double x[SPW][W];
+#pragma unroll
+            for (int hh = 0; hh < SPW; ++hh) {
+                if (stage == 1 || a.gnc) {
+#pragma unroll
+                    for (int u = 0; u < W; ++u)
+                        if (u < w[hh]) x[hh][u] = ld_gather(xg + col[hh][u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < W; ++u)
+                        if (u < w[hh]) x[hh][u] = ld_cg(xg + col[hh][u]);
+                }
+            }
+            const double al = stage == 1 ? a.a1 : a.a2, be = stage == 1 ? a.b1 : a.b2;
+            double* outp = stage == 1 ? a.out1 : a.out2;
+#pragma unroll
+            for (int hh = 0; hh < SPW; ++hh) {
+                const int q = warp + hh * kTmaWarps;
+                double sum = 0.0;
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    if (u < w[hh]) {
+                        double v;
+                        if constexpr (VM == 0) v = lds_f64(Aoff[hh] + u * 256);
+                        else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[hh][u] & 0xff) : craw[hh][u]));
+                        sum = fma(v, x[hh][u], sum);
+                    }
+                }
+                const int i = S.srow0 + (c * CS + q) * 32 + lane;
+                if (w[hh] > 0 && i < S.n) {
+                    const uint32_t vt = sb + Lay::HDR + Lay::A + Lay::B;
+                    const uint32_t r8 = 8 * (q * 32 + lane);
+                    const double xi = lds_f64(vt + r8), fi = lds_f64(vt + Lay::V + r8);
+                    const double prev = lds_f64(vt + 2 * Lay::V + r8);
+                    outp[i] = al * xi + (1.0 - al) * prev + be * (fi - sum);
+                }
+            }
+            if (stage == 1) {  // release the chunk's x_{k+1} to the other CTAs: the consumer warps' barrier
+                               // orders their stores before thread 0's gpu-scope release (cumulative)
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kTmaWarps) : "memory");
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    st_release(a.flags + c, epoch);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+    }
+    // the last CTA to finish publishes the epoch (the next launch waits for epoch + 1)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(reinterpret_cast<unsigned*>(a.sync + 1), 1u) == gridDim.x - 1) {
+            a.sync[1] = 0;
+            st_release(a.sync, epoch);
+        }
+    }
+}
+
 template <class Epi, bool DOTS, int VM, int CM, int W, int SPW, int NS>
 static void launch_tma_w(const SpOp& op, const double* xg, const Epi& e, double* part, unsigned* tk, DotOut dot_out,
                          cudaStream_t s) {
@@ -1105,6 +1361,67 @@ static bool launch_tma(const SpOp& op, const double* xg, const Epi& e, const dou
     CK(cudaGetLastError());
     ++g_launches;
     return true;
+}
+
+template <int VM, int CM, int W>
+static bool launch_smooth2_w(const SpOp& op, Smooth2Args a, cudaStream_t s) {
+    constexpr int NS = 3;
+    constexpr int SPW = (VM == 1) ? 2 : 1;
+    using Lay = TmaLayout<VM, CM, W, SPW, NS>;
+    a.halo = (op.S.maxoff + Lay::ROWS - 1) / Lay::ROWS + 1;  // chunks of ROWS rows
+    static int res = 0;
+    if (!res) {
+        CK(cudaFuncSetAttribute(k_smooth2_tma<VM, CM, W, SPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                Lay::BYTES));
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_smooth2_tma<VM, CM, W, SPW, NS>,
+                                                         32 * (kTmaWarps + 1), Lay::BYTES));
+        res = g_num_sms * (bps < 1 ? 1 : bps);
+    }
+    const int nchunks = (op.S.nslices + Lay::CS - 1) / Lay::CS;
+    const int g = nchunks < res ? nchunks : res;
+    // deadlock freedom needs every CTA resident (g <= res) and more CTAs than halo chunks
+    if (g <= 2 * a.halo + 2 || nchunks < 4 * (a.halo + 1)) return false;
+    launch_k(k_smooth2_tma<VM, CM, W, SPW, NS>, dim3(g), dim3(32 * (kTmaWarps + 1)), (size_t)Lay::BYTES, s, op.S, a);
+    CK(cudaGetLastError());
+    ++g_launches;
+    return true;
+}
+
+bool launch_smooth2(const SpOp& op, const double* xk, const double* xkm1, const double* f, double* out1, double* out2,
+                    double a1, double b1, double a2, double b2, int* flags, int* sync, cudaStream_t s) {
+    // opt-in (AMG_FUSE2=1): halves the pair's HBM traffic but is instruction-issue bound
+    static int on = -1;
+    if (on < 0) on = getenv("AMG_FUSE2") ? 1 : 0;
+    if (!on || !tma_enabled() || !op.sell || op.S.wmax < 4 || op.S.wmax > 8 || op.S.maxoff <= 0 ||
+        !aligned16(xk) || !aligned16(xkm1) || !aligned16(f) || !aligned16(out1))
+        return false;
+    Smooth2Args a{xk, xkm1, f, out1, out2, a1, b1, a2, b2, flags, sync, 0, 4, 0};
+    static int lag = -1, gnc = -1;
+    if (lag < 0) lag = getenv("AMG_FUSE2_LAG") ? atoi(getenv("AMG_FUSE2_LAG")) : 4;
+    if (gnc < 0) gnc = getenv("AMG_FUSE2_NC") ? 1 : 0;
+    a.lag = lag;
+    a.gnc = gnc;
+    switch (op.S.vmode * 4 + op.S.cmode) {
+        case 7:
+            switch (op.S.wmax) {
+                case 4: return launch_smooth2_w<1, 3, 4>(op, a, s);
+                case 5: return launch_smooth2_w<1, 3, 5>(op, a, s);
+                case 6: return launch_smooth2_w<1, 3, 6>(op, a, s);
+                case 7: return launch_smooth2_w<1, 3, 7>(op, a, s);
+                default: return launch_smooth2_w<1, 3, 8>(op, a, s);
+            }
+        case 0:
+            switch (op.S.wmax) {
+                case 4: return launch_smooth2_w<0, 0, 4>(op, a, s);
+                case 5: return launch_smooth2_w<0, 0, 5>(op, a, s);
+                case 6: return launch_smooth2_w<0, 0, 6>(op, a, s);
+                case 7: return launch_smooth2_w<0, 0, 7>(op, a, s);
+                default: return launch_smooth2_w<0, 0, 8>(op, a, s);
+            }
+        default:
+            return false;
+    }
 }
 
 void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f, const double* xprev, double cp,
