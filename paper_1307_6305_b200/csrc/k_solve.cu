@@ -42,6 +42,13 @@ bool pdl_enabled() {
     return on == 1;
 }
 
+// PDL only for launches of at most this many CTAs (the latency-bound coarse-level kernels); 0 = all
+int pdl_max_grid() {
+    static int g = -1;
+    if (g < 0) g = getenv("AMG_PDL_MAXGRID") ? atoi(getenv("AMG_PDL_MAXGRID")) : 0;
+    return g;
+}
+
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
     double2 r;
