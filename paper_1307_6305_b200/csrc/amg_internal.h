@@ -160,6 +160,7 @@ void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f,
 //  two consecutive general steps in one launch (x_{k+1} into out1, x_{k+2} into out2; out2 may alias xk,
 //  out1 may alias xkm1); flags [>= slices/8 + 1] and sync [3] are zero-initialised level scratch.
 //  Returns false (nothing launched) when the level is not eligible.
+bool fuse2_enabled();
 bool launch_smooth2(const SpOp& op, const double* xk, const double* xkm1, const double* f, double* out1, double* out2,
                     double a1, double b1, double a2, double b2, int* flags, int* sync, cudaStream_t s);
 //  resid: out = f - A xg; optional dot r.r into dots[0]

@@ -371,28 +371,32 @@ void amg::finish_build(amg_hierarchy* h) {
         Level& Lv = h->lev[k];
         if (k < h->L - 1 || k == 0) {
             Lv.T = build_tiles(Lv.A, 0, s);
+            pt.mark("tiles", k);
             if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
             if (Lv.S.sptr) Lv.S.chi = Lv.A.n + Lv.H.nhi - 1;
+            pt.mark("sell", k);
             if (Lv.S.sptr && h->opt.compress) compress_sell(Lv.S, Lv.A, s);
+            pt.mark("compress", k);
         }
         Lv.op.A = Lv.A;
         Lv.op.T = Lv.T;
         Lv.op.S = Lv.S;
         Lv.op.sell = Lv.S.sptr != nullptr;
         if (Lv.dist) build_split(h, k);
-        if (Lv.op.sell && !Lv.dist && k < h->L - 1) {  // fused step pairs (k_smooth2_tma) scratch
+        if (fuse2_enabled() && Lv.op.sell && !Lv.dist && k < h->L - 1) {  // fused step pairs (k_smooth2_tma) scratch
             Lv.S.maxoff = Lv.op.S.maxoff = max_col_offset(Lv.A, s);
             const size_t nf = (size_t)Lv.S.nslices / 8 + 2;
             Lv.fflags = halloc<int>(h, nf);
             Lv.fsync = halloc<int>(h, 4);
             CK(cudaMemsetAsync(Lv.fflags, 0, sizeof(int) * nf, s));
             CK(cudaMemsetAsync(Lv.fsync, 0, sizeof(int) * 4, s));
+            pt.mark("max offset", k);
         }
         // vector layout [pad | lower halo | own | upper halo]
         Lv.lo_pad = (Lv.H.nlo + 3) & ~3;
         Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : Lv.A.n;
     }
-    pt.mark("tiles");
+    pt.mark("formats");
     // level workspaces
     for (int k = 0; k < h->L; ++k) {
         Level& Lv = h->lev[k];

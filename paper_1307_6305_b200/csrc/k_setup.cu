@@ -12,10 +12,12 @@
 //  * Dense coarsest (pseudo-)inverse by Gauss-Jordan steps (SPD, no pivoting).
 // CUB (header-only, CUDA 12.9) supplies the radix sorts and scans.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "amg_internal.h"
@@ -31,6 +33,16 @@ static int grid_for(int64_t n) {
     if (g < 1) g = 1;
     if (g > 65535 * 8) g = 65535 * 8;
     return (int)g;
+}
+
+// grids of kernels that end in one global atomic per warp: a few waves of grid-stride blocks, so
+// the atomics do not serialise at one L2 slice (n / 256 blocks made them the kernels' cost)
+static int grid_red(int64_t n) { return std::min(grid_for(n), 148 * 8); }
+
+__device__ __forceinline__ int warp_max_i(int m) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    return m;
 }
 
 // persistent pinned host scratch (one per host thread) for the few scalars setup reads back
@@ -231,7 +243,7 @@ __global__ void k_max_off(int n, const int* __restrict__ rp, const int* __restri
 int max_col_offset(const Csr& A, cudaStream_t s) {
     int* o = dalloc<int>(1, s);
     CK(cudaMemsetAsync(o, 0, sizeof(int), s));
-    k_max_off<<<grid_for(A.n), kBlock, 0, s>>>(A.n, A.rp, A.ci, o);
+    k_max_off<<<grid_red(A.n), kBlock, 0, s>>>(A.n, A.rp, A.ci, o);
     ++g_launches;
     CK(cudaGetLastError());
     const int r = read_scalar(o, s);
@@ -256,7 +268,7 @@ __global__ void k_rowabs_max(int n, const int* __restrict__ rp, const double* __
 double inf_norm(const Csr& A, cudaStream_t s) {
     unsigned long long* o = dalloc<unsigned long long>(1, s);
     CK(cudaMemsetAsync(o, 0, sizeof(unsigned long long), s));
-    k_rowabs_max<<<grid_for(A.n), kBlock, 0, s>>>(A.n, A.rp, A.v, o);
+    k_rowabs_max<<<grid_red(A.n), kBlock, 0, s>>>(A.n, A.rp, A.v, o);
     ++g_launches;
     CK(cudaGetLastError());
     unsigned long long h = read_scalar(o, s);
@@ -342,33 +354,79 @@ __device__ __forceinline__ bool key_gt(const EKey& a, const EKey& b) {
 // free vertex with no free neighbour can never be matched (matches are never undone): it is marked
 // settled (mate -2, unmatched) so later rounds skip it.  Within one round only settled marks are
 // written, and a vertex is settled only if no neighbour is free, so no free vertex reads one.
-__global__ void k_propose(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                          const uint32_t* __restrict__ w, int* __restrict__ mate, int* __restrict__ prop,
-                          uint64_t salt, int off, int* any) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        int best = -1;
-        if (mate[v] == -1) {
-            EKey bk{};
-            for (int p = rp[v]; p < rp[v + 1]; ++p) {
+// G lanes per vertex (G a power of two <= 32, picked from the mean degree): lane t scans entries
+// t, t+G, ... and the group takes the max key by a shuffle butterfly.  Keys are distinct per
+// neighbour (they end in (lo, hi)), so the max does not depend on the scan order.  `list` (or
+// nullptr = all vertices 0..nv) holds the vertices still free when the batch started.
+__device__ __forceinline__ bool prop_gt(uint32_t w1, uint64_t h1, int u1, uint32_t w2, uint64_t h2, int u2, int v) {
+    if (w1 != w2) return w1 > w2;
+    if (h1 != h2) return h1 > h2;
+    const int lo1 = min(u1, v), hi1 = max(u1, v), lo2 = min(u2, v), hi2 = max(u2, v);
+    if (lo1 != lo2) return lo1 > lo2;
+    return hi1 > hi2;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_propose(int nv, const int* __restrict__ list, const int* __restrict__ rp,
+                                                    const int* __restrict__ ci, const uint32_t* __restrict__ w,
+                                                    int* __restrict__ mate, int* __restrict__ prop, uint64_t salt,
+                                                    int off, int* any) {
+    __shared__ int bany;
+    if (threadIdx.x == 0) bany = 0;
+    __syncthreads();
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, t = lane & (G - 1), gi = lane / G;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    bool found = false;
+    for (int base = wid * GPW; base < nv; base += nw * GPW) {  // trip count uniform per warp
+        const int idx = base + gi;
+        const int v = idx < nv ? (list ? list[idx] : idx) : -1;
+        const bool act = v >= 0 && mate[v] == -1;
+        uint32_t bw = 0;
+        uint64_t bh = 0;
+        int bu = -1;
+        if (act) {
+            const int p1 = rp[v + 1];
+            for (int p = rp[v] + t; p < p1; p += G) {
                 const int u = ci[p];
                 if (mate[u] != -1) continue;
-                EKey k = make_key(w[p], v, u, salt, off);
-                if (best < 0 || key_gt(k, bk)) { bk = k; best = u; }
+                const EKey k = make_key(w[p], v, u, salt, off);
+                if (bu < 0 || prop_gt(k.w, k.h, u, bw, bh, bu, v)) { bw = k.w; bh = k.h; bu = u; }
             }
-            if (best < 0) mate[v] = -2;
         }
-        prop[v] = best;
-        if (best >= 0) *any = 1;
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            const uint32_t ow = __shfl_xor_sync(0xffffffffu, bw, o, G);
+            const uint64_t oh = __shfl_xor_sync(0xffffffffu, bh, o, G);
+            const int ou = __shfl_xor_sync(0xffffffffu, bu, o, G);
+            if (ou >= 0 && (bu < 0 || prop_gt(ow, oh, ou, bw, bh, bu, v))) { bw = ow; bh = oh; bu = ou; }
+        }
+        if (act && t == 0) {
+            if (bu < 0) mate[v] = -2;
+            prop[v] = bu;
+            found |= bu >= 0;
+        }
+    }
+    if (found) bany = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && bany) *any = 1;
+}
+
+// handshake round, step 2: mutual proposals match.  A free vertex's proposal target u was free when
+// the batch started, so u is on the list and prop[u] is this round's.
+__global__ void k_accept(int nv, const int* __restrict__ list, int* __restrict__ mate, const int* __restrict__ prop) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nv; idx += gridDim.x * blockDim.x) {
+        const int v = list ? list[idx] : idx;
+        if (mate[v] != -1) continue;
+        const int u = prop[v];
+        if (u >= 0 && prop[u] == v) mate[v] = u;
     }
 }
 
-// handshake round, step 2: mutual proposals match
-__global__ void k_accept(int n, int* __restrict__ mate, const int* __restrict__ prop) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const int u = prop[v];
-        if (u >= 0 && mate[v] == -1 && prop[u] == v) mate[v] = u;
-    }
-}
+struct IsFree {
+    const int* mate;
+    __device__ bool operator()(int v) const { return mate[v] == -1; }
+};
 
 // attach (A3) + leader (A4)
 __global__ void k_leader(int n, const int* __restrict__ rp, const int* __restrict__ ci,
@@ -405,7 +463,6 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, in
     int* mate = dalloc<int>(n, s);
     int* prop = dalloc<int>(n, s);
     int* any = dalloc<int>(4, s);
-    int* hany = static_cast<int*>(pinned_scratch()) + 16;
     CK(cudaMemsetAsync(mate, 0xff, sizeof(int) * (size_t)n, s));
     int r = 0;
     const int g = grid_for(n);
@@ -413,21 +470,65 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, in
     // read back: a round without proposals means the matching is maximal, and further rounds are
     // no-ops, so the result does not depend on the batch size.
     constexpr int kBatch = 3;
+    static int gsel = -1;
+    if (gsel < 0) gsel = getenv("AMG_PROPOSE_G") ? atoi(getenv("AMG_PROPOSE_G")) : 0;
+    int Gl = gsel;
+    if (Gl <= 0) {  // about four entries per lane
+        const double dg = n > 0 ? (double)G.nnz / (double)n : 0.0;
+        Gl = 2;
+        while (Gl < 16 && 4.0 * Gl < dg) Gl <<= 1;
+    }
+    // after the first batch the rounds run over the vertices still free (a shrinking list)
+    int* list = nullptr;
+    int* list2 = nullptr;
+    int* nsel = dalloc<int>(2, s);
+    int* hsel = static_cast<int*>(pinned_scratch()) + 20;
+    int nv = n;
+    void* tmp = nullptr;
+    size_t tb = 0;
     for (;;) {
+        const int gp = std::max(1, std::min((int)(((int64_t)nv * Gl + kBlock - 1) / kBlock), 148 * 8));
+        const int ga = std::max(1, std::min(grid_for(nv), 148 * 8));
         for (int k = 0; k < kBatch; ++k) {
             CK(cudaMemsetAsync(any, 0, sizeof(int), s));
-            k_propose<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, prop, salt, id_off, any);
+            switch (Gl) {
+                case 1: k_propose<1><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
+                case 2: k_propose<2><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
+                case 4: k_propose<4><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
+                case 8: k_propose<8><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
+                default: k_propose<16><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
+            }
             ++g_launches;
-            k_accept<<<g, kBlock, 0, s>>>(n, mate, prop);
+            k_accept<<<ga, kBlock, 0, s>>>(nv, list, mate, prop);
             ++g_launches;
         }
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(hany, any, sizeof(int), cudaMemcpyDeviceToHost, s));
+        // next batch's list: the vertices still free
+        if (!list) {
+            list = dalloc<int>((size_t)n + 1, s);
+            list2 = dalloc<int>((size_t)n + 1, s);
+            size_t tb2 = 0;
+            CK(cub::DeviceSelect::If(nullptr, tb, thrust::counting_iterator<int>(0), list, nsel, n, IsFree{mate}, s));
+            CK(cub::DeviceSelect::If(nullptr, tb2, list, list2, nsel, n, IsFree{mate}, s));
+            tb = std::max(tb, tb2);
+            tmp = dalloc<char>(tb, s);
+            CK(cub::DeviceSelect::If(tmp, tb, thrust::counting_iterator<int>(0), list, nsel, n, IsFree{mate}, s));
+        } else {
+            CK(cub::DeviceSelect::If(tmp, tb, list, list2, nsel, nv, IsFree{mate}, s));
+            std::swap(list, list2);
+        }
+        CK(cudaMemcpyAsync(nsel + 1, any, sizeof(int), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(hsel, nsel, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         r += kBatch;
-        if (!*hany) break;
+        if (!hsel[1] || hsel[0] == 0) break;
+        nv = hsel[0];
         if (r > 30000) throw Error(-7, "matching did not terminate");
     }
+    dfree(list, s);
+    dfree(list2, s);
+    dfree(tmp, s);
+    dfree(nsel, s);
     int* leader = prop;  // reuse
     int* isl = dalloc<int>((size_t)n + 1, s);
     CK(cudaMemsetAsync(isl + n, 0, sizeof(int), s));
@@ -602,7 +703,8 @@ __global__ void k_rm_count(int nc, const int* __restrict__ rp, const int* __rest
         E[I] = e;
         m = max(m, e);
     }
-    atomicMax(emax, m);
+    m = warp_max_i(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(emax, m);
 }
 
 template <class VAL>
@@ -611,7 +713,7 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nc, const int* _
                                                             const int* __restrict__ perm, const int* __restrict__ aptr,
                                                             const int* __restrict__ eoff, bool drop,
                                                             int* __restrict__ tcol, VAL* __restrict__ tval,
-                                                            int* __restrict__ ucount, int emin) {
+                                                            int* __restrict__ ucount, int emin, int emax) {
     __shared__ unsigned long long skey[kRMWarps][kRM];
     __shared__ VAL sval[kRMWarps][kRM];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -620,7 +722,7 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nc, const int* _
     const int nwarp = gridDim.x * kRMWarps;
     for (int I = blockIdx.x * kRMWarps + wib; I < nc; I += nwarp) {
         const int e0 = eoff[I], E = eoff[I + 1] - e0;
-        if (E > kRM || E <= emin) continue;  // wide rows: k_rm_merge_block; rows <= emin: k_rm_small
+        if (E > emax || E <= emin) continue;  // wider rows: k_rm_hash / k_rm_merge_block; rows <= emin: k_rm_small
         // gather in (member, position) order, k = running rank; members are spread over the lanes
         // (one member per lane, a warp prefix sum of their row lengths gives each its first k)
         const int t0 = aptr[I], t1 = aptr[I + 1];
@@ -691,6 +793,130 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nc, const int* _
     }
 }
 
+
+// Sort-free warp merge (the default for emin < E <= kRM): the warp walks the row's entries in
+// (member, CSR position) order, 32 at a time (lane = entry within the chunk, its member found by a
+// shuffle binary search over the members' first ranks).  __match_any_sync groups the chunk's
+// entries by J; the group's lowest lane looks J up in a per-warp shared-memory hash table
+// (open addressing, 2 kRM slots) and adds the group's values to J's accumulator one at a time in
+// lane order.  Every accumulator therefore sees its entries in increasing k, the sequential order,
+// so fp64 sums are bit-exact with the definition (the first entry initialises it, so -0.0 survives).
+// The U distinct J are then ranked by counting (columns come out sorted) and written.
+constexpr int kRHWarps = 8;
+constexpr int kRHSlots = 2 * kRM;
+template <class VAL>
+struct RhWarp {
+    unsigned hk[kRHSlots];
+    VAL hv[kRHSlots];
+    VAL sv[32];
+    unsigned lj[kRM];
+    int list[kRM];
+    int cnt;
+};
+
+template <class VAL>
+__global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                           const VAL* __restrict__ src, const int* __restrict__ agg,
+                                                           const int* __restrict__ perm, const int* __restrict__ aptr,
+                                                           const int* __restrict__ eoff, bool drop,
+                                                           int* __restrict__ tcol, VAL* __restrict__ tval,
+                                                           int* __restrict__ ucount, int emin) {
+    extern __shared__ __align__(16) unsigned char rh_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    RhWarp<VAL>& W = reinterpret_cast<RhWarp<VAL>*>(rh_raw)[wib];
+    const unsigned NONE = 0xFFFFFFFFu;
+    for (int q = lane; q < kRHSlots; q += 32) W.hk[q] = NONE;
+    if (lane == 0) W.cnt = 0;
+    __syncwarp();
+    const int nwarp = gridDim.x * kRHWarps;
+    for (int I = blockIdx.x * kRHWarps + wib; I < nc; I += nwarp) {
+        const int e0 = eoff[I], E = eoff[I + 1] - e0;
+        if (E > kRM || E <= emin) continue;  // wide rows: k_rm_merge_block; rows <= emin: k_rm_small
+        const int t1 = aptr[I + 1];
+        for (int tb = aptr[I]; tb < t1; tb += 32) {  // blocks of <= 32 members
+            const int Mb = min(32, t1 - tb);
+            int p0 = 0, len = 0;
+            if (lane < Mb) {
+                const int v = perm[tb + lane];
+                p0 = rp[v];
+                len = rp[v + 1] - p0;
+            }
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int kb = incl - len;  // first rank of member `lane` within the block
+            const int Eb = __shfl_sync(0xffffffffu, incl, 31);
+            for (int c = 0; c < Eb; c += 32) {
+                const int k = c + lane;
+                // member m = largest m < Mb with kb[m] <= k (empty members are skipped over)
+                int m = 0;
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) {
+                    const int kbs = __shfl_sync(0xffffffffu, kb, (m + st) & 31);
+                    if (m + st < Mb && kbs <= k) m += st;
+                }
+                const int pm = __shfl_sync(0xffffffffu, p0, m);
+                const int km = __shfl_sync(0xffffffffu, kb, m);
+                unsigned J = NONE;
+                VAL v = VAL(0);
+                if (k < Eb) {
+                    const int pos = pm + (k - km);
+                    const unsigned j = (unsigned)agg[ci[pos]];
+                    v = src[pos];
+                    J = (drop && j == (unsigned)I) ? NONE : j;
+                }
+                W.sv[lane] = v;
+                const unsigned grp = __match_any_sync(0xffffffffu, J);
+                __syncwarp();
+                if (J != NONE && __ffs(grp) - 1 == lane) {
+                    unsigned h = (J * 2654435761u) >> (32 - 9);
+                    bool fresh;
+                    for (;;) {
+                        const unsigned old = atomicCAS(&W.hk[h], NONE, J);
+                        if (old == NONE) { fresh = true; break; }
+                        if (old == J) { fresh = false; break; }
+                        h = (h + 1) & (kRHSlots - 1);
+                    }
+                    unsigned bits = grp;
+                    VAL a;
+                    if (fresh) {
+                        a = W.sv[lane];
+                        bits &= bits - 1;
+                        W.list[atomicAdd(&W.cnt, 1)] = (int)h;
+                    } else {
+                        a = W.hv[h];
+                    }
+                    while (bits) {
+                        a += W.sv[__ffs(bits) - 1];
+                        bits &= bits - 1;
+                    }
+                    W.hv[h] = a;
+                }
+                __syncwarp();
+            }
+        }
+        const int U = W.cnt;
+        for (int u = lane; u < U; u += 32) W.lj[u] = W.hk[W.list[u]];
+        __syncwarp();
+        for (int u = lane; u < U; u += 32) {
+            const unsigned J = W.lj[u];
+            int rank = 0;
+            for (int r = 0; r < U; ++r) rank += W.lj[r] < J;
+            const int h = W.list[u];
+            tcol[e0 + rank] = (int)J;
+            tval[e0 + rank] = W.hv[h];
+            W.hk[h] = NONE;
+        }
+        if (lane == 0) {
+            ucount[I] = U;
+            W.cnt = 0;
+        }
+        __syncwarp();
+    }
+}
 
 // Same merge for the rare wide coarse rows (kRM < E <= kRMB), one 256-thread CTA per row with the
 // buffers in dynamic shared memory.
@@ -877,6 +1103,79 @@ __global__ void __launch_bounds__(256) k_rm_small(int nc, const int* __restrict_
     }
 }
 
+// Pass-graph rows (uint32 weights: integer sums, so neither the summation order nor the column order
+// matters to the matching, whose keys are order free) with emin < E <= G: G lanes per row, lane t =
+// entry t in (member, CSR position) order (member by a shuffle binary search), __match_any_sync on
+// (row slot, J) groups equal J, the group's first lane sums it and takes output slot = number of
+// group heads before it (first-occurrence order: deterministic, unsorted).
+template <int G>
+__global__ void __launch_bounds__(256) k_qg_small(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                  const uint32_t* __restrict__ src, const int* __restrict__ agg,
+                                                  const int* __restrict__ perm, const int* __restrict__ aptr,
+                                                  const int* __restrict__ eoff, int* __restrict__ tcol,
+                                                  uint32_t* __restrict__ tval, int* __restrict__ ucount, int emin) {
+    __shared__ uint32_t sw[256];
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, t = lane & (G - 1), gi = lane / G;
+    const unsigned NONE = 0xFFFFFFFFu;
+    const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    uint32_t* ws = sw + (threadIdx.x & ~31);
+    for (int base = wid * GPW; base < nc; base += nw * GPW) {
+        const int I = base + gi;
+        const bool rowok = I < nc;
+        const int e0 = rowok ? eoff[I] : 0;
+        const int E = rowok ? eoff[I + 1] - e0 : 0;
+        const bool mine = rowok && E > emin && E <= G;
+        const int t0 = mine ? aptr[I] : 0;
+        const int M = mine ? aptr[I + 1] - t0 : 0;
+        int p0 = 0, len = 0;
+        if (t < M) {
+            const int v = perm[t0 + t];
+            p0 = rp[v];
+            len = rp[v + 1] - p0;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o, G);
+            if (t >= o) incl += y;
+        }
+        const int kb = incl - len;
+        int m = 0;
+#pragma unroll
+        for (int st = G / 2; st > 0; st >>= 1) {
+            const int kbs = __shfl_sync(0xffffffffu, kb, (m + st) & (G - 1), G);
+            if (m + st < M && kbs <= t) m += st;
+        }
+        const int pm = __shfl_sync(0xffffffffu, p0, m, G);
+        const int km = __shfl_sync(0xffffffffu, kb, m, G);
+        unsigned J = NONE;
+        uint32_t wv = 0;
+        if (mine && t < E) {
+            const int pos = pm + (t - km);
+            const unsigned j = (unsigned)agg[ci[pos]];
+            wv = src[pos];
+            J = j == (unsigned)I ? NONE : j;
+        }
+        ws[lane] = wv;
+        const unsigned long long key = ((unsigned long long)gi << 32) | J;
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const bool head = J != NONE && __ffs(grp) - 1 == lane;
+        const unsigned hb = __ballot_sync(0xffffffffu, head) & gm;
+        __syncwarp();
+        if (head) {
+            uint32_t acc = 0;
+            for (unsigned b = grp; b; b &= b - 1) acc += ws[__ffs(b) - 1];
+            const int slot = __popc(hb & ((1u << lane) - 1u));
+            tcol[e0 + slot] = (int)J;
+            tval[e0 + slot] = acc;
+        }
+        if (mine && t == 0) ucount[I] = __popc(hb);
+        __syncwarp();
+    }
+}
+
 // returns false (nothing allocated) if some coarse row has more than kRM entries
 template <class VAL>
 static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg, int nc,
@@ -888,7 +1187,7 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
     int* emax = dalloc<int>(1, s);
     CK(cudaMemsetAsync(emax, 0, sizeof(int), s));
     CK(cudaMemsetAsync(E + nc, 0, sizeof(int), s));
-    k_rm_count<<<grid_for(nc), kBlock, 0, s>>>(nc, rp, perm, aptr, E, emax);
+    k_rm_count<<<grid_red(nc), kBlock, 0, s>>>(nc, rp, perm, aptr, E, emax);
     ++g_launches;
     CK(cudaGetLastError());
     const int mx = read_scalar(emax, s);
@@ -907,8 +1206,31 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
     // larger rows: the warp bitonic merge (and the CTA merge above kRM entries)
     static int small_on = -1;
     if (small_on < 0) small_on = getenv("AMG_RM_NO_SMALL") ? 0 : 1;
+    static int qg_on = -1;
+    if (qg_on < 0) qg_on = getenv("AMG_QG_SORTED") ? 0 : 1;
     int emin = 0;
-    if (small_on) {
+    if constexpr (std::is_same<VAL, uint32_t>::value) {
+        if (small_on && qg_on && drop) {  // pass graphs: unsorted sub-warp merges up to 32 entries
+            const int g8 = (int)std::min<int64_t>((nc + 31) / 32, 148LL * 32);
+            k_qg_small<8><<<g8, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc, 0);
+            ++g_launches;
+            emin = 8;
+            if (mx > 8) {
+                const int g16 = (int)std::min<int64_t>((nc + 15) / 16, 148LL * 32);
+                k_qg_small<16><<<g16, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc, 8);
+                ++g_launches;
+                emin = 16;
+            }
+            if (mx > 16) {
+                const int g32 = (int)std::min<int64_t>((nc + 7) / 8, 148LL * 32);
+                k_qg_small<32><<<g32, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc, 16);
+                ++g_launches;
+                emin = 32;
+            }
+            CK(cudaGetLastError());
+        }
+    }
+    if (small_on && emin == 0) {
         const int gb = (int)std::min<int64_t>((nc + 31) / 32, 148LL * 32);
         k_rm_small<VAL, 8><<<gb, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, 0);
         ++g_launches;
@@ -923,11 +1245,28 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
         }
         CK(cudaGetLastError());
     }
-    const int nb = (int)std::min<int64_t>((nc + kRMWarps - 1) / kRMWarps, 148LL * 16);
-    if (mx > emin)
+    // rows of emin < E <= split: bitonic warp merge; split < E <= kRM: hash warp merge
+    static int split = -1;
+    if (split < 0) split = getenv("AMG_RM_SPLIT") ? std::min(kRM, atoi(getenv("AMG_RM_SPLIT"))) : 32;
+    if (mx > emin && split > emin) {
+        const int nb = (int)std::min<int64_t>((nc + kRMWarps - 1) / kRMWarps, 148LL * 16);
         k_rm_merge<VAL><<<nb, 32 * kRMWarps, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc,
+                                                     emin, split);
+        ++g_launches;
+        emin = split;
+    }
+    if (mx > emin) {
+        const size_t sm = sizeof(RhWarp<VAL>) * kRHWarps;
+        static bool cfg = false;
+        if (!cfg) {
+            CK(cudaFuncSetAttribute(k_rm_hash<VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            cfg = true;
+        }
+        const int nb = (int)std::min<int64_t>((nc + kRHWarps - 1) / kRHWarps, 148LL * 3);
+        k_rm_hash<VAL><<<nb, 32 * kRHWarps, sm, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc,
                                                      emin);
-    ++g_launches;
+        ++g_launches;
+    }
     CK(cudaGetLastError());
     if (mx > kRM) {  // list the wide rows, one CTA each
         int* flag = dalloc<int>((size_t)nc + 1, s);
@@ -1124,7 +1463,8 @@ __global__ void k_sell_fill(int n, int nslices, const int* __restrict__ rp, cons
 __global__ void k_max_int(int n, const int* __restrict__ a, int* out) {
     int m = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = max(m, a[i]);
-    atomicMax(out, m);
+    m = warp_max_i(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s) {
@@ -1142,7 +1482,7 @@ Sell build_sell(const Csr& A, double max_pad_ratio, cudaStream_t s) {
     {
         int* wm = dalloc<int>(1, s);
         CK(cudaMemsetAsync(wm, 0, sizeof(int), s));
-        k_max_int<<<grid_for(S.nslices), kBlock, 0, s>>>(S.nslices, width, wm);
+        k_max_int<<<grid_red(S.nslices), kBlock, 0, s>>>(S.nslices, width, wm);
         ++g_launches;
         CK(cudaGetLastError());
         S.wmax = read_scalar(wm, s);
@@ -1353,7 +1693,7 @@ void compress_sell(Sell& S, const Csr& A, cudaStream_t s) {
     CK(cudaMemsetAsync(gv, 0xff, sizeof(unsigned long long) * kGHT, s));
     CK(cudaMemsetAsync(gc, 0xff, sizeof(unsigned long long) * kGHT, s));
     CK(cudaMemsetAsync(aux, 0, sizeof(int) * 8, s));
-    const int g = grid_for((int64_t)S.nslices * 32);
+    const int g = grid_red((int64_t)S.nslices * 32);
     k_distinct<<<g, kBlock, 0, s>>>(S, gv, gc, aux, aux + 2);
     ++g_launches;
     k_minmax_off<<<g, kBlock, 0, s>>>(S, aux + 3);

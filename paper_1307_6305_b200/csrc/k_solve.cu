@@ -1395,12 +1395,16 @@ static bool launch_smooth2_w(const SpOp& op, Smooth2Args a, cudaStream_t s) {
     return true;
 }
 
-bool launch_smooth2(const SpOp& op, const double* xk, const double* xkm1, const double* f, double* out1, double* out2,
-                    double a1, double b1, double a2, double b2, int* flags, int* sync, cudaStream_t s) {
-    // opt-in (AMG_FUSE2=1): halves the pair's HBM traffic but is instruction-issue bound
+// opt-in (AMG_FUSE2=1): halves the pair's HBM traffic but is instruction-issue bound
+bool fuse2_enabled() {
     static int on = -1;
     if (on < 0) on = getenv("AMG_FUSE2") ? 1 : 0;
-    if (!on || !tma_enabled() || !op.sell || op.S.wmax < 4 || op.S.wmax > 8 || op.S.maxoff <= 0 ||
+    return on != 0;
+}
+
+bool launch_smooth2(const SpOp& op, const double* xk, const double* xkm1, const double* f, double* out1, double* out2,
+                    double a1, double b1, double a2, double b2, int* flags, int* sync, cudaStream_t s) {
+    if (!fuse2_enabled() || !tma_enabled() || !op.sell || op.S.wmax < 4 || op.S.wmax > 8 || op.S.maxoff <= 0 ||
         !aligned16(xk) || !aligned16(xkm1) || !aligned16(f) || !aligned16(out1))
         return false;
     Smooth2Args a{xk, xkm1, f, out1, out2, a1, b1, a2, b2, flags, sync, 0, 4, 0};
