@@ -694,35 +694,59 @@ void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaSt
 constexpr int kRM = 256;          // entries per warp buffer
 constexpr int kRMWarps = 8;       // warps per block
 
+// E[I] = entries of coarse row I before merging; rows are also sorted into size classes
+// (E <= 8, <= 16, <= 32, <= kRM, larger) by warp-aggregated appends to lists[c * nc ..]: each class
+// has its own kernel, and a row's output position comes from the scan of E, so the (run-dependent)
+// list order does not change any result.
+constexpr int kRMClasses = 5;
+__device__ __forceinline__ int rm_class(int e, int kmax) { return e <= 8 ? 0 : e <= 16 ? 1 : e <= 32 ? 2 : e <= kmax ? 3 : 4; }
+
 __global__ void k_rm_count(int nc, const int* __restrict__ rp, const int* __restrict__ perm,
-                          const int* __restrict__ aptr, int* __restrict__ E, int* __restrict__ emax) {
+                           const int* __restrict__ aptr, int* __restrict__ E, int* __restrict__ emax,
+                           int* __restrict__ lists, int* __restrict__ counts, int kmax) {
     int m = 0;
-    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
-        int e = 0;
-        for (int t = aptr[I]; t < aptr[I + 1]; ++t) e += rp[perm[t] + 1] - rp[perm[t]];
-        E[I] = e;
-        m = max(m, e);
+    const int lane = threadIdx.x & 31;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int base = wid * 32; base < nc; base += nw * 32) {  // uniform trip count per warp
+        const int I = base + lane;
+        int c = -1;
+        if (I < nc) {
+            int e = 0;
+            for (int t = aptr[I]; t < aptr[I + 1]; ++t) e += rp[perm[t] + 1] - rp[perm[t]];
+            E[I] = e;
+            m = max(m, e);
+            c = rm_class(e, kmax);
+        }
+#pragma unroll
+        for (int k = 0; k < kRMClasses; ++k) {
+            const unsigned mk = __ballot_sync(0xffffffffu, c == k);
+            if (!mk) continue;
+            int b0 = 0;
+            if (lane == __ffs(mk) - 1) b0 = atomicAdd(counts + k, __popc(mk));
+            b0 = __shfl_sync(0xffffffffu, b0, __ffs(mk) - 1);
+            if (c == k) lists[(size_t)k * nc + b0 + __popc(mk & ((1u << lane) - 1u))] = I;
+        }
     }
     m = warp_max_i(m);
-    if ((threadIdx.x & 31) == 0) atomicMax(emax, m);
+    if (lane == 0) atomicMax(emax, m);
 }
 
 template <class VAL>
-__global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+__global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
                                                             const VAL* __restrict__ src, const int* __restrict__ agg,
                                                             const int* __restrict__ perm, const int* __restrict__ aptr,
                                                             const int* __restrict__ eoff, bool drop,
                                                             int* __restrict__ tcol, VAL* __restrict__ tval,
-                                                            int* __restrict__ ucount, int emin, int emax) {
+                                                            int* __restrict__ ucount) {
     __shared__ unsigned long long skey[kRMWarps][kRM];
     __shared__ VAL sval[kRMWarps][kRM];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned long long* key = skey[wib];
     VAL* val = sval[wib];
     const int nwarp = gridDim.x * kRMWarps;
-    for (int I = blockIdx.x * kRMWarps + wib; I < nc; I += nwarp) {
+    for (int r = blockIdx.x * kRMWarps + wib; r < nl; r += nwarp) {
+        const int I = list[r];
         const int e0 = eoff[I], E = eoff[I + 1] - e0;
-        if (E > emax || E <= emin) continue;  // wider rows: k_rm_hash / k_rm_merge_block; rows <= emin: k_rm_small
         // gather in (member, position) order, k = running rank; members are spread over the lanes
         // (one member per lane, a warp prefix sum of their row lengths gives each its first k)
         const int t0 = aptr[I], t1 = aptr[I + 1];
@@ -815,12 +839,12 @@ struct RhWarp {
 };
 
 template <class VAL>
-__global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+__global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
                                                            const VAL* __restrict__ src, const int* __restrict__ agg,
                                                            const int* __restrict__ perm, const int* __restrict__ aptr,
                                                            const int* __restrict__ eoff, bool drop,
                                                            int* __restrict__ tcol, VAL* __restrict__ tval,
-                                                           int* __restrict__ ucount, int emin) {
+                                                           int* __restrict__ ucount) {
     extern __shared__ __align__(16) unsigned char rh_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     RhWarp<VAL>& W = reinterpret_cast<RhWarp<VAL>*>(rh_raw)[wib];
@@ -829,9 +853,9 @@ __global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nc, const int* __
     if (lane == 0) W.cnt = 0;
     __syncwarp();
     const int nwarp = gridDim.x * kRHWarps;
-    for (int I = blockIdx.x * kRHWarps + wib; I < nc; I += nwarp) {
-        const int e0 = eoff[I], E = eoff[I + 1] - e0;
-        if (E > kRM || E <= emin) continue;  // wide rows: k_rm_merge_block; rows <= emin: k_rm_small
+    for (int r = blockIdx.x * kRHWarps + wib; r < nl; r += nwarp) {
+        const int I = list[r];
+        const int e0 = eoff[I];
         const int t1 = aptr[I + 1];
         for (int tb = aptr[I]; tb < t1; tb += 32) {  // blocks of <= 32 members
             const int Mb = min(32, t1 - tb);
@@ -1026,11 +1050,11 @@ __global__ void k_rm_compact(int nc, const int* __restrict__ eoff, const int* __
 // same J; the head sums its run in increasing k (the sequential order: bit-exact); its output slot
 // is the number of heads with a smaller J (columns come out sorted).  Rows with E > G are skipped.
 template <class VAL, int G>
-__global__ void __launch_bounds__(256) k_rm_small(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+__global__ void __launch_bounds__(256) k_rm_small(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
                                                   const VAL* __restrict__ src, const int* __restrict__ agg,
                                                   const int* __restrict__ perm, const int* __restrict__ aptr,
                                                   const int* __restrict__ eoff, bool drop, int* __restrict__ tcol,
-                                                  VAL* __restrict__ tval, int* __restrict__ ucount, int emin) {
+                                                  VAL* __restrict__ tval, int* __restrict__ ucount) {
     constexpr int GPW = 32 / G;  // rows per warp
     const int lane = threadIdx.x & 31;
     const int t = lane & (G - 1);
@@ -1038,12 +1062,11 @@ __global__ void __launch_bounds__(256) k_rm_small(int nc, const int* __restrict_
     const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const int wstride = ((gridDim.x * blockDim.x) >> 5) * GPW;
     // the warp's rows share one trip count (full-mask shuffles below)
-    for (int wb = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW; wb < nc; wb += wstride) {
-        const int I = wb + lane / G;
-        const bool rowok = I < nc;
-        const int e0 = rowok ? eoff[I] : 0;
-        const int E = rowok ? eoff[I + 1] - e0 : 0;
-        const bool mine = rowok && E > emin && E <= G;
+    for (int wb = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW; wb < nl; wb += wstride) {
+        const int idx = wb + lane / G;
+        const bool mine = idx < nl;
+        const int I = mine ? list[idx] : 0;
+        const int e0 = mine ? eoff[I] : 0;
         // members of the aggregate: lane t < M holds member t's first position and row length
         const int t0 = mine ? aptr[I] : 0;
         const int M = mine ? aptr[I + 1] - t0 : 0;
@@ -1109,11 +1132,11 @@ __global__ void __launch_bounds__(256) k_rm_small(int nc, const int* __restrict_
 // (row slot, J) groups equal J, the group's first lane sums it and takes output slot = number of
 // group heads before it (first-occurrence order: deterministic, unsorted).
 template <int G>
-__global__ void __launch_bounds__(256) k_qg_small(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+__global__ void __launch_bounds__(256) k_qg_small(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
                                                   const uint32_t* __restrict__ src, const int* __restrict__ agg,
                                                   const int* __restrict__ perm, const int* __restrict__ aptr,
                                                   const int* __restrict__ eoff, int* __restrict__ tcol,
-                                                  uint32_t* __restrict__ tval, int* __restrict__ ucount, int emin) {
+                                                  uint32_t* __restrict__ tval, int* __restrict__ ucount) {
     __shared__ uint32_t sw[256];
     constexpr int GPW = 32 / G;
     const int lane = threadIdx.x & 31, t = lane & (G - 1), gi = lane / G;
@@ -1121,12 +1144,12 @@ __global__ void __launch_bounds__(256) k_qg_small(int nc, const int* __restrict_
     const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     uint32_t* ws = sw + (threadIdx.x & ~31);
-    for (int base = wid * GPW; base < nc; base += nw * GPW) {
-        const int I = base + gi;
-        const bool rowok = I < nc;
-        const int e0 = rowok ? eoff[I] : 0;
-        const int E = rowok ? eoff[I + 1] - e0 : 0;
-        const bool mine = rowok && E > emin && E <= G;
+    for (int base = wid * GPW; base < nl; base += nw * GPW) {
+        const int idx = base + gi;
+        const bool mine = idx < nl;
+        const int I = mine ? list[idx] : 0;
+        const int e0 = mine ? eoff[I] : 0;
+        const int E = mine ? eoff[I + 1] - e0 : 0;
         const int t0 = mine ? aptr[I] : 0;
         const int M = mine ? aptr[I + 1] - t0 : 0;
         int p0 = 0, len = 0;
@@ -1184,115 +1207,93 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
     (void)n;
     (void)nnz;
     int* E = dalloc<int>((size_t)nc + 1, s);
-    int* emax = dalloc<int>(1, s);
-    CK(cudaMemsetAsync(emax, 0, sizeof(int), s));
+    int* cnt = dalloc<int>(8, s);  // emax, counts[5]
+    int* lists = dalloc<int>((size_t)kRMClasses * nc + 1, s);
+    CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
     CK(cudaMemsetAsync(E + nc, 0, sizeof(int), s));
-    k_rm_count<<<grid_red(nc), kBlock, 0, s>>>(nc, rp, perm, aptr, E, emax);
+    static int split = -1;  // AMG_RM_SPLIT=16: rows of 16 < E <= 32 also go to the hash merge
+    if (split < 0) split = getenv("AMG_RM_SPLIT") ? atoi(getenv("AMG_RM_SPLIT")) : 32;
+    k_rm_count<<<grid_red(nc), kBlock, 0, s>>>(nc, rp, perm, aptr, E, cnt, lists, cnt + 1, kRM);
     ++g_launches;
     CK(cudaGetLastError());
-    const int mx = read_scalar(emax, s);
-    dfree(emax, s);
+    int* hc = static_cast<int*>(pinned_scratch()) + 40;
+    CK(cudaMemcpyAsync(hc, cnt, 6 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int mx = hc[0];
+    int ncl[kRMClasses];
+    for (int k = 0; k < kRMClasses; ++k) ncl[k] = hc[1 + k];
+    dfree(cnt, s);
     if (mx > kRMB) {
         dfree(E, s);
+        dfree(lists, s);
         return false;
     }
+    auto L = [&](int k) { return lists + (size_t)k * nc; };
     int* eoff = dalloc<int>((size_t)nc + 1, s);
     const int64_t tot = exclusive_scan_total(E, eoff, nc, s);
     int* tcol = dalloc<int>((size_t)tot + 8, s);
     VAL* tval = dalloc<VAL>((size_t)tot + 8, s);
     int* uc = E;  // reuse: unique counts
     CK(cudaMemsetAsync(uc + nc, 0, sizeof(int), s));
-    // rows of <= 8 / <= 32 entries: sort-free shuffle merges (4 rows per warp / 1 row per warp);
-    // larger rows: the warp bitonic merge (and the CTA merge above kRM entries)
-    static int small_on = -1;
-    if (small_on < 0) small_on = getenv("AMG_RM_NO_SMALL") ? 0 : 1;
-    static int qg_on = -1;
-    if (qg_on < 0) qg_on = getenv("AMG_QG_SORTED") ? 0 : 1;
-    int emin = 0;
+    auto grid_rows = [](int nrows, int rows_per_block, int cap) {
+        return (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)nrows + rows_per_block - 1) / rows_per_block, cap));
+    };
+    // class kernels: E <= 8 | <= 16 | <= 32: sub-warp merges (pass graphs: unsorted k_qg_small; fp64:
+    // k_rm_small for <= 8, the bitonic warp merge above); <= kRM: the hash warp merge; wider: one CTA
+    bool pass_graph = false;
+    if constexpr (std::is_same<VAL, uint32_t>::value) pass_graph = drop;
+    int hash_from = 3;  // first class sent to the hash merge
+    if (split <= 16) hash_from = 2;
+    if (split <= 8) hash_from = 1;
     if constexpr (std::is_same<VAL, uint32_t>::value) {
-        if (small_on && qg_on && drop) {  // pass graphs: unsorted sub-warp merges up to 32 entries
-            const int g8 = (int)std::min<int64_t>((nc + 31) / 32, 148LL * 32);
-            k_qg_small<8><<<g8, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc, 0);
-            ++g_launches;
-            emin = 8;
-            if (mx > 8) {
-                const int g16 = (int)std::min<int64_t>((nc + 15) / 16, 148LL * 32);
-                k_qg_small<16><<<g16, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc, 8);
-                ++g_launches;
-                emin = 16;
-            }
-            if (mx > 16) {
-                const int g32 = (int)std::min<int64_t>((nc + 7) / 8, 148LL * 32);
-                k_qg_small<32><<<g32, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc, 16);
-                ++g_launches;
-                emin = 32;
-            }
-            CK(cudaGetLastError());
+        if (pass_graph) {
+            if (ncl[0]) k_qg_small<8><<<grid_rows(ncl[0], 32, 148 * 32), 256, 0, s>>>(ncl[0], L(0), rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc);
+            if (ncl[1]) k_qg_small<16><<<grid_rows(ncl[1], 16, 148 * 32), 256, 0, s>>>(ncl[1], L(1), rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc);
+            if (ncl[2]) k_qg_small<32><<<grid_rows(ncl[2], 8, 148 * 32), 256, 0, s>>>(ncl[2], L(2), rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc);
+            g_launches += 3;
+            hash_from = 3;
         }
     }
-    if (small_on && emin == 0) {
-        const int gb = (int)std::min<int64_t>((nc + 31) / 32, 148LL * 32);
-        k_rm_small<VAL, 8><<<gb, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, 0);
+    if (!pass_graph) {
+        if (ncl[0]) k_rm_small<VAL, 8><<<grid_rows(ncl[0], 32, 148 * 32), 256, 0, s>>>(ncl[0], L(0), rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
         ++g_launches;
-        emin = 8;
-        static int g16 = -1;
-        if (g16 < 0) g16 = getenv("AMG_RM_16") ? 1 : 0;  // measured a wash on C3: opt-in
-        if (mx > 8 && g16) {
-            const int gw = (int)std::min<int64_t>((nc + 15) / 16, 148LL * 32);
-            k_rm_small<VAL, 16><<<gw, 256, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, 8);
-            ++g_launches;
-            emin = 16;
-        }
-        CK(cudaGetLastError());
+        for (int k = 1; k < hash_from; ++k)
+            if (ncl[k]) {
+                k_rm_merge<VAL><<<grid_rows(ncl[k], kRMWarps, 148 * 16), 32 * kRMWarps, 0, s>>>(
+                    ncl[k], L(k), rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
+                ++g_launches;
+            }
     }
-    // rows of emin < E <= split: bitonic warp merge; split < E <= kRM: hash warp merge
-    static int split = -1;
-    if (split < 0) split = getenv("AMG_RM_SPLIT") ? std::min(kRM, atoi(getenv("AMG_RM_SPLIT"))) : 32;
-    if (mx > emin && split > emin) {
-        const int nb = (int)std::min<int64_t>((nc + kRMWarps - 1) / kRMWarps, 148LL * 16);
-        k_rm_merge<VAL><<<nb, 32 * kRMWarps, 0, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc,
-                                                     emin, split);
-        ++g_launches;
-        emin = split;
-    }
-    if (mx > emin) {
+    CK(cudaGetLastError());
+    {
         const size_t sm = sizeof(RhWarp<VAL>) * kRHWarps;
         static bool cfg = false;
         if (!cfg) {
             CK(cudaFuncSetAttribute(k_rm_hash<VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cfg = true;
         }
-        const int nb = (int)std::min<int64_t>((nc + kRHWarps - 1) / kRHWarps, 148LL * 3);
-        k_rm_hash<VAL><<<nb, 32 * kRHWarps, sm, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc,
-                                                     emin);
-        ++g_launches;
+        for (int k = hash_from; k <= 3; ++k)
+            if (ncl[k]) {
+                k_rm_hash<VAL><<<grid_rows(ncl[k], kRHWarps, 148 * 3), 32 * kRHWarps, sm, s>>>(
+                    ncl[k], L(k), rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
+                ++g_launches;
+            }
     }
     CK(cudaGetLastError());
-    if (mx > kRM) {  // list the wide rows, one CTA each
-        int* flag = dalloc<int>((size_t)nc + 1, s);
-        int* pos = dalloc<int>((size_t)nc + 1, s);
-        CK(cudaMemsetAsync(flag + nc, 0, sizeof(int), s));
-        k_wide_flags<<<grid_for(nc), kBlock, 0, s>>>(nc, eoff, kRM, flag);
-        ++g_launches;
-        const int nwide = (int)exclusive_scan_total(flag, pos, nc, s);
-        int* wide = dalloc<int>((size_t)nwide + 1, s);
-        k_scatter_flagged<<<grid_for(nc), kBlock, 0, s>>>(nc, flag, pos, wide);
-        ++g_launches;
+    if (ncl[4]) {  // the wide rows, one CTA each
         const size_t sm = (size_t)kRMB * (sizeof(unsigned long long) + sizeof(VAL));
         static bool cfg = false;
         if (!cfg) {
             CK(cudaFuncSetAttribute(k_rm_merge_block<VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cfg = true;
         }
-        const int g = nwide < 148 * 2 ? (nwide > 0 ? nwide : 1) : 148 * 2;
-        k_rm_merge_block<VAL><<<g, 256, sm, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, wide,
-                                                 nwide);
+        const int g = std::min(ncl[4], 148 * 2);
+        k_rm_merge_block<VAL><<<g, 256, sm, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, L(4),
+                                                 ncl[4]);
         ++g_launches;
         CK(cudaGetLastError());
-        dfree(flag, s);
-        dfree(pos, s);
-        dfree(wide, s);
     }
+    dfree(lists, s);
     int* nrp = dalloc<int>((size_t)nc + 1, s);
     const int64_t S = exclusive_scan_total(uc, nrp, nc, s);
     int* ocol = dalloc<int>((size_t)S + 8, s);
