@@ -686,57 +686,229 @@ static void quotient_impl(int n, int64_t nnz, const int* rp, const int* ci, cons
 // ------------------------------------------------------------------ row-merge quotient / Galerkin
 void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s);
 // Coarse row I is the merge of its members' rows (members = perm[aptr[I] .. aptr[I+1]), increasing
-// vertex order).  One warp per coarse row gathers the E <= 256 entries as keys (J = agg(col), k)
-// with k the entry's rank in (member, CSR position) order, bitonic-sorts them in shared memory,
-// and sums every run of equal J sequentially in k order -- the same order as the sequential
-// definition, so fp64 Galerkin values are bit-exact with it.  Rows with E > 256 (rare; only
-// very wide coarse rows) make the level fall back to the radix-sort path.
+// vertex order).  Two steps:
+//  1. staging: every fine row's entries, mapped (J = agg(col), value), are copied in perm order into
+//     one array, so coarse row I's E entries are the contiguous segment [S[aptr[I]], S[aptr[I+1]])
+//     in (member, CSR position) order -- the order k of the sequential definition;
+//  2. merge: each segment is reduced to its distinct J in place, by a kernel chosen by the row's
+//     size class (sub-warp shuffle/match merges, a warp bitonic or hash merge, one CTA for the
+//     widest).  Every run of equal J is summed sequentially in k order, so fp64 Galerkin values
+//     are bit-exact with the definition; fp64 rows come out sorted by J.  Pass-graph rows (uint32
+//     weights, integer sums) may come out in first-occurrence order: the matching is order free.
+// Rows with E > kRMB make the level fall back to the radix-sort path.
 constexpr int kRM = 256;          // entries per warp buffer
 constexpr int kRMWarps = 8;       // warps per block
+constexpr int kRMB = 4096;        // entries per CTA buffer (widest rows)
+constexpr int kRMClasses = 5;     // E <= 8 | <= 16 | <= 32 | <= kRM | <= kRMB
 
-// E[I] = entries of coarse row I before merging; rows are also sorted into size classes
-// (E <= 8, <= 16, <= 32, <= kRM, larger) by warp-aggregated appends to lists[c * nc ..]: each class
-// has its own kernel, and a row's output position comes from the scan of E, so the (run-dependent)
-// list order does not change any result.
-constexpr int kRMClasses = 5;
-__device__ __forceinline__ int rm_class(int e, int kmax) { return e <= 8 ? 0 : e <= 16 ? 1 : e <= 32 ? 2 : e <= kmax ? 3 : 4; }
-
-__global__ void k_rm_count(int nc, const int* __restrict__ rp, const int* __restrict__ perm,
-                           const int* __restrict__ aptr, int* __restrict__ E, int* __restrict__ emax,
-                           int* __restrict__ lists, int* __restrict__ counts, int kmax) {
-    int m = 0;
-    const int lane = threadIdx.x & 31;
-    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    for (int base = wid * 32; base < nc; base += nw * 32) {  // uniform trip count per warp
-        const int I = base + lane;
-        int c = -1;
-        if (I < nc) {
-            int e = 0;
-            for (int t = aptr[I]; t < aptr[I + 1]; ++t) e += rp[perm[t] + 1] - rp[perm[t]];
-            E[I] = e;
-            m = max(m, e);
-            c = rm_class(e, kmax);
-        }
-#pragma unroll
-        for (int k = 0; k < kRMClasses; ++k) {
-            const unsigned mk = __ballot_sync(0xffffffffu, c == k);
-            if (!mk) continue;
-            int b0 = 0;
-            if (lane == __ffs(mk) - 1) b0 = atomicAdd(counts + k, __popc(mk));
-            b0 = __shfl_sync(0xffffffffu, b0, __ffs(mk) - 1);
-            if (c == k) lists[(size_t)k * nc + b0 + __popc(mk & ((1u << lane) - 1u))] = I;
-        }
+// lenp[t] = row length of fine vertex perm[t]
+__global__ void k_stage_len(int n, const int* __restrict__ rp, const int* __restrict__ perm, int* __restrict__ lenp) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int v = perm[t];
+        lenp[t] = rp[v + 1] - rp[v];
     }
-    m = warp_max_i(m);
-    if (lane == 0) atomicMax(emax, m);
 }
 
+// One warp per 32 consecutive t: their entries are the contiguous range [S[t0], S[t0 + 32]); lane
+// writes position e (coalesced), its row found by a shuffle binary search over the 32 S values.
 template <class VAL>
-__global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                            const VAL* __restrict__ src, const int* __restrict__ agg,
-                                                            const int* __restrict__ perm, const int* __restrict__ aptr,
+__global__ void k_stage_fill(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                             const VAL* __restrict__ src, const int* __restrict__ agg, const int* __restrict__ perm,
+                             const int* __restrict__ S, unsigned* __restrict__ stJ, VAL* __restrict__ stv) {
+    const int lane = threadIdx.x & 31;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int t0 = wid * 32; t0 < n; t0 += nw * 32) {
+        const int t = t0 + lane;
+        const int st = t < n ? S[t] : S[n];
+        const int p0 = t < n ? rp[perm[t]] : 0;
+        const int sb = __shfl_sync(0xffffffffu, st, 0);
+        const int se = S[min(t0 + 32, n)];
+        const int nr = min(32, n - t0);
+        for (int eb = sb; eb < se; eb += 32) {  // warp-uniform bounds: every lane shuffles
+            const int e = eb + lane;
+            int m = 0;
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) {
+                const int sm = __shfl_sync(0xffffffffu, st, (m + w) & 31);
+                if (m + w < nr && sm <= e) m += w;
+            }
+            const int ps = __shfl_sync(0xffffffffu, p0, m) + (e - __shfl_sync(0xffffffffu, st, m));
+            if (e < se) {
+                stJ[e] = (unsigned)agg[ci[ps]];
+                stv[e] = src[ps];
+            }
+        }
+    }
+}
+
+// eoff[I] = segment start, E = its length; rows sorted into size classes by warp-aggregated appends
+// to lists[c * nc ..] (a row's output position comes from eoff, so the list order changes nothing)
+__device__ __forceinline__ int rm_class(int e) { return e <= 8 ? 0 : e <= 16 ? 1 : e <= 32 ? 2 : e <= kRM ? 3 : 4; }
+
+__global__ void __launch_bounds__(256) k_rm_classify(int nc, int n, const int* __restrict__ aptr,
+                                                     const int* __restrict__ S, int* __restrict__ eoff,
+                                                     int* __restrict__ emax, int* __restrict__ lists,
+                                                     int* __restrict__ counts) {
+    // one tile of 256 rows per iteration; per-class offsets: warp ballots -> block prefix in shared
+    // memory -> one global atomic per class per tile (a global atomic per warp serialised)
+    __shared__ int wc[8][kRMClasses];
+    __shared__ int gb[kRMClasses];
+    int mx = 0;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    for (int tile = blockIdx.x; tile * 256 < nc; tile += gridDim.x) {
+        const int I = tile * 256 + threadIdx.x;
+        int c = -1;
+        if (I < nc) {
+            const int e0 = S[aptr[I]], e = S[aptr[I + 1]] - e0;
+            eoff[I] = e0;
+            if (I == nc - 1) eoff[nc] = S[n];
+            mx = max(mx, e);
+            c = e > kRMB ? -1 : rm_class(e);
+        }
+        unsigned mk[kRMClasses];
+#pragma unroll
+        for (int k = 0; k < kRMClasses; ++k) {
+            mk[k] = __ballot_sync(0xffffffffu, c == k);
+            if (lane == 0) wc[wib][k] = __popc(mk[k]);
+        }
+        __syncthreads();
+        if (threadIdx.x < kRMClasses) {
+            const int k = threadIdx.x;
+            int acc = 0;
+            for (int w = 0; w < 8; ++w) { const int t = wc[w][k]; wc[w][k] = acc; acc += t; }
+            gb[k] = acc ? atomicAdd(counts + k, acc) : 0;
+        }
+        __syncthreads();
+        if (c >= 0) {
+            unsigned m = 0;
+#pragma unroll
+            for (int k = 0; k < kRMClasses; ++k) if (c == k) m = mk[k];
+            lists[(size_t)c * nc + gb[c] + wc[wib][c] + __popc(m & ((1u << lane) - 1u))] = I;
+        }
+        __syncthreads();
+    }
+    mx = warp_max_i(mx);
+    if (lane == 0) atomicMax(emax, mx);
+}
+
+// Class kernels.  In place: a row's segment [eoff[I], eoff[I+1]) is read whole before its distinct
+// entries are written to its first U slots; uc[I] = U.  `drop`: J == I (a self loop) is skipped.
+
+// E <= G, G lanes per row: lane t holds entry k = t.  An entry heads its run if no earlier entry has
+// the same J (found with __match_any_sync on (row slot, J)); the head sums its run in increasing k.
+// SORTED: output slot = number of heads with a smaller J (fp64 levels); else the number of heads
+// before it (first-occurrence order, pass graphs).
+template <class VAL, int G, bool SORTED>
+__global__ void __launch_bounds__(256) k_rm_small(int nl, const int* __restrict__ list, const int* __restrict__ eoff,
+                                                  bool drop, unsigned* __restrict__ stJ, VAL* __restrict__ stv,
+                                                  int* __restrict__ ucount) {
+    __shared__ VAL sv[256];
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, t = lane & (G - 1), gi = lane / G;
+    const unsigned NONE = 0xFFFFFFFFu;
+    const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    VAL* ws = sv + (threadIdx.x & ~31);
+    // list == nullptr: the class holds most rows, so walk all nl = nc rows in order (coalesced eoff,
+    // no list indirection) and skip the rows of other classes
+    const int elo = G == 8 ? -1 : G / 2;
+    for (int base = wid * GPW; base < nl; base += nw * GPW) {  // uniform trip count per warp
+        const int idx = base + gi;
+        bool mine = idx < nl;
+        const int I = mine ? (list ? list[idx] : idx) : 0;
+        const int e0 = mine ? eoff[I] : 0;
+        int E = mine ? eoff[I + 1] - e0 : 0;
+        if (!list && (E <= elo || E > G)) {
+            mine = false;
+            E = 0;
+        }
+        unsigned J = NONE;
+        VAL v = VAL(0);
+        if (t < E) {
+            const unsigned j = stJ[e0 + t];
+            v = stv[e0 + t];
+            J = (drop && j == (unsigned)I) ? NONE : j;
+        }
+        ws[lane] = v;
+        const unsigned long long key = ((unsigned long long)gi << 32) | J;
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const bool head = J != NONE && __ffs(grp) - 1 == lane;
+        const unsigned hb = __ballot_sync(0xffffffffu, head) & gm;
+        __syncwarp();
+        VAL acc = v;
+        if (head)
+            for (unsigned b = grp & (grp - 1); b; b &= b - 1) acc += ws[__ffs(b) - 1];
+        int slot;
+        if constexpr (SORTED) {
+            slot = 0;
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                const unsigned Jr = __shfl_sync(0xffffffffu, J, r, G);
+                if (((hb >> (gi * G + r)) & 1u) && Jr < J) ++slot;
+            }
+        } else {
+            slot = __popc(hb & ((1u << lane) - 1u));
+        }
+        if (head) {
+            stJ[e0 + slot] = J;
+            stv[e0 + slot] = acc;
+        }
+        if (mine && t == 0) ucount[I] = __popc(hb);
+        __syncwarp();
+    }
+}
+
+// Pass-graph rows of E <= K, one thread each (registers only: the warp versions above are bound by
+// the shuffle/match pipe at these sizes).  First-occurrence order, integer sums.  list == nullptr:
+// all nl = nc rows in order, rows of other classes skipped.
+template <int K>
+__global__ void __launch_bounds__(256) k_qg_thread(int nl, const int* __restrict__ list, const int* __restrict__ eoff,
+                                                   unsigned* __restrict__ stJ, uint32_t* __restrict__ stv,
+                                                   int* __restrict__ ucount) {
+    const unsigned NONE = 0xFFFFFFFFu;
+    const int elo = K == 8 ? -1 : K / 2;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nl; idx += gridDim.x * blockDim.x) {
+        const int I = list ? list[idx] : idx;
+        const int e0 = eoff[I], E = eoff[I + 1] - e0;
+        if (!list && (E <= elo || E > K)) continue;
+        unsigned J[K];
+        uint32_t w[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            J[k] = NONE;
+            w[k] = 0;
+            if (k < E) {
+                const unsigned j = stJ[e0 + k];
+                w[k] = stv[e0 + k];
+                J[k] = j == (unsigned)I ? NONE : j;
+            }
+        }
+        int u = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            bool head = J[k] != NONE;
+            uint32_t acc = w[k];
+#pragma unroll
+            for (int r = 0; r < K; ++r) {
+                if (r < k && J[r] == J[k]) head = false;
+                if (r > k && J[r] == J[k]) acc += w[r];
+            }
+            if (head) {
+                stJ[e0 + u] = J[k];
+                stv[e0 + u] = acc;
+                ++u;
+            }
+        }
+        ucount[I] = u;
+    }
+}
+
+// kRM-entry rows, one warp each: keys (J, k) bitonic-sorted in shared memory, runs of equal J
+// summed in k order (sorted output)
+template <class VAL>
+__global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* __restrict__ list,
                                                             const int* __restrict__ eoff, bool drop,
-                                                            int* __restrict__ tcol, VAL* __restrict__ tval,
+                                                            unsigned* __restrict__ stJ, VAL* __restrict__ stv,
                                                             int* __restrict__ ucount) {
     __shared__ unsigned long long skey[kRMWarps][kRM];
     __shared__ VAL sval[kRMWarps][kRM];
@@ -747,38 +919,16 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* _
     for (int r = blockIdx.x * kRMWarps + wib; r < nl; r += nwarp) {
         const int I = list[r];
         const int e0 = eoff[I], E = eoff[I + 1] - e0;
-        // gather in (member, position) order, k = running rank; members are spread over the lanes
-        // (one member per lane, a warp prefix sum of their row lengths gives each its first k)
-        const int t0 = aptr[I], t1 = aptr[I + 1];
-        int kbase = 0;
-        for (int tc = t0; tc < t1; tc += 32) {
-            const int t = tc + lane;
-            int p0 = 0, len = 0;
-            if (t < t1) {
-                const int v = perm[t];
-                p0 = rp[v];
-                len = rp[v + 1] - p0;
-            }
-            int incl = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int kk = kbase + incl - len;
-            for (int q = 0; q < len; ++q) {
-                const int J = agg[ci[p0 + q]];
-                const unsigned long long hi = (drop && J == I) ? 0xFFFFFFFFull : (unsigned long long)(unsigned)J;
-                key[kk + q] = (hi << 32) | (unsigned)(kk + q);
-                val[kk + q] = src[p0 + q];
-            }
-            kbase += __shfl_sync(0xffffffffu, incl, 31);
+        for (int q = lane; q < E; q += 32) {
+            const unsigned J = stJ[e0 + q];
+            const unsigned long long hi = (drop && J == (unsigned)I) ? 0xFFFFFFFFull : (unsigned long long)J;
+            key[q] = (hi << 32) | (unsigned)q;
+            val[q] = stv[e0 + q];
         }
         int P = 1;
         while (P < E) P <<= 1;
         for (int q = E + lane; q < P; q += 32) key[q] = ~0ull;
         __syncwarp();
-        // bitonic sort of key[0..P) (ascending)
         for (int size = 2; size <= P; size <<= 1) {
             for (int stride = size >> 1; stride > 0; stride >>= 1) {
                 for (int q = lane; q < P; q += 32) {
@@ -792,7 +942,6 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* _
                 __syncwarp();
             }
         }
-        // runs of equal J: heads, ranks, sequential sums in k order
         int base = 0;
         for (int q0 = 0; q0 < E; q0 += 32) {
             const int q = q0 + lane;
@@ -806,9 +955,10 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* _
             if (head) {
                 const int slot = e0 + base + __popc(hm & ((1u << lane) - 1));
                 VAL acc = val[(unsigned)(key[q] & 0xFFFFFFFFull)];
-                for (int r = q + 1; r < E && (unsigned)(key[r] >> 32) == J; ++r) acc += val[(unsigned)(key[r] & 0xFFFFFFFFull)];
-                tcol[slot] = (int)J;
-                tval[slot] = acc;
+                for (int r2 = q + 1; r2 < E && (unsigned)(key[r2] >> 32) == J; ++r2)
+                    acc += val[(unsigned)(key[r2] & 0xFFFFFFFFull)];
+                stJ[slot] = J;
+                stv[slot] = acc;
             }
             base += __popc(hm);
         }
@@ -817,15 +967,11 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* _
     }
 }
 
-
-// Sort-free warp merge (the default for emin < E <= kRM): the warp walks the row's entries in
-// (member, CSR position) order, 32 at a time (lane = entry within the chunk, its member found by a
-// shuffle binary search over the members' first ranks).  __match_any_sync groups the chunk's
-// entries by J; the group's lowest lane looks J up in a per-warp shared-memory hash table
-// (open addressing, 2 kRM slots) and adds the group's values to J's accumulator one at a time in
-// lane order.  Every accumulator therefore sees its entries in increasing k, the sequential order,
-// so fp64 sums are bit-exact with the definition (the first entry initialises it, so -0.0 survives).
-// The U distinct J are then ranked by counting (columns come out sorted) and written.
+// Sort-free warp merge for E <= kRM: chunks of 32 entries in k order; __match_any_sync groups a
+// chunk's equal J; the group's first lane finds J in a per-warp shared-memory hash table (open
+// addressing, 2 kRM slots) and adds the group's values to J's accumulator one at a time in lane
+// order, so every accumulator sees its entries in increasing k (the first initialises it, so -0.0
+// survives).  The U distinct J are then ranked by counting (sorted output) and written.
 constexpr int kRHWarps = 8;
 constexpr int kRHSlots = 2 * kRM;
 template <class VAL>
@@ -839,11 +985,9 @@ struct RhWarp {
 };
 
 template <class VAL>
-__global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                           const VAL* __restrict__ src, const int* __restrict__ agg,
-                                                           const int* __restrict__ perm, const int* __restrict__ aptr,
+__global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __restrict__ list,
                                                            const int* __restrict__ eoff, bool drop,
-                                                           int* __restrict__ tcol, VAL* __restrict__ tval,
+                                                           unsigned* __restrict__ stJ, VAL* __restrict__ stv,
                                                            int* __restrict__ ucount) {
     extern __shared__ __align__(16) unsigned char rh_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -855,72 +999,44 @@ __global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __
     const int nwarp = gridDim.x * kRHWarps;
     for (int r = blockIdx.x * kRHWarps + wib; r < nl; r += nwarp) {
         const int I = list[r];
-        const int e0 = eoff[I];
-        const int t1 = aptr[I + 1];
-        for (int tb = aptr[I]; tb < t1; tb += 32) {  // blocks of <= 32 members
-            const int Mb = min(32, t1 - tb);
-            int p0 = 0, len = 0;
-            if (lane < Mb) {
-                const int v = perm[tb + lane];
-                p0 = rp[v];
-                len = rp[v + 1] - p0;
+        const int e0 = eoff[I], E = eoff[I + 1] - e0;
+        for (int c = 0; c < E; c += 32) {
+            const int k = c + lane;
+            unsigned J = NONE;
+            VAL v = VAL(0);
+            if (k < E) {
+                const unsigned j = stJ[e0 + k];
+                v = stv[e0 + k];
+                J = (drop && j == (unsigned)I) ? NONE : j;
             }
-            int incl = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+            W.sv[lane] = v;
+            const unsigned grp = __match_any_sync(0xffffffffu, J);
+            __syncwarp();
+            if (J != NONE && __ffs(grp) - 1 == lane) {
+                unsigned h = (J * 2654435761u) >> (32 - 9);
+                bool fresh;
+                for (;;) {
+                    const unsigned old = atomicCAS(&W.hk[h], NONE, J);
+                    if (old == NONE) { fresh = true; break; }
+                    if (old == J) { fresh = false; break; }
+                    h = (h + 1) & (kRHSlots - 1);
+                }
+                unsigned bits = grp;
+                VAL a;
+                if (fresh) {
+                    a = W.sv[lane];
+                    bits &= bits - 1;
+                    W.list[atomicAdd(&W.cnt, 1)] = (int)h;
+                } else {
+                    a = W.hv[h];
+                }
+                while (bits) {
+                    a += W.sv[__ffs(bits) - 1];
+                    bits &= bits - 1;
+                }
+                W.hv[h] = a;
             }
-            const int kb = incl - len;  // first rank of member `lane` within the block
-            const int Eb = __shfl_sync(0xffffffffu, incl, 31);
-            for (int c = 0; c < Eb; c += 32) {
-                const int k = c + lane;
-                // member m = largest m < Mb with kb[m] <= k (empty members are skipped over)
-                int m = 0;
-#pragma unroll
-                for (int st = 16; st > 0; st >>= 1) {
-                    const int kbs = __shfl_sync(0xffffffffu, kb, (m + st) & 31);
-                    if (m + st < Mb && kbs <= k) m += st;
-                }
-                const int pm = __shfl_sync(0xffffffffu, p0, m);
-                const int km = __shfl_sync(0xffffffffu, kb, m);
-                unsigned J = NONE;
-                VAL v = VAL(0);
-                if (k < Eb) {
-                    const int pos = pm + (k - km);
-                    const unsigned j = (unsigned)agg[ci[pos]];
-                    v = src[pos];
-                    J = (drop && j == (unsigned)I) ? NONE : j;
-                }
-                W.sv[lane] = v;
-                const unsigned grp = __match_any_sync(0xffffffffu, J);
-                __syncwarp();
-                if (J != NONE && __ffs(grp) - 1 == lane) {
-                    unsigned h = (J * 2654435761u) >> (32 - 9);
-                    bool fresh;
-                    for (;;) {
-                        const unsigned old = atomicCAS(&W.hk[h], NONE, J);
-                        if (old == NONE) { fresh = true; break; }
-                        if (old == J) { fresh = false; break; }
-                        h = (h + 1) & (kRHSlots - 1);
-                    }
-                    unsigned bits = grp;
-                    VAL a;
-                    if (fresh) {
-                        a = W.sv[lane];
-                        bits &= bits - 1;
-                        W.list[atomicAdd(&W.cnt, 1)] = (int)h;
-                    } else {
-                        a = W.hv[h];
-                    }
-                    while (bits) {
-                        a += W.sv[__ffs(bits) - 1];
-                        bits &= bits - 1;
-                    }
-                    W.hv[h] = a;
-                }
-                __syncwarp();
-            }
+            __syncwarp();
         }
         const int U = W.cnt;
         for (int u = lane; u < U; u += 32) W.lj[u] = W.hk[W.list[u]];
@@ -928,10 +1044,10 @@ __global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __
         for (int u = lane; u < U; u += 32) {
             const unsigned J = W.lj[u];
             int rank = 0;
-            for (int r = 0; r < U; ++r) rank += W.lj[r] < J;
+            for (int q = 0; q < U; ++q) rank += W.lj[q] < J;
             const int h = W.list[u];
-            tcol[e0 + rank] = (int)J;
-            tval[e0 + rank] = W.hv[h];
+            stJ[e0 + rank] = J;
+            stv[e0 + rank] = W.hv[h];
             W.hk[h] = NONE;
         }
         if (lane == 0) {
@@ -942,34 +1058,25 @@ __global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __
     }
 }
 
-// Same merge for the rare wide coarse rows (kRM < E <= kRMB), one 256-thread CTA per row with the
-// buffers in dynamic shared memory.
-constexpr int kRMB = 4096;
+// the widest rows (kRM < E <= kRMB), one 256-thread CTA each: the bitonic merge in dynamic shared
+// memory
 template <class VAL>
-__global__ void __launch_bounds__(256) k_rm_merge_block(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                        const VAL* __restrict__ src, const int* __restrict__ agg,
-                                                        const int* __restrict__ perm, const int* __restrict__ aptr,
+__global__ void __launch_bounds__(256) k_rm_merge_block(int nl, const int* __restrict__ list,
                                                         const int* __restrict__ eoff, bool drop,
-                                                        int* __restrict__ tcol, VAL* __restrict__ tval,
-                                                        int* __restrict__ ucount, const int* __restrict__ wide,
-                                                        int nwide) {
+                                                        unsigned* __restrict__ stJ, VAL* __restrict__ stv,
+                                                        int* __restrict__ ucount) {
     extern __shared__ __align__(16) unsigned char rmb_raw[];
     unsigned long long* key = reinterpret_cast<unsigned long long*>(rmb_raw);
     VAL* val = reinterpret_cast<VAL*>(key + kRMB);
     __shared__ int wsum[9];
-    for (int wi = blockIdx.x; wi < nwide; wi += gridDim.x) {
-        const int I = wide[wi];
+    for (int wi = blockIdx.x; wi < nl; wi += gridDim.x) {
+        const int I = list[wi];
         const int e0 = eoff[I], E = eoff[I + 1] - e0;
-        int k = 0;
-        for (int t = aptr[I]; t < aptr[I + 1]; ++t) {
-            const int v = perm[t], p0 = rp[v], len = rp[v + 1] - p0;
-            for (int q = threadIdx.x; q < len; q += blockDim.x) {
-                const int J = agg[ci[p0 + q]];
-                const unsigned long long hi = (drop && J == I) ? 0xFFFFFFFFull : (unsigned long long)(unsigned)J;
-                key[k + q] = (hi << 32) | (unsigned)(k + q);
-                val[k + q] = src[p0 + q];
-            }
-            k += len;
+        for (int q = threadIdx.x; q < E; q += blockDim.x) {
+            const unsigned J = stJ[e0 + q];
+            const unsigned long long hi = (drop && J == (unsigned)I) ? 0xFFFFFFFFull : (unsigned long long)J;
+            key[q] = (hi << 32) | (unsigned)q;
+            val[q] = stv[e0 + q];
         }
         int P = 1;
         while (P < E) P <<= 1;
@@ -987,7 +1094,6 @@ __global__ void __launch_bounds__(256) k_rm_merge_block(int nc, const int* __res
                 }
                 __syncthreads();
             }
-        // heads and ranks in chunks of blockDim (block-wide exclusive count via per-warp popc)
         int base = 0;
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         for (int q0 = 0; q0 < E; q0 += blockDim.x) {
@@ -1011,8 +1117,8 @@ __global__ void __launch_bounds__(256) k_rm_merge_block(int nc, const int* __res
                 const int slot = e0 + base + wsum[wid] + __popc(hm & ((1u << lane) - 1));
                 VAL acc = val[(unsigned)(key[q] & 0xFFFFFFFFull)];
                 for (int r = q + 1; r < E && (unsigned)(key[r] >> 32) == J; ++r) acc += val[(unsigned)(key[r] & 0xFFFFFFFFull)];
-                tcol[slot] = (int)J;
-                tval[slot] = acc;
+                stJ[slot] = J;
+                stv[slot] = acc;
             }
             base += wsum[8];
             __syncthreads();
@@ -1022,198 +1128,40 @@ __global__ void __launch_bounds__(256) k_rm_merge_block(int nc, const int* __res
     }
 }
 
-__global__ void k_wide_flags(int nc, const int* __restrict__ eoff, int lim, int* __restrict__ flag) {
-    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x)
-        flag[I] = (eoff[I + 1] - eoff[I]) > lim;
-}
-
-__global__ void k_scatter_flagged(int n, const int* __restrict__ flag, const int* __restrict__ pos, int* __restrict__ out) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        if (flag[i]) out[pos[i]] = i;
-}
-
 template <class VAL>
 __global__ void k_rm_compact(int nc, const int* __restrict__ eoff, const int* __restrict__ orp,
-                             const int* __restrict__ tcol, const VAL* __restrict__ tval, int* __restrict__ ocol,
+                             const unsigned* __restrict__ tcol, const VAL* __restrict__ tval, int* __restrict__ ocol,
                              VAL* __restrict__ oval) {
     for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
         const int src = eoff[I], dst = orp[I], u = orp[I + 1] - orp[I];
         for (int r = 0; r < u; ++r) {
-            ocol[dst + r] = tcol[src + r];
+            ocol[dst + r] = (int)tcol[src + r];
             oval[dst + r] = tval[src + r];
         }
     }
 }
 
-// Coarse rows with E <= G entries, G lanes per row (32 / G rows per warp), no sort: lane t holds
-// entry k = t of the (member, CSR position) order; an entry is a run head if no earlier entry has the
-// same J; the head sums its run in increasing k (the sequential order: bit-exact); its output slot
-// is the number of heads with a smaller J (columns come out sorted).  Rows with E > G are skipped.
-template <class VAL, int G>
-__global__ void __launch_bounds__(256) k_rm_small(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                  const VAL* __restrict__ src, const int* __restrict__ agg,
-                                                  const int* __restrict__ perm, const int* __restrict__ aptr,
-                                                  const int* __restrict__ eoff, bool drop, int* __restrict__ tcol,
-                                                  VAL* __restrict__ tval, int* __restrict__ ucount) {
-    constexpr int GPW = 32 / G;  // rows per warp
-    const int lane = threadIdx.x & 31;
-    const int t = lane & (G - 1);
-    const unsigned NONE = 0xFFFFFFFFu;
-    const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const int wstride = ((gridDim.x * blockDim.x) >> 5) * GPW;
-    // the warp's rows share one trip count (full-mask shuffles below)
-    for (int wb = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW; wb < nl; wb += wstride) {
-        const int idx = wb + lane / G;
-        const bool mine = idx < nl;
-        const int I = mine ? list[idx] : 0;
-        const int e0 = mine ? eoff[I] : 0;
-        // members of the aggregate: lane t < M holds member t's first position and row length
-        const int t0 = mine ? aptr[I] : 0;
-        const int M = mine ? aptr[I + 1] - t0 : 0;
-        int p0 = 0, len = 0;
-        if (t < M) {
-            const int v = perm[t0 + t];
-            p0 = rp[v];
-            len = rp[v + 1] - p0;
-        }
-        int incl = len;
-#pragma unroll
-        for (int o = 1; o < G; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o, G);
-            if (t >= o) incl += y;
-        }
-        const int kb = incl - len;
-        // entry k = t: its member and CSR position
-        int pos = -1;
-#pragma unroll
-        for (int m = 0; m < G; ++m) {
-            const int kbm = __shfl_sync(0xffffffffu, kb, m, G);
-            const int lnm = __shfl_sync(0xffffffffu, len, m, G);
-            const int pm = __shfl_sync(0xffffffffu, p0, m, G);
-            if (m < M && t >= kbm && t < kbm + lnm) pos = pm + (t - kbm);
-        }
-        unsigned J = NONE;
-        VAL val = VAL(0);
-        if (mine && pos >= 0) {
-            const unsigned j = (unsigned)agg[ci[pos]];
-            val = src[pos];
-            J = (drop && j == (unsigned)I) ? NONE : j;
-        }
-        // run head = first entry (in k order) of its J; the head sums its run in increasing k
-        bool head = J != NONE;
-        VAL acc = val;
-#pragma unroll
-        for (int r = 0; r < G; ++r) {
-            const unsigned Jr = __shfl_sync(0xffffffffu, J, r, G);
-            const VAL vr = __shfl_sync(0xffffffffu, val, r, G);
-            if (Jr == J && r < t) head = false;
-            if (Jr == J && r > t) acc += vr;
-        }
-        // output slot = number of heads with a smaller J (columns sorted)
-        int rank = 0;
-#pragma unroll
-        for (int r = 0; r < G; ++r) {
-            const unsigned Jr = __shfl_sync(0xffffffffu, J, r, G);
-            const int hr = __shfl_sync(0xffffffffu, (int)head, r, G);
-            if (hr && Jr < J) ++rank;
-        }
-        const unsigned hb = __ballot_sync(0xffffffffu, head && mine);
-        if (head && mine) {
-            tcol[e0 + rank] = (int)J;
-            tval[e0 + rank] = acc;
-        }
-        if (mine && t == 0) ucount[I] = __popc(hb & gm);
-    }
-}
-
-// Pass-graph rows (uint32 weights: integer sums, so neither the summation order nor the column order
-// matters to the matching, whose keys are order free) with emin < E <= G: G lanes per row, lane t =
-// entry t in (member, CSR position) order (member by a shuffle binary search), __match_any_sync on
-// (row slot, J) groups equal J, the group's first lane sums it and takes output slot = number of
-// group heads before it (first-occurrence order: deterministic, unsorted).
-template <int G>
-__global__ void __launch_bounds__(256) k_qg_small(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                  const uint32_t* __restrict__ src, const int* __restrict__ agg,
-                                                  const int* __restrict__ perm, const int* __restrict__ aptr,
-                                                  const int* __restrict__ eoff, int* __restrict__ tcol,
-                                                  uint32_t* __restrict__ tval, int* __restrict__ ucount) {
-    __shared__ uint32_t sw[256];
-    constexpr int GPW = 32 / G;
-    const int lane = threadIdx.x & 31, t = lane & (G - 1), gi = lane / G;
-    const unsigned NONE = 0xFFFFFFFFu;
-    const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
-    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    uint32_t* ws = sw + (threadIdx.x & ~31);
-    for (int base = wid * GPW; base < nl; base += nw * GPW) {
-        const int idx = base + gi;
-        const bool mine = idx < nl;
-        const int I = mine ? list[idx] : 0;
-        const int e0 = mine ? eoff[I] : 0;
-        const int E = mine ? eoff[I + 1] - e0 : 0;
-        const int t0 = mine ? aptr[I] : 0;
-        const int M = mine ? aptr[I + 1] - t0 : 0;
-        int p0 = 0, len = 0;
-        if (t < M) {
-            const int v = perm[t0 + t];
-            p0 = rp[v];
-            len = rp[v + 1] - p0;
-        }
-        int incl = len;
-#pragma unroll
-        for (int o = 1; o < G; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o, G);
-            if (t >= o) incl += y;
-        }
-        const int kb = incl - len;
-        int m = 0;
-#pragma unroll
-        for (int st = G / 2; st > 0; st >>= 1) {
-            const int kbs = __shfl_sync(0xffffffffu, kb, (m + st) & (G - 1), G);
-            if (m + st < M && kbs <= t) m += st;
-        }
-        const int pm = __shfl_sync(0xffffffffu, p0, m, G);
-        const int km = __shfl_sync(0xffffffffu, kb, m, G);
-        unsigned J = NONE;
-        uint32_t wv = 0;
-        if (mine && t < E) {
-            const int pos = pm + (t - km);
-            const unsigned j = (unsigned)agg[ci[pos]];
-            wv = src[pos];
-            J = j == (unsigned)I ? NONE : j;
-        }
-        ws[lane] = wv;
-        const unsigned long long key = ((unsigned long long)gi << 32) | J;
-        const unsigned grp = __match_any_sync(0xffffffffu, key);
-        const bool head = J != NONE && __ffs(grp) - 1 == lane;
-        const unsigned hb = __ballot_sync(0xffffffffu, head) & gm;
-        __syncwarp();
-        if (head) {
-            uint32_t acc = 0;
-            for (unsigned b = grp; b; b &= b - 1) acc += ws[__ffs(b) - 1];
-            const int slot = __popc(hb & ((1u << lane) - 1u));
-            tcol[e0 + slot] = (int)J;
-            tval[e0 + slot] = acc;
-        }
-        if (mine && t == 0) ucount[I] = __popc(hb);
-        __syncwarp();
-    }
-}
-
-// returns false (nothing allocated) if some coarse row has more than kRM entries
+// returns false (nothing allocated) if some coarse row has more than kRMB entries
 template <class VAL>
 static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg, int nc,
                               bool drop, const int* perm, const int* aptr, int** orp, int** oci, VAL** oval,
                               int64_t* onnz, cudaStream_t s) {
-    (void)n;
     (void)nnz;
-    int* E = dalloc<int>((size_t)nc + 1, s);
+    // 1. staging offsets S (perm order) and the staged entries
+    int* S = dalloc<int>((size_t)n + 1, s);
+    {
+        int* lenp = dalloc<int>((size_t)n + 1, s);
+        CK(cudaMemsetAsync(lenp + n, 0, sizeof(int), s));
+        k_stage_len<<<grid_for(n), kBlock, 0, s>>>(n, rp, perm, lenp);
+        ++g_launches;
+        exclusive_scan_total(lenp, S, n, s);
+        dfree(lenp, s);
+    }
     int* cnt = dalloc<int>(8, s);  // emax, counts[5]
     int* lists = dalloc<int>((size_t)kRMClasses * nc + 1, s);
+    int* eoff = dalloc<int>((size_t)nc + 1, s);
     CK(cudaMemsetAsync(cnt, 0, 8 * sizeof(int), s));
-    CK(cudaMemsetAsync(E + nc, 0, sizeof(int), s));
-    static int split = -1;  // AMG_RM_SPLIT=16: rows of 16 < E <= 32 also go to the hash merge
-    if (split < 0) split = getenv("AMG_RM_SPLIT") ? atoi(getenv("AMG_RM_SPLIT")) : 32;
-    k_rm_count<<<grid_red(nc), kBlock, 0, s>>>(nc, rp, perm, aptr, E, cnt, lists, cnt + 1, kRM);
+    k_rm_classify<<<std::max(1, std::min((nc + 255) / 256, 148 * 8)), 256, 0, s>>>(nc, n, aptr, S, eoff, cnt, lists, cnt + 1);
     ++g_launches;
     CK(cudaGetLastError());
     int* hc = static_cast<int*>(pinned_scratch()) + 40;
@@ -1224,43 +1172,72 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
     for (int k = 0; k < kRMClasses; ++k) ncl[k] = hc[1 + k];
     dfree(cnt, s);
     if (mx > kRMB) {
-        dfree(E, s);
+        dfree(S, s);
         dfree(lists, s);
+        dfree(eoff, s);
         return false;
     }
+    int tot = 0;
+    CK(cudaMemcpyAsync(&tot, eoff + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    unsigned* stJ = dalloc<unsigned>((size_t)tot + 8, s);
+    VAL* stv = dalloc<VAL>((size_t)tot + 8, s);
+    {
+        const int g = std::max(1, std::min((n + 255) / 256, 148 * 16));
+        k_stage_fill<VAL><<<g, 256, 0, s>>>(n, rp, ci, src, agg, perm, S, stJ, stv);
+        ++g_launches;
+        CK(cudaGetLastError());
+    }
+    dfree(S, s);
     auto L = [&](int k) { return lists + (size_t)k * nc; };
-    int* eoff = dalloc<int>((size_t)nc + 1, s);
-    const int64_t tot = exclusive_scan_total(E, eoff, nc, s);
-    int* tcol = dalloc<int>((size_t)tot + 8, s);
-    VAL* tval = dalloc<VAL>((size_t)tot + 8, s);
-    int* uc = E;  // reuse: unique counts
+    int* uc = dalloc<int>((size_t)nc + 1, s);
     CK(cudaMemsetAsync(uc + nc, 0, sizeof(int), s));
     auto grid_rows = [](int nrows, int rows_per_block, int cap) {
         return (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)nrows + rows_per_block - 1) / rows_per_block, cap));
     };
-    // class kernels: E <= 8 | <= 16 | <= 32: sub-warp merges (pass graphs: unsorted k_qg_small; fp64:
-    // k_rm_small for <= 8, the bitonic warp merge above); <= kRM: the hash warp merge; wider: one CTA
+    // 2. class kernels.  Pass graphs: unsorted sub-warp merges up to 32 entries.  fp64: sorted
+    // sub-warp merge up to 8, the bitonic warp merge up to 32 (AMG_RM_SPLIT=8|16 moves the rows
+    // above it to the hash merge); the hash warp merge up to kRM; one CTA above.
+    static int split = -1;
+    if (split < 0) split = getenv("AMG_RM_SPLIT") ? atoi(getenv("AMG_RM_SPLIT")) : 32;
     bool pass_graph = false;
     if constexpr (std::is_same<VAL, uint32_t>::value) pass_graph = drop;
-    int hash_from = 3;  // first class sent to the hash merge
-    if (split <= 16) hash_from = 2;
-    if (split <= 8) hash_from = 1;
-    if constexpr (std::is_same<VAL, uint32_t>::value) {
-        if (pass_graph) {
-            if (ncl[0]) k_qg_small<8><<<grid_rows(ncl[0], 32, 148 * 32), 256, 0, s>>>(ncl[0], L(0), rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc);
-            if (ncl[1]) k_qg_small<16><<<grid_rows(ncl[1], 16, 148 * 32), 256, 0, s>>>(ncl[1], L(1), rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc);
-            if (ncl[2]) k_qg_small<32><<<grid_rows(ncl[2], 8, 148 * 32), 256, 0, s>>>(ncl[2], L(2), rp, ci, src, agg, perm, aptr, eoff, tcol, tval, uc);
-            g_launches += 3;
-            hash_from = 3;
+    int hash_from = 3;
+    // a class with more than half the rows walks all rows in order (list == nullptr)
+    auto LL = [&](int k, int* nrows) -> const int* {
+        if (2 * (int64_t)ncl[k] > nc) { *nrows = nc; return nullptr; }
+        *nrows = ncl[k];
+        return L(k);
+    };
+    if (pass_graph) {
+        int nr;
+        const int* l;
+        static int qthr = -1;
+        if (qthr < 0) qthr = getenv("AMG_QG_WARP") ? 0 : 1;
+        if (qthr) {
+            if constexpr (std::is_same<VAL, uint32_t>::value) {
+                if (ncl[0]) { l = LL(0, &nr); k_qg_thread<8><<<grid_rows(nr, 256, 148 * 16), 256, 0, s>>>(nr, l, eoff, stJ, stv, uc); }
+                if (ncl[1]) { l = LL(1, &nr); k_qg_thread<16><<<grid_rows(nr, 256, 148 * 16), 256, 0, s>>>(nr, l, eoff, stJ, stv, uc); }
+            }
+        } else {
+            if (ncl[0]) { l = LL(0, &nr); k_rm_small<VAL, 8, false><<<grid_rows(nr, 32, 148 * 32), 256, 0, s>>>(nr, l, eoff, drop, stJ, stv, uc); }
+            if (ncl[1]) { l = LL(1, &nr); k_rm_small<VAL, 16, false><<<grid_rows(nr, 16, 148 * 32), 256, 0, s>>>(nr, l, eoff, drop, stJ, stv, uc); }
         }
-    }
-    if (!pass_graph) {
-        if (ncl[0]) k_rm_small<VAL, 8><<<grid_rows(ncl[0], 32, 148 * 32), 256, 0, s>>>(ncl[0], L(0), rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
+        if (ncl[2]) { l = LL(2, &nr); k_rm_small<VAL, 32, false><<<grid_rows(nr, 8, 148 * 32), 256, 0, s>>>(nr, l, eoff, drop, stJ, stv, uc); }
+        g_launches += 3;
+    } else {
+        if (split <= 16) hash_from = 2;
+        if (split <= 8) hash_from = 1;
+        if (ncl[0]) {
+            int nr;
+            const int* l = LL(0, &nr);
+            k_rm_small<VAL, 8, true><<<grid_rows(nr, 32, 148 * 32), 256, 0, s>>>(nr, l, eoff, drop, stJ, stv, uc);
+        }
         ++g_launches;
         for (int k = 1; k < hash_from; ++k)
             if (ncl[k]) {
-                k_rm_merge<VAL><<<grid_rows(ncl[k], kRMWarps, 148 * 16), 32 * kRMWarps, 0, s>>>(
-                    ncl[k], L(k), rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
+                k_rm_merge<VAL><<<grid_rows(ncl[k], kRMWarps, 148 * 16), 32 * kRMWarps, 0, s>>>(ncl[k], L(k), eoff, drop,
+                                                                                                 stJ, stv, uc);
                 ++g_launches;
             }
     }
@@ -1274,43 +1251,42 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
         }
         for (int k = hash_from; k <= 3; ++k)
             if (ncl[k]) {
-                k_rm_hash<VAL><<<grid_rows(ncl[k], kRHWarps, 148 * 3), 32 * kRHWarps, sm, s>>>(
-                    ncl[k], L(k), rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc);
+                k_rm_hash<VAL><<<grid_rows(ncl[k], kRHWarps, 148 * 3), 32 * kRHWarps, sm, s>>>(ncl[k], L(k), eoff, drop,
+                                                                                               stJ, stv, uc);
                 ++g_launches;
             }
     }
     CK(cudaGetLastError());
-    if (ncl[4]) {  // the wide rows, one CTA each
+    if (ncl[4]) {
         const size_t sm = (size_t)kRMB * (sizeof(unsigned long long) + sizeof(VAL));
         static bool cfg = false;
         if (!cfg) {
             CK(cudaFuncSetAttribute(k_rm_merge_block<VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cfg = true;
         }
-        const int g = std::min(ncl[4], 148 * 2);
-        k_rm_merge_block<VAL><<<g, 256, sm, s>>>(nc, rp, ci, src, agg, perm, aptr, eoff, drop, tcol, tval, uc, L(4),
-                                                 ncl[4]);
+        k_rm_merge_block<VAL><<<std::min(ncl[4], 148 * 2), 256, sm, s>>>(ncl[4], L(4), eoff, drop, stJ, stv, uc);
         ++g_launches;
         CK(cudaGetLastError());
     }
     dfree(lists, s);
+    // 3. compact the merged segments into the coarse CSR
     int* nrp = dalloc<int>((size_t)nc + 1, s);
-    const int64_t S = exclusive_scan_total(uc, nrp, nc, s);
-    int* ocol = dalloc<int>((size_t)S + 8, s);
-    VAL* ov = dalloc<VAL>((size_t)S + 8, s);
-    CK(cudaMemsetAsync(ocol + S, 0, 8 * sizeof(int), s));
-    CK(cudaMemsetAsync(ov + S, 0, 8 * sizeof(VAL), s));
-    k_rm_compact<VAL><<<grid_for(nc), kBlock, 0, s>>>(nc, eoff, nrp, tcol, tval, ocol, ov);
+    const int64_t Sn = exclusive_scan_total(uc, nrp, nc, s);
+    int* ocol = dalloc<int>((size_t)Sn + 8, s);
+    VAL* ov = dalloc<VAL>((size_t)Sn + 8, s);
+    CK(cudaMemsetAsync(ocol + Sn, 0, 8 * sizeof(int), s));
+    CK(cudaMemsetAsync(ov + Sn, 0, 8 * sizeof(VAL), s));
+    k_rm_compact<VAL><<<grid_for(nc), kBlock, 0, s>>>(nc, eoff, nrp, stJ, stv, ocol, ov);
     ++g_launches;
     CK(cudaGetLastError());
-    dfree(tcol, s);
-    dfree(tval, s);
+    dfree(stJ, s);
+    dfree(stv, s);
     dfree(eoff, s);
-    dfree(E, s);
+    dfree(uc, s);
     *orp = nrp;
     *oci = ocol;
     *oval = ov;
-    *onnz = S;
+    *onnz = Sn;
     return true;
 }
 
