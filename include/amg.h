@@ -86,7 +86,10 @@ typedef struct {
     int32_t  lanczos_steps; /* 0 = lambda_1 = ||A_l||_inf (default); k > 0 = reading A24
                                (SURVEY 8(f) item 3): lambda_1 = min(||A_l||_inf, 1.1 theta_k), theta_k the
                                largest Ritz value of k Lanczos steps (smoothed levels; amg_setup only) */
-    int32_t  reserved32;
+    int32_t  mis_k;         /* 0 = p passes of pairwise matching (default); k >= 1 = reading A25 (SURVEY
+                               8(f) item 2): each level is aggregated once by the MIS of
+                               the graph of A^k grown into neighbourhood aggregates, p is ignored; k <= 8,
+                               amg_setup only */
     int64_t  reserved[1];
 } amg_options;
 

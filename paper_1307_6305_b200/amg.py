@@ -29,7 +29,7 @@ class amg_options(ctypes.Structure):
                 ("max_iter", ctypes.c_int32), ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
                 ("use_graphs", ctypes.c_int32), ("compress", ctypes.c_int32), ("tail_nnz", ctypes.c_int64),
                 ("gather_rows", ctypes.c_int64), ("tail_smem", ctypes.c_int32), ("cycle", ctypes.c_int32),
-                ("amli_kappa", ctypes.c_double), ("lanczos_steps", ctypes.c_int32), ("reserved32", ctypes.c_int32),
+                ("amli_kappa", ctypes.c_double), ("lanczos_steps", ctypes.c_int32), ("mis_k", ctypes.c_int32),
                 ("reserved", ctypes.c_int64 * 1)]
 
 

@@ -124,6 +124,9 @@ void free_graph(PassGraph& g, cudaStream_t s);
 // one aggregation pass: handshake matching + attach + leader numbering.  agg_t[v] in [0, *nc).
 // id_off = global id of local vertex 0 (hash keys use global ids, docs/keys.md); 0 on one GPU.
 int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, int* nc, int* rounds, cudaStream_t s);
+// reading A25 (opt-in mis_k > 0): MIS of the graph of A^k + layered growth, one aggregation per level
+int mis_aggregate(const PassGraph& G, int k, uint64_t seed, int level, int* agg, int* nc, int* rounds, cudaStream_t s);
+uint64_t host_sm64(uint64_t z);
 // G_{t+1} = quotient of G_t under agg_t (multiplicities summed, self-loops dropped)
 PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStream_t s);
 // agg[i] = agg_t[agg[i]]

@@ -246,7 +246,12 @@ void amg::build_levels(amg_hierarchy* h, int l0) {
         pt.mark("pass graph 0", l);
         int* agg = nullptr;
         int nc = Lv.A.n;
-        for (int t = 0; t < p; ++t) {
+        if (h->opt.mis_k > 0) {  // reading A25: one MIS-k aggregation replaces the p matching passes
+            agg = dalloc<int>((size_t)G.n + 8, s);
+            mis_aggregate(G, h->opt.mis_k, h->opt.seed, l, agg, &nc, &Lv.rounds[0], s);
+            pt.mark("MIS-k aggregation", l);
+        }
+        for (int t = 0; t < (h->opt.mis_k > 0 ? 0 : p); ++t) {
             const uint64_t salt = host_sm64(h->opt.seed ^ (((uint64_t)l << 8) ^ (uint64_t)t));
             int* agg_t = dalloc<int>((size_t)G.n + 8, s);
             int nct = 0;
@@ -1023,6 +1028,8 @@ static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t 
     if (comm && !comm->c) return fail(AMG_E_ARG, "amg_setup_dist: invalid communicator");
     if (o.lanczos_steps < 0 || o.lanczos_steps > 64 || (comm && o.lanczos_steps > 0))
         return fail(AMG_E_ARG, "amg_setup: lanczos_steps must be in [0, 64] (single GPU only)");
+    if (o.mis_k < 0 || o.mis_k > 8 || (comm && o.mis_k > 0))
+        return fail(AMG_E_ARG, "amg_setup: mis_k must be in [0, 8] (single GPU only)");
     if (o.kappa != 0.0 && !(o.kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: kappa must be 0 or > 1");
     if (o.kappa > 1.0 && !(Em_of(poly_degree, o.kappa) < 1.0))
         return fail(AMG_E_ARG, "amg_setup: E_m(kappa) >= 1: the smoother would not converge (reading A9)");

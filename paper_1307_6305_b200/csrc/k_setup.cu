@@ -549,6 +549,166 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, in
     return 0;
 }
 
+// ------------------------------------------------------------------ MIS-k aggregation (reading A25)
+// The paper's own partitioner, opt-in (mis_k > 0).
+// (A) S = the greedy MIS of the graph of A^k in decreasing key order, key(v) = (hi32(splitmix64(v ^
+// misalt)) << 32) | v.  Computed by rounds with fixed priorities: an undecided vertex joins S iff its
+// key is the largest among the undecided vertices within distance k (k max-propagation sweeps);
+// then every undecided vertex within distance k of S is excluded (k OR sweeps).  A vertex joins only
+// once every larger-key vertex of its k-ball is decided, and it is decided out only by an S member
+// within distance k, so the rounds reproduce the sequential greedy set exactly.
+// (B) layered growth: in layer d = 1..k every unassigned vertex takes, among its neighbours assigned
+// in layers < d, the root of largest key.  Aggregate id = rank of the root in vertex order.
+__device__ __forceinline__ uint64_t mis_key(int v, uint64_t misalt) {
+    return ((sm64((uint64_t)v ^ misalt) >> 32) << 32) | (uint64_t)(uint32_t)v;
+}
+
+// state: 0 undecided, 1 in S, 2 excluded
+__global__ void k_mis_seed(int n, const uint8_t* __restrict__ state, uint64_t misalt, uint64_t* __restrict__ M) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        M[v] = state[v] == 0 ? mis_key(v, misalt) : 0ull;
+}
+
+__global__ void k_mis_max(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                          const uint64_t* __restrict__ Min, uint64_t* __restrict__ Mout) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint64_t m = Min[v];
+        for (int p = rp[v]; p < rp[v + 1]; ++p) m = max(m, Min[ci[p]]);
+        Mout[v] = m;
+    }
+}
+
+__global__ void k_mis_join(int n, uint8_t* __restrict__ state, const uint64_t* __restrict__ M, uint64_t misalt,
+                           uint8_t* __restrict__ E) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint8_t st = state[v];
+        if (st == 0 && M[v] == mis_key(v, misalt)) {
+            st = 1;
+            state[v] = 1;
+        }
+        E[v] = st == 1;
+    }
+}
+
+__global__ void k_mis_or(int n, const int* __restrict__ rp, const int* __restrict__ ci, const uint8_t* __restrict__ Ein,
+                         uint8_t* __restrict__ Eout) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint8_t e = Ein[v];
+        for (int p = rp[v]; p < rp[v + 1] && !e; ++p) e = Ein[ci[p]];
+        Eout[v] = e;
+    }
+}
+
+__global__ void k_mis_exclude(int n, uint8_t* __restrict__ state, const uint8_t* __restrict__ E, int* any) {
+    bool und = false;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        if (state[v] == 0) {
+            if (E[v]) state[v] = 2;
+            else und = true;
+        }
+    }
+    if (__any_sync(0xffffffffu, und) && (threadIdx.x & 31) == 0) *any = 1;
+}
+
+__global__ void k_mis_root0(int n, const uint8_t* __restrict__ state, int* __restrict__ root, int* __restrict__ isl) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        root[v] = state[v] == 1 ? v : -1;
+        isl[v] = state[v] == 1;
+    }
+}
+
+__global__ void k_mis_grow(int n, const int* __restrict__ rp, const int* __restrict__ ci, const int* __restrict__ rin,
+                           int* __restrict__ rout, uint64_t misalt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        int r = rin[v];
+        if (r < 0) {
+            uint64_t bk = 0;
+            for (int p = rp[v]; p < rp[v + 1]; ++p) {
+                const int c = rin[ci[p]];
+                if (c >= 0) {
+                    const uint64_t k = mis_key(c, misalt);
+                    if (r < 0 || k > bk) { r = c; bk = k; }
+                }
+            }
+        }
+        rout[v] = r;
+    }
+}
+
+__global__ void k_mis_assign(int n, const int* __restrict__ root, const int* __restrict__ id, int* __restrict__ agg,
+                             int* bad) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int r = root[v];
+        if (r < 0) { *bad = 1; agg[v] = -1; }
+        else agg[v] = id[r];
+    }
+}
+
+int mis_aggregate(const PassGraph& G, int k, uint64_t seed, int level, int* agg, int* nc, int* rounds, cudaStream_t s) {
+    const int n = G.n;
+    const uint64_t misalt = host_sm64(seed ^ 0x4D49530000000000ULL ^ (uint64_t)level);
+    uint8_t* state = dalloc<uint8_t>((size_t)n + 16, s);
+    uint8_t* E0 = dalloc<uint8_t>((size_t)n + 16, s);
+    uint8_t* E1 = dalloc<uint8_t>((size_t)n + 16, s);
+    uint64_t* M0 = dalloc<uint64_t>((size_t)n + 1, s);
+    uint64_t* M1 = dalloc<uint64_t>((size_t)n + 1, s);
+    int* flag = dalloc<int>(2, s);
+    int* hflag = static_cast<int*>(pinned_scratch()) + 48;
+    CK(cudaMemsetAsync(state, 0, (size_t)n, s));
+    const int g = grid_for(n);
+    int r = 0;
+    for (;;) {
+        ++r;
+        if (r > 100000) throw Error(-7, "MIS did not terminate");
+        k_mis_seed<<<g, kBlock, 0, s>>>(n, state, misalt, M0);
+        for (int d = 0; d < k; ++d) {
+            k_mis_max<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, M0, M1);
+            std::swap(M0, M1);
+        }
+        k_mis_join<<<g, kBlock, 0, s>>>(n, state, M0, misalt, E0);
+        for (int d = 0; d < k; ++d) {
+            k_mis_or<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, E0, E1);
+            std::swap(E0, E1);
+        }
+        CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+        k_mis_exclude<<<grid_red(n), kBlock, 0, s>>>(n, state, E0, flag);
+        g_launches += 2 * k + 3;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (!*hflag) break;
+    }
+    dfree(M0, s);
+    dfree(M1, s);
+    dfree(E0, s);
+    dfree(E1, s);
+    int* root = dalloc<int>((size_t)n + 1, s);
+    int* root2 = dalloc<int>((size_t)n + 1, s);
+    int* isl = dalloc<int>((size_t)n + 1, s);
+    int* id = dalloc<int>((size_t)n + 1, s);
+    CK(cudaMemsetAsync(isl + n, 0, sizeof(int), s));
+    k_mis_root0<<<g, kBlock, 0, s>>>(n, state, root, isl);
+    for (int d = 1; d <= k; ++d) {
+        k_mis_grow<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, root, root2, misalt);
+        std::swap(root, root2);
+    }
+    *nc = (int)exclusive_scan_total(isl, id, n, s);
+    CK(cudaMemsetAsync(flag + 1, 0, sizeof(int), s));
+    k_mis_assign<<<g, kBlock, 0, s>>>(n, root, id, agg, flag + 1);
+    g_launches += k + 2;
+    CK(cudaGetLastError());
+    const int bad = read_scalar(flag + 1, s);
+    dfree(root, s);
+    dfree(root2, s);
+    dfree(isl, s);
+    dfree(id, s);
+    dfree(state, s);
+    dfree(flag, s);
+    *rounds = r;
+    if (bad) throw Error(-7, "MIS-k growth left a vertex unassigned");
+    return 0;
+}
+
 // ------------------------------------------------------------------ segmented reductions
 // keys for every stored entry of a CSR: (agg(i) << b) | agg(j); `drop` => self entries get the
 // sentinel (all ones in the low 2b bits) which sorts last.
@@ -967,20 +1127,22 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* _
     }
 }
 
-// Sort-free warp merge for E <= kRM: chunks of 32 entries in k order; __match_any_sync groups a
-// chunk's equal J; the group's first lane finds J in a per-warp shared-memory hash table (open
-// addressing, 2 kRM slots) and adds the group's values to J's accumulator one at a time in lane
-// order, so every accumulator sees its entries in increasing k (the first initialises it, so -0.0
-// survives).  The U distinct J are then ranked by counting (sorted output) and written.
+// Sort-free warp merge for E <= kRM, in two sweeps.  (1) The row's entries are staged in shared
+// memory in k order while the distinct J are collected: __match_any_sync groups a 32-entry chunk's
+// equal J and the group's first lane inserts J into a per-warp hash set (open addressing, 2 kRM
+// slots), appending it to the distinct list when new.  (2) The U distinct J are ranked by counting
+// (sorted output); lane u then owns the u-th one and walks all E staged entries in k order, adding
+// those equal to it -- every sum in the sequential order (the first entry initialises it, so -0.0
+// survives), and the walk is warp-uniform: no per-group serial loops.
 constexpr int kRHWarps = 8;
 constexpr int kRHSlots = 2 * kRM;
 template <class VAL>
 struct RhWarp {
     unsigned hk[kRHSlots];
-    VAL hv[kRHSlots];
-    VAL sv[32];
+    unsigned sJ[kRM];
+    VAL sv[kRM];
     unsigned lj[kRM];
-    int list[kRM];
+    short ls[kRM];
     int cnt;
 };
 
@@ -1003,52 +1165,49 @@ __global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __
         for (int c = 0; c < E; c += 32) {
             const int k = c + lane;
             unsigned J = NONE;
-            VAL v = VAL(0);
             if (k < E) {
                 const unsigned j = stJ[e0 + k];
-                v = stv[e0 + k];
                 J = (drop && j == (unsigned)I) ? NONE : j;
+                W.sJ[k] = J;
+                W.sv[k] = stv[e0 + k];
             }
-            W.sv[lane] = v;
             const unsigned grp = __match_any_sync(0xffffffffu, J);
-            __syncwarp();
             if (J != NONE && __ffs(grp) - 1 == lane) {
                 unsigned h = (J * 2654435761u) >> (32 - 9);
-                bool fresh;
                 for (;;) {
                     const unsigned old = atomicCAS(&W.hk[h], NONE, J);
-                    if (old == NONE) { fresh = true; break; }
-                    if (old == J) { fresh = false; break; }
+                    if (old == NONE) {
+                        const int u = atomicAdd(&W.cnt, 1);
+                        W.lj[u] = J;
+                        W.ls[u] = (short)h;
+                        break;
+                    }
+                    if (old == J) break;
                     h = (h + 1) & (kRHSlots - 1);
                 }
-                unsigned bits = grp;
-                VAL a;
-                if (fresh) {
-                    a = W.sv[lane];
-                    bits &= bits - 1;
-                    W.list[atomicAdd(&W.cnt, 1)] = (int)h;
-                } else {
-                    a = W.hv[h];
-                }
-                while (bits) {
-                    a += W.sv[__ffs(bits) - 1];
-                    bits &= bits - 1;
-                }
-                W.hv[h] = a;
             }
-            __syncwarp();
         }
-        const int U = W.cnt;
-        for (int u = lane; u < U; u += 32) W.lj[u] = W.hk[W.list[u]];
         __syncwarp();
-        for (int u = lane; u < U; u += 32) {
-            const unsigned J = W.lj[u];
+        const int U = W.cnt;
+        for (int ub = 0; ub < U; ub += 32) {
+            const int u = ub + lane;
+            const unsigned Ju = u < U ? W.lj[u] : NONE;
             int rank = 0;
-            for (int q = 0; q < U; ++q) rank += W.lj[q] < J;
-            const int h = W.list[u];
-            stJ[e0 + rank] = J;
-            stv[e0 + rank] = W.hv[h];
-            W.hk[h] = NONE;
+            for (int q = 0; q < U; ++q) rank += W.lj[q] < Ju;
+            VAL acc = VAL(0);
+            bool have = false;
+            for (int k = 0; k < E; ++k) {
+                if (W.sJ[k] == Ju) {
+                    const VAL v = W.sv[k];
+                    acc = have ? acc + v : v;
+                    have = true;
+                }
+            }
+            if (u < U) {
+                stJ[e0 + rank] = Ju;
+                stv[e0 + rank] = acc;
+                W.hk[W.ls[u]] = NONE;
+            }
         }
         if (lane == 0) {
             ucount[I] = U;

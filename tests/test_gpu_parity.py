@@ -467,3 +467,74 @@ def test_structural_zeros_fe_pattern(amg, oracle_mod):
         assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
     finally:
         amg.amg_free(h)
+
+
+def _fe_pattern(N):
+    """The P1-FE right-triangle pattern of test_structural_zeros_fe_pattern (5-point values, the two
+    hypotenuse couplings stored as structural zeros), Dirichlet-like d on the x = 0 column."""
+    n = N * N
+    rows = []
+    for y in range(N):
+        for x in range(N):
+            i = y * N + x
+            nb = [(i - 1, -1.0)] * (x > 0) + [(i + 1, -1.0)] * (x < N - 1) + [(i - N, -1.0)] * (y > 0) + \
+                [(i + N, -1.0)] * (y < N - 1) + [(i - N - 1, 0.0)] * (x > 0 and y > 0) + \
+                [(i + N + 1, 0.0)] * (x < N - 1 and y < N - 1)
+            rows.append(sorted(nb + [(i, -sum(v for _, v in nb))]))
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.array([c for r in rows for c, _ in r], np.int32)
+    v = np.array([w for r in rows for _, w in r])
+    d = np.zeros(n)
+    d[::N] = 1.0
+    return rp, ci, v, d
+
+
+@pytest.mark.parametrize("case", ["C1", "fe96", "rgg"])
+@pytest.mark.parametrize("k", [2, 4])
+def test_mis_k_parity(amg, gen_mod, oracle_mod, case, k):
+    """Reading A25 (opt-in mis_k): the GPU's MIS-k aggregates are bit-exact with the
+    oracle's sequential greedy MIS on every level, coarse operators bit-exact (integer-valued inputs),
+    B_0(r) <= 1e-10 and iteration counts +-1."""
+    if case == "C1":
+        p = gen_mod.problem("C1")
+        rp, ci, v, d = p.rp, p.ci, p.val, p.d
+        m, cs = p.params["degree"], p.params["coarsest_size"]
+    elif case == "fe96":
+        rp, ci, v, d = _fe_pattern(96)
+        m, cs = 4, 100
+    else:
+        p = gen_mod.rgg(20000, seed=7)
+        rp, ci, v, d = p.rp, p.ci, p.val, p.d
+        m, cs = 4, 100
+    n = len(rp) - 1
+    hier = oracle_mod.Hierarchy(rp, ci, v, d, 1, m, coarsest_size=cs, mis_k=k)
+    h = amg.amg_setup(rp, ci, v, d, 1, m, amg.amg_options_default(coarsest_size=cs, mis_k=k))
+    try:
+        compare_hierarchy(amg, h, hier, m, exact_values=True)
+        r = np.random.default_rng(3).uniform(-1, 1, n)
+        if d is None or not np.any(d):
+            r -= r.mean()
+        z = np.empty(n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        ref = hier.precond(r, nu=2, level=0)
+        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        b = gen_mod.rhs(n, 0)
+        if d is None or not np.any(d):
+            b = b - b.mean()
+        x = np.zeros(n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        oref = hier.solve(b, tol=1e-8, nu=2)
+        assert st == 0 and abs(it - oref["iters"]) <= 1, (it, oref["iters"])
+    finally:
+        amg.amg_free(h)
+
+
+def test_mis_k_args(amg):
+    """mis_k outside [0, 8] is AMG_E_ARG."""
+    p_rp = np.array([0, 2, 4], np.int64)
+    ci = np.array([0, 1, 0, 1], np.int32)
+    v = np.array([1.0, -1.0, -1.0, 1.0])
+    with pytest.raises(amg.AmgError) as e:
+        amg.amg_setup(p_rp, ci, v, np.ones(2), 1, 2, amg.amg_options_default(mis_k=9))
+    assert e.value.code == amg.AMG_E_ARG

@@ -17,6 +17,7 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--no-graphs", action="store_true")
 ap.add_argument("--size", type=int, default=None)
 ap.add_argument("--user-stream", action="store_true")
+ap.add_argument("--mis-k", type=int, default=0)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -30,6 +31,7 @@ arrs = [torch.from_numpy(x).to(dev) if x is not None else None for x in (p.rp, p
 b = torch.from_numpy(gen.rhs(p.n, prm["seed"])).to(dev)
 x = torch.zeros(p.n, dtype=torch.float64, device=dev)
 o = amg.amg_options_default(coarsest_size=prm["coarsest_size"], max_iter=a.max_iter, use_graphs=0 if a.no_graphs else 1)
+o.mis_k = a.mis_k
 if os.environ.get("AMG_COMPRESS"):
     o.compress = int(os.environ["AMG_COMPRESS"])
 if os.environ.get("AMG_TAIL_NNZ"):
