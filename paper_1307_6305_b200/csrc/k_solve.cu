@@ -557,6 +557,13 @@ __global__ void __launch_bounds__(kBlock) k_sell_pipe(Sell S, const double* __re
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// the same address held in an ordinary register: opaque to the compiler, so it is not
+// rematerialised from the CTA id before every shared load of an unrolled body (4 uniform ops each)
+__device__ __forceinline__ uint32_t smem_reg(const void* p) {
+    uint32_t r;
+    asm("mov.b32 %0, %1;" : "=r"(r) : "r"(smem_u32(p)));
+    return r;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -685,7 +692,7 @@ __device__ __forceinline__ void tma_slice(const Epi& epi, uint32_t sb, int q, ui
         int cr;
         if constexpr (CM == 3) {
             craw[u] = lds_u16(A + u * 64);
-            cr = craw[u] >> 8;
+            cr = (int)__byte_perm((uint32_t)craw[u], 0u, 0x4441u);  // byte 1 (PRMT + LEA address)
         } else {
             if constexpr (VM == 1) craw[u] = lds_u8(A + u * 32);
             if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
@@ -708,7 +715,7 @@ __device__ __forceinline__ void tma_slice(const Epi& epi, uint32_t sb, int q, ui
     for (int u = 0; u < K; ++u) {
         double v;
         if constexpr (VM == 0) v = lds_f64(A + u * 256);
-        else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[u] & 0xff) : craw[u]));
+        else v = lds_f64(sv_a + 8 * (CM == 3 ? (int)__byte_perm((uint32_t)craw[u], 0u, 0x4440u) : craw[u]));
         sum = fma(v, x[u], sum);
     }
     (void)HDR;
@@ -818,7 +825,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
         }
     } else {
         // consumers: shared-window addresses are formed once (32-bit ld.shared below)
-        const uint32_t tsm_a = smem_u32(tsm), sv_a = smem_u32(sv), sc_a = smem_u32(sc);
+        const uint32_t tsm_a = smem_reg(tsm), sv_a = smem_reg(sv), sc_a = smem_reg(sc);
         const double* __restrict__ xgr = xg;
         for (int k = 0; k < K; ++k) {
             const int st = k % NS, j = k / NS;
@@ -854,7 +861,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
                     int cr;
                     if constexpr (CM == 3) {
                         craw[h][u] = lds_u16(A + u * 64);
-                        cr = craw[h][u] >> 8;
+                        cr = (int)__byte_perm((uint32_t)craw[h][u], 0u, 0x4441u);
                     } else {
                         if constexpr (VM == 1) craw[h][u] = lds_u8(A + u * 32);
                         if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
@@ -896,14 +903,19 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_sell_tma(Sell S, const
                 const int q = warp + h * kTmaWarps;
                 const uint32_t A = sb + Lay::HDR + aoff[h] * 32 * St::ESA + lane * St::ESA;
                 double sum = 0.0;
+                auto term = [&](int u) {
+                    double v;
+                    if constexpr (VM == 0) v = lds_f64(A + u * 256);
+                    else v = lds_f64(sv_a + 8 * (CM == 3 ? (int)__byte_perm((uint32_t)craw[h][u], 0u, 0x4440u) : craw[h][u]));
+                    sum = fma(v, x[h][u], sum);
+                };
+                if (w[h] == W) {
 #pragma unroll
-                for (int u = 0; u < W; ++u) {
-                    if (u < w[h]) {
-                        double v;
-                        if constexpr (VM == 0) v = lds_f64(A + u * 256);
-                        else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[h][u] & 0xff) : craw[h][u]));
-                        sum = fma(v, x[h][u], sum);
-                    }
+                    for (int u = 0; u < W; ++u) term(u);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < W; ++u)
+                        if (u < w[h]) term(u);
                 }
                 const int i = S.srow0 + (c * CS + q) * 32 + lane;
                 const uint32_t r8 = 8 * (q * 32 + lane);
@@ -1177,7 +1189,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth2_tma(Sell S, Sm
             __syncwarp();
         }
     } else {
-        const uint32_t tsm_a = smem_u32(tsm), sv_a = smem_u32(sv), sc_a = smem_u32(sc);
+        const uint32_t tsm_a = smem_reg(tsm), sv_a = smem_reg(sv), sc_a = smem_reg(sc);
         for (int t = 0; t < T; ++t) {
             int stage, c;
             task(t, stage, c);
@@ -1206,7 +1218,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth2_tma(Sell S, Sm
                         int cr;
                         if constexpr (CM == 3) {
                             craw[hh][u] = lds_u16(A + u * 64);
-                            cr = craw[hh][u] >> 8;
+                            cr = (int)__byte_perm((uint32_t)craw[hh][u], 0u, 0x4441u);
                         } else {
                             if constexpr (VM == 1) craw[hh][u] = lds_u8(A + u * 32);
                             if constexpr (CM == 0) cr = lds_s32(Bc + u * 128);
@@ -1247,7 +1259,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth2_tma(Sell S, Sm
                     if (u < w[hh]) {
                         double v;
                         if constexpr (VM == 0) v = lds_f64(Aoff[hh] + u * 256);
-                        else v = lds_f64(sv_a + 8 * (CM == 3 ? (craw[hh][u] & 0xff) : craw[hh][u]));
+                        else v = lds_f64(sv_a + 8 * (CM == 3 ? (int)__byte_perm((uint32_t)craw[hh][u], 0u, 0x4440u) : craw[hh][u]));
                         sum = fma(v, x[hh][u], sum);
                     }
                 }
