@@ -1295,6 +1295,10 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1)) k_smooth2_tma(Sell S, Sm
     }
 }
 
+// formats that get W = 32 instances (variable-width levels wider than 16, e.g. the RGG's level 0:
+// 1-byte value codes + int16 column offsets); the others stop at 16 to bound compile time
+__host__ __device__ constexpr bool tma_wide_fmt(int vm, int cm) { return (vm == 1 && cm == 2) || (vm == 0 && cm == 2); }
+
 template <class Epi, bool DOTS, int VM, int CM, int W, int SPW, int NS>
 static void launch_tma_w(const SpOp& op, const double* xg, const Epi& e, double* part, unsigned* tk, DotOut dot_out,
                          cudaStream_t s) {
@@ -1348,7 +1352,8 @@ static void launch_tma_fmt(const SpOp& op, const double* xg, const Epi& e, doubl
         case 8: launch_tma_v<Epi, DOTS, VM, CM, 8>(op, xg, e, part, tk, d, s); break;
         default:
             if (op.S.wmax <= 12) launch_tma_w<Epi, DOTS, VM, CM, 12, 1, 3>(op, xg, e, part, tk, d, s);
-            else launch_tma_w<Epi, DOTS, VM, CM, 16, 1, 3>(op, xg, e, part, tk, d, s);
+            else if (op.S.wmax <= 16) launch_tma_w<Epi, DOTS, VM, CM, 16, 1, 3>(op, xg, e, part, tk, d, s);
+            else if constexpr (tma_wide_fmt(VM, CM)) launch_tma_w<Epi, DOTS, VM, CM, 32, 1, 3>(op, xg, e, part, tk, d, s);
     }
 }
 
@@ -1362,8 +1367,9 @@ static bool launch_tma(const SpOp& op, const double* xg, const Epi& e, const dou
     static int min_slices = -1;  // AMG_TMA_MIN_SLICES (experiments)
     if (min_slices < 0) min_slices = getenv("AMG_TMA_MIN_SLICES") ? atoi(getenv("AMG_TMA_MIN_SLICES")) : 8 * 148 * kTmaWarps;
     static int max_w = -1;  // AMG_TMA_MAX_W (experiments)
-    if (max_w < 0) max_w = getenv("AMG_TMA_MAX_W") ? atoi(getenv("AMG_TMA_MAX_W")) : 16;
-    if (!(tma_enabled() && op.sell && op.S.wmax <= max_w && op.S.nslices >= min_slices && aligned16(xg) &&
+    if (max_w < 0) max_w = getenv("AMG_TMA_MAX_W") ? atoi(getenv("AMG_TMA_MAX_W")) : 32;
+    const int wcap = tma_wide_fmt(op.S.vmode, op.S.cmode) ? 32 : 16;  // W = 32 instances: wide formats only
+    if (!(tma_enabled() && op.sell && op.S.wmax <= std::min(max_w, wcap) && op.S.nslices >= min_slices && aligned16(xg) &&
           (!v0 || aligned16(v0)) && (!v1 || aligned16(v1))))
         return false;
     double* part = ds ? ds->partials : nullptr;

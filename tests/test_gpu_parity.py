@@ -538,3 +538,32 @@ def test_mis_k_args(amg):
     with pytest.raises(amg.AmgError) as e:
         amg.amg_setup(p_rp, ci, v, np.ones(2), 1, 2, amg.amg_options_default(mis_k=9))
     assert e.value.code == amg.AMG_E_ARG
+
+
+def test_smoother_tma_wide_slices_parity(amg, gen_mod, oracle_mod):
+    """An RGG level 0 with slices wider than 16 (up to ~27 entries; 1-byte value codes + int16 column
+    offsets) and > 9472 slices runs the W = 32 TMA instance: one smoother application, one residual-class
+    B_0(r) and the solve's iteration count against the oracle."""
+    p = gen_mod.rgg(400000, seed=3)
+    rl = np.diff(p.rp)
+    assert rl.max() > 16
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 4, 4, coarsest_size=100)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 4, 4, amg.amg_options_default(coarsest_size=100))
+    try:
+        assert amg.amg_get_info(h)["level0_format"] == 2
+        rng = np.random.default_rng(4)
+        n = len(p.rp) - 1
+        f = rng.uniform(-1, 1, n)
+        x0 = rng.uniform(-1, 1, n)
+        x = np.empty(n)
+        amg.amg_level_smooth(h, 0, f, x0, x)
+        ref = hier.smooth(0, f, x0)
+        assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+        r = rng.uniform(-1, 1, n)
+        r -= r.mean()
+        z = np.empty(n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        zr = hier.precond(r, nu=2, level=0)
+        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+    finally:
+        amg.amg_free(h)
