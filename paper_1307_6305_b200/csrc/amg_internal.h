@@ -98,6 +98,7 @@ void dfree(void* p, cudaStream_t s);
 
 // validation of the user CSR (reading A17).  Returns bit flags (0 = valid).
 // Columns must lie in [cmin, cmax) ([0, n) on one GPU; [-nlo, n+nhi) relative on a row-partitioned level).
+int pattern_rp32(int n, const int64_t* rp, const int32_t* ci, int* rp32, cudaStream_t s);
 int validate_input(int n, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v, const double* d,
                    cudaStream_t s);
 // A_0 = L + diag(d) with inserted missing diagonals; returns a fresh Csr.

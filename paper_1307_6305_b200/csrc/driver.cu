@@ -197,23 +197,81 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         void* r = nullptr;
         if (cudaMallocAsync(&r, want, s) == cudaSuccess) dfree(r, s); else cudaGetLastError();
     }
-    void *t_ci, *t_v, *t_d;
+    void *t_ci, *t_v = nullptr, *t_d = nullptr;
     const int32_t* ci = stage_in(ci_in, (size_t)nnz_in, s, &t_ci);
-    const double* v = stage_in(v_in, (size_t)nnz_in, s, &t_v);
-    const double* d = stage_in(d_in, (size_t)n, s, &t_d);
+    // Host inputs: the values (and d) are copied on a side stream while level 0's value-free
+    // matching passes run on the pattern (row_ptr, col), which is checked first (ranges, order).
+    const bool host_vals = (v_in && !is_device_ptr(v_in)) || (d_in && !is_device_ptr(d_in));
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev_vals = nullptr;
+    const double *v, *d;
+    if (host_vals) {
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_vals, cudaEventDisableTiming));
+        cudaEvent_t ev0;  // cs allocates from the pool after the row_ptr/col staging on s
+        CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev0, s));
+        CK(cudaStreamWaitEvent(cs, ev0, 0));
+        CK(cudaEventDestroy(ev0));
+        v = stage_in(v_in, (size_t)nnz_in, cs, &t_v);
+        d = stage_in(d_in, (size_t)n, cs, &t_d);
+        CK(cudaEventRecord(ev_vals, cs));
+    } else {
+        v = stage_in(v_in, (size_t)nnz_in, s, &t_v);
+        d = stage_in(d_in, (size_t)n, s, &t_d);
+    }
+    auto join_vals = [&]() {
+        if (!cs) return;
+        CK(cudaStreamWaitEvent(s, ev_vals, 0));
+        CK(cudaStreamSynchronize(cs));
+        CK(cudaEventDestroy(ev_vals));
+        CK(cudaStreamDestroy(cs));
+        cs = nullptr;
+    };
+    auto free_inputs = [&]() { dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s); };
     pt.mark("stage inputs");
+    int* agg0 = nullptr;
+    int nc0 = 0;
+    if (host_vals && n > h->opt.coarsest_size) {
+        int* rp32 = dalloc<int>((size_t)n + 8, s);
+        const int pf = pattern_rp32(n, rp, ci, rp32, s);
+        if (pf) {
+            dfree(rp32, s);
+            join_vals();
+            free_inputs();
+            throw Error(AMG_E_INPUT, validation_message(pf));
+        }
+        try {
+            Csr P;  // the input pattern: G_0's off-diagonal entries are the same as A_0's
+            P.n = n;
+            P.nnz = nnz_in;
+            P.rp = rp32;
+            P.ci = const_cast<int*>(ci);
+            PassGraph G = pass_graph0(P, s);
+            pt.mark("pass graph 0 (overlapped)", 0);
+            agg0 = aggregate_level(h, 0, G, &nc0);
+        } catch (...) {
+            dfree(rp32, s);
+            join_vals();
+            free_inputs();
+            throw;
+        }
+        dfree(rp32, s);
+    }
+    join_vals();
     int vf = validate_input(n, 0, n, rp, ci, v, d, s);
     pt.mark("validate");
     if (vf) {
-        dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
+        dfree(agg0, s);
+        free_inputs();
         throw Error(AMG_E_INPUT, validation_message(vf));
     }
     h->singular = !(d && any_nonzero(n, d, s));
     h->lev[0].A = form_A0(n, rp, ci, v, d, s);
-    dfree(t_rp, s); dfree(t_ci, s); dfree(t_v, s); dfree(t_d, s);
+    free_inputs();
     h->L = 1;
     pt.mark("form A0");
-    build_levels(h, 0);
+    build_levels(h, 0, agg0, nc0);
     finish_build(h);
 }
 
@@ -227,10 +285,49 @@ std::string amg::validation_message(int vf) {
 // Level loop from level l0, whose operator every rank holds whole: lambda_1,
 // kappa and coefficients, p matching passes composed into agg_l, the aggregate order and the
 // Galerkin product, until n_l <= coarsest_size.
-void amg::build_levels(amg_hierarchy* h, int l0) {
+// p matching passes (or one MIS-k aggregation, reading A25) on level l's pass graph G (consumed);
+// returns agg_l (device, caller-owned) and n_{l+1}
+int* amg::aggregate_level(amg_hierarchy* h, int l, PassGraph& G, int* nc_out) {
     cudaStream_t s = h->s;
     PhaseTimer pt(s);
-    const int m = h->m, p = h->p;
+    Level& Lv = h->lev[l];
+    const int n = G.n, p = h->p;
+    int* agg = nullptr;
+    int nc = n;
+    if (h->opt.mis_k > 0) {
+        agg = dalloc<int>((size_t)G.n + 8, s);
+        mis_aggregate(G, h->opt.mis_k, h->opt.seed, l, agg, &nc, &Lv.rounds[0], s);
+        pt.mark("MIS-k aggregation", l);
+    }
+    for (int t = 0; t < (h->opt.mis_k > 0 ? 0 : p); ++t) {
+        const uint64_t salt = host_sm64(h->opt.seed ^ (((uint64_t)l << 8) ^ (uint64_t)t));
+        int* agg_t = dalloc<int>((size_t)G.n + 8, s);
+        int nct = 0;
+        aggregate_pass(G, salt, 0, agg_t, &nct, &Lv.rounds[t], s);
+        pt.mark("matching pass", l);
+        if (t + 1 < p) {
+            PassGraph G2 = quotient_graph(G, agg_t, nct, s);
+            free_graph(G, s);
+            G = G2;
+            pt.mark("quotient graph", l);
+        }
+        if (t == 0) {
+            agg = agg_t;
+        } else {
+            compose(n, agg, agg_t, s);
+            dfree(agg_t, s);
+        }
+        nc = nct;
+    }
+    free_graph(G, s);
+    *nc_out = nc;
+    return agg;
+}
+
+void amg::build_levels(amg_hierarchy* h, int l0, int* agg0, int nc0) {
+    cudaStream_t s = h->s;
+    PhaseTimer pt(s);
+    const int m = h->m;
     int l = l0;
     for (;;) {
         Level& Lv = h->lev[l];
@@ -242,36 +339,17 @@ void amg::build_levels(amg_hierarchy* h, int l0) {
         pt.mark("lambda1", l);
         if (Lv.A.n <= h->opt.coarsest_size) break;
         if (l + 1 >= kMaxLevels) throw Error(AMG_E_SETUP, "too many levels");
-        PassGraph G = pass_graph0(Lv.A, s);
-        pt.mark("pass graph 0", l);
         int* agg = nullptr;
         int nc = Lv.A.n;
-        if (h->opt.mis_k > 0) {  // reading A25: one MIS-k aggregation replaces the p matching passes
-            agg = dalloc<int>((size_t)G.n + 8, s);
-            mis_aggregate(G, h->opt.mis_k, h->opt.seed, l, agg, &nc, &Lv.rounds[0], s);
-            pt.mark("MIS-k aggregation", l);
+        if (l == l0 && agg0) {  // level 0's aggregation already ran (overlapped with the value copies)
+            agg = agg0;
+            nc = nc0;
+            agg0 = nullptr;
+        } else {
+            PassGraph G = pass_graph0(Lv.A, s);
+            pt.mark("pass graph 0", l);
+            agg = aggregate_level(h, l, G, &nc);
         }
-        for (int t = 0; t < (h->opt.mis_k > 0 ? 0 : p); ++t) {
-            const uint64_t salt = host_sm64(h->opt.seed ^ (((uint64_t)l << 8) ^ (uint64_t)t));
-            int* agg_t = dalloc<int>((size_t)G.n + 8, s);
-            int nct = 0;
-            aggregate_pass(G, salt, 0, agg_t, &nct, &Lv.rounds[t], s);
-            pt.mark("matching pass", l);
-            if (t + 1 < p) {
-                PassGraph G2 = quotient_graph(G, agg_t, nct, s);
-                free_graph(G, s);
-                G = G2;
-                pt.mark("quotient graph", l);
-            }
-            if (t == 0) {
-                agg = agg_t;
-            } else {
-                compose(Lv.A.n, agg, agg_t, s);
-                dfree(agg_t, s);
-            }
-            nc = nct;
-        }
-        free_graph(G, s);
         if (nc >= Lv.A.n) {
             dfree(agg, s);
             throw Error(AMG_E_SETUP, "coarsening stagnated (n_{l+1} = n_l)");

@@ -128,7 +128,8 @@ uint64_t host_sm64(uint64_t z);
 double kappa_rule(int m);
 void poly_coeffs(double l1, double kappa, int m, double* a, double* b);
 // level loop (a1-a6) from h->lev[l0].A, which every rank holds whole (replicated); sets h->L
-void build_levels(amg_hierarchy* h, int l0);
+void build_levels(amg_hierarchy* h, int l0, int* agg0 = nullptr, int nc0 = 0);
+int* aggregate_level(amg_hierarchy* h, int l, PassGraph& G, int* nc);
 // coarsest inverse, SpMV formats, workspaces, tail (after all levels exist)
 void finish_build(amg_hierarchy* h);
 // vector of level l laid out for halo exchange: returns the pointer to its first own element

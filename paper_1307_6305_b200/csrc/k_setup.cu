@@ -137,6 +137,44 @@ __global__ void k_validate(int n, int cmin, int cmax, const int64_t* __restrict_
     }
 }
 
+// The pattern part of the checks (row_ptr monotone, columns in [0, n) and strictly increasing,
+// pattern symmetry) and the int32 row pointers of the pattern: enough to run the value-free matching passes of level 0
+// safely while the values are still being copied in (e2e path).
+__global__ void k_pattern_rp32(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               int* __restrict__ rp32, int* flags) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+        rp32[i] = (int)rp[i];
+        if (i == n) continue;
+        const int64_t p0 = rp[i], p1 = rp[i + 1];
+        if (p1 < p0 || (i == 0 && p0 != 0)) { atomicOr(flags, VF_RP); continue; }
+        int f = 0;
+        for (int64_t p = p0; p < p1; ++p) {
+            const int c = ci[p];
+            if (c < 0 || c >= n) { f |= VF_RANGE; continue; }
+            if (p > p0 && c <= ci[p - 1]) f |= VF_UNSORTED;
+            if (c == i) continue;
+            int64_t lo = rp[c], hi = rp[c + 1];  // the pattern must be symmetric (the matching relies on it)
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (ci[mid] < i) lo = mid + 1; else hi = mid;
+            }
+            if (!(lo < rp[c + 1] && ci[lo] == i)) f |= VF_ASYM;
+        }
+        if (f) atomicOr(flags, f);
+    }
+}
+
+int pattern_rp32(int n, const int64_t* rp, const int32_t* ci, int* rp32, cudaStream_t s) {
+    int* fl = dalloc<int>(1, s);
+    CK(cudaMemsetAsync(fl, 0, sizeof(int), s));
+    k_pattern_rp32<<<grid_for((int64_t)n + 1), kBlock, 0, s>>>(n, rp, ci, rp32, fl);
+    ++g_launches;
+    CK(cudaGetLastError());
+    int f = read_scalar(fl, s);
+    dfree(fl, s);
+    return f;
+}
+
 int validate_input(int n, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v, const double* d,
                    cudaStream_t s) {
     int* fl = dalloc<int>(1, s);
