@@ -883,6 +883,7 @@ static void quotient_impl(int n, int64_t nnz, const int* rp, const int* ci, cons
 
 // ------------------------------------------------------------------ row-merge quotient / Galerkin
 void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s);
+void aggregate_order_counting(int n, const int* agg, int nc, int* perm, int* aptr, bool sorted, cudaStream_t s);
 // Coarse row I is the merge of its members' rows (members = perm[aptr[I] .. aptr[I+1]), increasing
 // vertex order).  Two steps:
 //  1. staging: every fine row's entries, mapped (J = agg(col), value), are copied in perm order into
@@ -1493,7 +1494,7 @@ PassGraph quotient_graph(const PassGraph& G, const int* agg_t, int nc, cudaStrea
     if (!getenv("AMG_RADIX_QUOTIENT")) {
         int* perm = dalloc<int>((size_t)G.n + 8, s);
         int* aptr = dalloc<int>((size_t)nc + 8, s);
-        aggregate_order(G.n, agg_t, nc, perm, aptr, s);
+        aggregate_order_counting(G.n, agg_t, nc, perm, aptr, false, s);  // pass graphs: any member order
         const bool ok = quotient_rowmerge<uint32_t>(G.n, G.nnz, G.rp, G.ci, G.w, agg_t, nc, true, perm, aptr, &H.rp,
                                                     &H.ci, &H.w, &H.nnz, s);
         dfree(perm, s);
@@ -1542,7 +1543,79 @@ __global__ void k_aptr(int nc, int n, const int* __restrict__ sorted_agg, int* _
     }
 }
 
+// Counting-sort aggregate order: members counted per aggregate (atomics), aptr by a scan, members
+// placed by atomic cursors, then (sorted) each aggregate's members sorted in increasing vertex order
+// by one thread (insertion sort; heap sort for the rare aggregates of > 32 members).  sorted == false
+// (the pass graphs, whose merges are order free) skips the last step.
+__global__ void k_agg_count(int n, const int* __restrict__ agg, int* __restrict__ cnt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) atomicAdd(cnt + agg[v], 1);
+}
+
+__global__ void k_agg_place(int n, const int* __restrict__ agg, const int* __restrict__ aptr, int* __restrict__ cur,
+                            int* __restrict__ perm) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int I = agg[v];
+        perm[aptr[I] + atomicAdd(cur + I, 1)] = v;
+    }
+}
+
+__device__ void heap_sift(int* a, int i, int m) {
+    for (;;) {
+        int c = 2 * i + 1;
+        if (c >= m) return;
+        if (c + 1 < m && a[c + 1] > a[c]) ++c;
+        if (a[i] >= a[c]) return;
+        const int t = a[i]; a[i] = a[c]; a[c] = t;
+        i = c;
+    }
+}
+
+__global__ void k_agg_sortseg(int nc, const int* __restrict__ aptr, int* __restrict__ perm) {
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+        int* a = perm + aptr[I];
+        const int m = aptr[I + 1] - aptr[I];
+        if (m <= 32) {
+            for (int k = 1; k < m; ++k) {
+                const int x = a[k];
+                int j = k - 1;
+                while (j >= 0 && a[j] > x) { a[j + 1] = a[j]; --j; }
+                a[j + 1] = x;
+            }
+        } else {
+            for (int k = m / 2 - 1; k >= 0; --k) heap_sift(a, k, m);
+            for (int e = m - 1; e > 0; --e) {
+                const int t = a[0]; a[0] = a[e]; a[e] = t;
+                heap_sift(a, 0, e);
+            }
+        }
+    }
+}
+
+void aggregate_order_counting(int n, const int* agg, int nc, int* perm, int* aptr, bool sorted, cudaStream_t s) {
+    int* cnt = dalloc<int>((size_t)nc + 1, s);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)nc + 1), s));
+    k_agg_count<<<grid_for(n), kBlock, 0, s>>>(n, agg, cnt);
+    exclusive_scan_total(cnt, aptr, nc, s);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)nc, s));
+    k_agg_place<<<grid_for(n), kBlock, 0, s>>>(n, agg, aptr, cnt, perm);
+    g_launches += 2;
+    if (sorted) {
+        k_agg_sortseg<<<grid_for(nc), kBlock, 0, s>>>(nc, aptr, perm);
+        ++g_launches;
+    }
+    CK(cudaGetLastError());
+    dfree(cnt, s);
+}
+
 void aggregate_order(int n, const int* agg, int nc, int* perm, int* aptr, cudaStream_t s) {
+    // the level order (members sorted) stays on the radix sort: the counting version's per-aggregate
+    // sort measured slower there (C3 setup 19.2 vs 20.0 ms); AMG_AGG_COUNTING=1 selects it
+    static int radix = -1;
+    if (radix < 0) radix = getenv("AMG_AGG_COUNTING") ? 0 : 1;
+    if (!radix) {
+        aggregate_order_counting(n, agg, nc, perm, aptr, true, s);
+        return;
+    }
     int* iota = dalloc<int>(n, s);
     int* sk = dalloc<int>(n, s);
     k_iota<<<grid_for(n), kBlock, 0, s>>>(n, iota);
