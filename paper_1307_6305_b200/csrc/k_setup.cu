@@ -524,10 +524,13 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, in
     int nv = n;
     void* tmp = nullptr;
     size_t tb = 0;
+    static int first = -1;  // rounds before the first free-list compaction (AMG_MATCH_FIRST; 2 measured best)
+    if (first < 0) first = getenv("AMG_MATCH_FIRST") ? std::max(1, atoi(getenv("AMG_MATCH_FIRST"))) : 2;
     for (;;) {
         const int gp = std::max(1, std::min((int)(((int64_t)nv * Gl + kBlock - 1) / kBlock), 148 * 8));
         const int ga = std::max(1, std::min(grid_for(nv), 148 * 8));
-        for (int k = 0; k < kBatch; ++k) {
+        const int nb = list ? kBatch : first;
+        for (int k = 0; k < nb; ++k) {
             CK(cudaMemsetAsync(any, 0, sizeof(int), s));
             switch (Gl) {
                 case 1: k_propose<1><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
@@ -558,7 +561,7 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, in
         CK(cudaMemcpyAsync(nsel + 1, any, sizeof(int), cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(hsel, nsel, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        r += kBatch;
+        r += nb;
         if (!hsel[1] || hsel[0] == 0) break;
         nv = hsel[0];
         if (r > 30000) throw Error(-7, "matching did not terminate");
@@ -1176,10 +1179,14 @@ __global__ void __launch_bounds__(32 * kRMWarps) k_rm_merge(int nl, const int* _
 constexpr int kRHWarps = 8;
 constexpr int kRHSlots = 2 * kRM;
 template <class VAL>
+struct alignas(16) RhEnt {  // one staged entry: a single 16-byte (8-byte for uint32) shared load
+    VAL v;
+    unsigned J;
+};
+template <class VAL>
 struct RhWarp {
+    RhEnt<VAL> se[kRM];
     unsigned hk[kRHSlots];
-    unsigned sJ[kRM];
-    VAL sv[kRM];
     unsigned lj[kRM];
     short ls[kRM];
     int cnt;
@@ -1207,8 +1214,8 @@ __global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __
             if (k < E) {
                 const unsigned j = stJ[e0 + k];
                 J = (drop && j == (unsigned)I) ? NONE : j;
-                W.sJ[k] = J;
-                W.sv[k] = stv[e0 + k];
+                W.se[k].J = J;
+                W.se[k].v = stv[e0 + k];
             }
             const unsigned grp = __match_any_sync(0xffffffffu, J);
             if (J != NONE && __ffs(grp) - 1 == lane) {
@@ -1233,14 +1240,13 @@ __global__ void __launch_bounds__(32 * kRHWarps) k_rm_hash(int nl, const int* __
             const unsigned Ju = u < U ? W.lj[u] : NONE;
             int rank = 0;
             for (int q = 0; q < U; ++q) rank += W.lj[q] < Ju;
-            VAL acc = VAL(0);
-            bool have = false;
+            // -0.0 + v == v exactly for every v, so starting from -0.0 the first term initialises the
+            // sum and the additions are those of the sequential definition
+            VAL acc = std::is_same<VAL, double>::value ? VAL(-0.0) : VAL(0);
+#pragma unroll 4
             for (int k = 0; k < E; ++k) {
-                if (W.sJ[k] == Ju) {
-                    const VAL v = W.sv[k];
-                    acc = have ? acc + v : v;
-                    have = true;
-                }
+                const RhEnt<VAL> e = W.se[k];
+                if (e.J == Ju) acc += e.v;
             }
             if (u < U) {
                 stJ[e0 + rank] = Ju;
