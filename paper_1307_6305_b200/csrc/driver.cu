@@ -16,6 +16,7 @@
 #include <ctime>
 #include <cstdlib>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/amg.h"
@@ -127,9 +128,40 @@ static void destroy_graphs(amg_hierarchy* h) {
     h->graph_nu = 0;
 }
 
+static double now_ms() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+
+// Pinned 64-byte host mirrors of the handles' scalars, recycled through a process-wide free list:
+// cudaMallocHost / cudaFreeHost cost ~0.5 ms each, once per amg_setup / amg_free otherwise.
+static std::mutex g_pin_mu;
+static std::vector<double*> g_pin_free;
+static double* pinned_take() {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        if (!g_pin_free.empty()) {
+            double* p = g_pin_free.back();
+            g_pin_free.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    CK(cudaMallocHost(&p, 8 * sizeof(double)));
+    return static_cast<double*>(p);
+}
+static void pinned_give(double* p) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(p);
+}
+
 static void release(amg_hierarchy* h) {
     if (!h) return;
+    static const bool trace = getenv("AMG_FREE_TRACE") != nullptr;
+    const double t0 = trace ? now_ms() : 0.0;
     destroy_graphs(h);
+    const double t1 = trace ? now_ms() : 0.0;
     if (h->s) {
         for (int l = 0; l < h->L; ++l) {
             dfree(h->lev[l].A.rp, h->s);
@@ -140,9 +172,12 @@ static void release(amg_hierarchy* h) {
         }
         for (void* p : h->allocs) dfree(p, h->s);
         for (void* p : h->ws_allocs) dfree(p, h->s);
-        cudaStreamSynchronize(h->s);  // the stream itself is the thread's persistent library stream
     }
-    if (h->hsc) cudaFreeHost(h->hsc);
+    const double t2 = trace ? now_ms() : 0.0;
+    if (h->s) cudaStreamSynchronize(h->s);  // the stream itself is the thread's persistent library stream
+    const double t3 = trace ? now_ms() : 0.0;
+    if (trace) fprintf(stderr, "[amg free] graphs %.3f ms, frees %.3f ms, sync %.3f ms\n", t1 - t0, t2 - t1, t3 - t2);
+    if (h->hsc) pinned_give(h->hsc);
     if (h->e0) cudaEventDestroy(h->e0);
     if (h->e1) cudaEventDestroy(h->e1);
     if (h->pe0) cudaEventDestroy(h->pe0);
@@ -510,7 +545,7 @@ void amg::finish_build(amg_hierarchy* h) {
     h->ds.partials = halloc<double>(h, (size_t)(kMaxWin + 2) * 4096);
     h->ds.ticket = halloc<unsigned>(h, 4);
     CK(cudaMemsetAsync(h->ds.ticket, 0, 4 * sizeof(unsigned), s));
-    CK(cudaMallocHost(&h->hsc, 8 * sizeof(double)));
+    h->hsc = pinned_take();
     if (h->comm) {
         h->ar_send = halloc<double>(h, kArMax);
         h->ar_recv = halloc<double>(h, (size_t)kArMax * h->comm->size);
@@ -932,26 +967,30 @@ static void outer_iteration(amg_hierarchy* h, int pos, int nu) {
     if (dist) dot_allreduce(h, {rr});
 }
 
-static void capture_graphs(amg_hierarchy* h, int nu) {
-    destroy_graphs(h);
-    h->graphs.resize(h->W, nullptr);
-    for (int pos = 0; pos < h->W; ++pos) {
-        cudaGraph_t g;
-        long long before = g_launches;
-        CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
-        try {
-            outer_iteration(h, pos, nu);
-        } catch (...) {
-            cudaStreamEndCapture(h->s, &g);
-            throw;
-        }
-        CK(cudaStreamEndCapture(h->s, &g));
-        h->graph_launches = g_launches - before;
-        g_launches = before;
-        CK(cudaGraphInstantiate(&h->graphs[pos], g, 0));
-        CK(cudaGraphDestroy(g));
+// One graph per restart-window position, captured lazily: position p+1's graph is captured on the
+// host while position p's graph runs on the device (capture only records; the stream's pending work
+// keeps executing), so the ~0.5 ms per capture + instantiation hides behind the solve.
+static void capture_graph(amg_hierarchy* h, int pos, int nu) {
+    if (h->graph_nu != nu) {
+        destroy_graphs(h);
+        h->graphs.assign(h->W, nullptr);
+        h->graph_nu = nu;
     }
-    h->graph_nu = nu;
+    if (h->graphs[pos]) return;
+    cudaGraph_t g;
+    long long before = g_launches;
+    CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+    try {
+        outer_iteration(h, pos, nu);
+    } catch (...) {
+        cudaStreamEndCapture(h->s, &g);
+        throw;
+    }
+    CK(cudaStreamEndCapture(h->s, &g));
+    h->graph_launches = g_launches - before;
+    g_launches = before;
+    CK(cudaGraphInstantiate(&h->graphs[pos], g, 0));
+    CK(cudaGraphDestroy(g));
 }
 
 static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol, int nu, int* iters_out,
@@ -971,7 +1010,6 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     // distributed handle whose whole hierarchy is replicated (g = 0): gather the caller's blocks
     const bool gather_in = h->comm && !dist;
     ensure_inner_ws(h, nu);
-    if (graphs && h->graph_nu != nu) capture_graphs(h, nu);
     long long launches0 = g_launches;
     CK(cudaEventRecord(h->e0, s));
     // inputs
@@ -994,6 +1032,11 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     if (dist) dot_allreduce(h, {rr, bb});
     CK(cudaMemsetAsync(h->flag, 0, sizeof(int), s));
     CK(cudaMemcpyAsync(h->hsc, rr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (graphs) {  // while the inputs copy and the first residual runs
+        const long long l0 = g_launches;
+        capture_graph(h, 0, nu);
+        launches0 += g_launches - l0;
+    }
     CK(cudaStreamSynchronize(s));
     const double bnorm = std::sqrt(h->hsc[1]);
     double rnorm = std::sqrt(h->hsc[0]);
@@ -1013,6 +1056,8 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
             if (graphs) {
                 CK(cudaGraphLaunch(h->graphs[pos], s));
                 ++graph_runs;
+                const int nxt = (pos + 1) % h->W;
+                if (!h->graphs[nxt]) capture_graph(h, nxt, nu);  // overlaps this iteration
             } else {
                 outer_iteration(h, pos, nu);
             }
