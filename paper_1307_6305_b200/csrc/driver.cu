@@ -16,7 +16,9 @@
 #include <ctime>
 #include <cstdlib>
 #include <string>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/amg.h"
@@ -121,9 +123,68 @@ static void record_event(cudaEvent_t e, cudaStream_t s) {
         CK(cudaEventRecord(e, s));
 }
 
-static void destroy_graphs(amg_hierarchy* h) {
+// cudaGraphExecDestroy of a handle's 5 graphs costs ~1.2 ms of host time; amg_free hands them to a
+// process-wide worker thread instead (joined, and the rest destroyed, at exit).
+namespace {
+struct GraphReaper {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<std::pair<int, cudaGraphExec_t>> q;
+    bool stop = false;
+    std::thread th;
+    GraphReaper() : th([this] { run(); }) {}
+    void run() {
+        std::unique_lock<std::mutex> lk(mu);
+        for (;;) {
+            cv.wait(lk, [this] { return stop || !q.empty(); });
+            auto items = std::move(q);
+            q.clear();
+            const bool last = stop;
+            lk.unlock();
+            for (auto& it : items) {
+                cudaSetDevice(it.first);
+                cudaGraphExecDestroy(it.second);
+            }
+            lk.lock();
+            if (last && q.empty()) return;
+        }
+    }
+    void push(int dev, cudaGraphExec_t g) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            q.emplace_back(dev, g);
+        }
+        cv.notify_one();
+    }
+    void shutdown() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_one();
+        if (th.joinable()) th.join();
+    }
+};
+GraphReaper* g_reaper = nullptr;
+std::mutex g_reaper_mu;
+GraphReaper* reaper() {
+    std::lock_guard<std::mutex> lk(g_reaper_mu);
+    if (!g_reaper) {
+        g_reaper = new GraphReaper();
+        std::atexit([] { if (g_reaper) g_reaper->shutdown(); });
+    }
+    return g_reaper;
+}
+}  // namespace
+
+static void destroy_graphs(amg_hierarchy* h, bool deferred = false) {
+    int dev = 0;
+    if (deferred) cudaGetDevice(&dev);
     for (auto g : h->graphs)
-        if (g) cudaGraphExecDestroy(g);
+        if (g) {
+            if (deferred) reaper()->push(dev, g);
+            else cudaGraphExecDestroy(g);
+        }
     h->graphs.clear();
     h->graph_nu = 0;
 }
@@ -160,7 +221,7 @@ static void release(amg_hierarchy* h) {
     if (!h) return;
     static const bool trace = getenv("AMG_FREE_TRACE") != nullptr;
     const double t0 = trace ? now_ms() : 0.0;
-    destroy_graphs(h);
+    destroy_graphs(h, true);
     const double t1 = trace ? now_ms() : 0.0;
     if (h->s) {
         for (int l = 0; l < h->L; ++l) {
