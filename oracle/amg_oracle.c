@@ -17,9 +17,10 @@
  * Pins: every function here is pinned by a -m "not gpu" test in tests/ against
  * something other than itself (closed forms, dense linear algebra, brute force,
  * the paper's golden example); see DESIGN.md "Oracle pins".  The multilevel
- * nonlinear k-cycle (ocycle with cycle=0 below ml levels > 2) is "parity
- * unpinned" beyond its partial pins (two-level equality, homogeneity, the linear
- * V-cycle symmetry probe), SURVEY 8(c) pins table.
+ * nonlinear k-cycle (ocycle with cycle=0 at > 2 levels) is pinned in its two
+ * closed-form regimes (nu large: the P:136 two-level formula with the exact
+ * A_1^{-1}, L = 3 and 4; nu = 1: one optimal inner step along B_1 rho) and by
+ * homogeneity; for nu = 2 at L >= 3 only those general pins apply.
  */
 #include <math.h>
 #include <stdint.h>

@@ -734,3 +734,47 @@ def test_mis_hierarchy_paper_protocol(oracle_mod):
         hc = oracle_mod.Hierarchy(rp, ci, v, None, 1, 4, coarsest_size=99, mis_k=4, cycle=cyc)
         r = hc.solve(b, tol=1e-8, nu=2, xstar=xs)
         assert r["status"] == 0 and r["iters"] <= 40
+
+
+def test_kcycle_three_and_four_levels_pinned(oracle_mod, gen_mod):
+    """The nonlinear k-cycle at L > 2 against mathematics:
+    (1) with nu large the inner FCG on level 1 is preconditioned by a linear SPD B_1, so it is PCG and
+        solves A_1 e = rho exactly (Krylov termination): B_0 equals the two-level formula of P:136
+        with the exact A_1^{-1} (L = 3 and L = 4);
+    (2) with nu = 1 the inner FCG takes one step from e = 0 along d = B_1 rho with the optimal
+        (A_1-norm minimising) step d.rho / d.A_1 d: B_0(r) is the smoothed two-level cycle with that
+        coarse correction, B_1 itself the exact two-level operator of level 1 (L = 3)."""
+    p = gen_mod.grid2d(18)
+    rng = np.random.default_rng(2)
+    r = rng.standard_normal(p.n)
+    for cs, L in [(30, 3), (10, 4)]:
+        hk = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=cs)
+        assert hk.nlev == L
+        mats = []
+        for l in range(hk.nlev):
+            rp, ci, v = hk.level_csr(l)
+            mats.append(H.dense(rp, ci, v))
+
+        def smoother_R(l):
+            l1 = hk.level_info(l)["lambda1"]
+            kap = hk.level_info(l)["kappa"]
+            return H.matfun_sym(mats[l], H.q_closed_form(l1 / kap, l1, 3))
+
+        A, A1 = mats[0], mats[1]
+        R = smoother_R(0)
+        P = H.P_dense(hk.level_agg(0), hk.level_info(0)["nc"])
+        B = H.two_level_B(A, P, R, np.linalg.inv(A1))
+        z = hk.precond(r, nu=2 * A1.shape[0])
+        assert np.linalg.norm(z - B @ r) <= 1e-12 * np.linalg.norm(B @ r), L
+        if L == 3:
+            R1 = smoother_R(1)
+            P1 = H.P_dense(hk.level_agg(1), hk.level_info(1)["nc"])
+            B1 = H.two_level_B(A1, P1, R1, np.linalg.inv(mats[2]))
+            x0 = R @ r
+            rho = P.T @ (r - A @ x0)
+            d = B1 @ rho
+            e = (d @ rho) / (d @ (A1 @ d)) * d
+            x1 = x0 + P @ e
+            x2 = x1 + R @ (r - A @ x1)
+            z1 = hk.precond(r, nu=1)
+            assert np.linalg.norm(z1 - x2) <= 1e-12 * np.linalg.norm(x2)
