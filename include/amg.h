@@ -155,7 +155,8 @@ int amg_setup(amg_handle* out, int64_t n, const int64_t* row_ptr, const int32_t*
  *   b        fp64[n] right-hand side (host or device)
  *   x        fp64[n] in: initial guess x_0; out: solution (host or device; overwritten)
  *   tol      stop when ||r_k||_2 <= tol ||b||_2 on the recursive residual (reading A14)
- *   k_inner  nu >= 1 inner FCG iterations per coarse-level visit (k-cycle, l.321; BASELINE uses 2)
+ *   k_inner  1 <= nu <= 16 inner FCG iterations per coarse-level visit (k-cycle, l.321; BASELINE uses 2;
+ *            16 = the inner direction window)
  *   iters    out (nullable): outer iterations performed
  *   relres   out (nullable): ||r||/||b|| at exit
  * Returns AMG_OK, AMG_NOT_CONVERGED, AMG_E_BREAKDOWN or an error.

@@ -567,3 +567,21 @@ def test_smoother_tma_wide_slices_parity(amg, gen_mod, oracle_mod):
         assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("nu", [1, 3, 16])
+def test_kcycle_nu_regimes_parity(amg, gen_mod, oracle_mod, nu):
+    """B_0(r) on a 3-level hierarchy for nu = 1 and nu = 16 (the two pinned closed-form regimes of the
+    k-cycle, tests/test_oracle_pins.py) and nu = 3, against the oracle to 1e-10."""
+    p = gen_mod.grid2d(18)
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=30)
+    assert hier.nlev == 3
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 2, 3, amg.amg_options_default(coarsest_size=30))
+    try:
+        r = np.random.default_rng(2).standard_normal(p.n)
+        z = np.empty(p.n)
+        amg.amg_level_precond(h, 0, nu, r, z)
+        ref = hier.precond(r, nu=nu, level=0)
+        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+    finally:
+        amg.amg_free(h)
