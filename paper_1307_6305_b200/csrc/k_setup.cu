@@ -67,12 +67,17 @@ static int bits_for(int64_t x) {  // smallest b >= 1 with 2^b >= x
 }
 
 // exclusive scan of int32 flags/counts into out (n+1 entries: out[n] = total); returns total
-static int64_t exclusive_scan_total(const int* in, int* out, int n, cudaStream_t s) {
+// the same without reading the total back (callers that know it: no host synchronisation)
+static void exclusive_scan(const int* in, int* out, int n, cudaStream_t s) {
     size_t tb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n + 1, s));
     void* tmp = dalloc<char>(tb, s);
     CK(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, n + 1, s));
     dfree(tmp, s);
+}
+
+static int64_t exclusive_scan_total(const int* in, int* out, int n, cudaStream_t s) {
+    exclusive_scan(in, out, n, s);
     int total = read_scalar(out + n, s);
     return total;
 }
@@ -1350,7 +1355,6 @@ template <class VAL>
 static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, const VAL* src, const int* agg, int nc,
                               bool drop, const int* perm, const int* aptr, int** orp, int** oci, VAL** oval,
                               int64_t* onnz, cudaStream_t s) {
-    (void)nnz;
     // 1. staging offsets S (perm order) and the staged entries
     int* S = dalloc<int>((size_t)n + 1, s);
     {
@@ -1358,7 +1362,7 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
         CK(cudaMemsetAsync(lenp + n, 0, sizeof(int), s));
         k_stage_len<<<grid_for(n), kBlock, 0, s>>>(n, rp, perm, lenp);
         ++g_launches;
-        exclusive_scan_total(lenp, S, n, s);
+        exclusive_scan(lenp, S, n, s);  // S[n] = nnz: no read back
         dfree(lenp, s);
     }
     int* cnt = dalloc<int>(8, s);  // emax, counts[5]
@@ -1381,9 +1385,7 @@ static bool quotient_rowmerge(int n, int64_t nnz, const int* rp, const int* ci, 
         dfree(eoff, s);
         return false;
     }
-    int tot = 0;
-    CK(cudaMemcpyAsync(&tot, eoff + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    const int64_t tot = nnz;  // = S[n] = eoff[nc]: every stored entry is staged once
     unsigned* stJ = dalloc<unsigned>((size_t)tot + 8, s);
     VAL* stv = dalloc<VAL>((size_t)tot + 8, s);
     {
@@ -1601,7 +1603,7 @@ void aggregate_order_counting(int n, const int* agg, int nc, int* perm, int* apt
     int* cnt = dalloc<int>((size_t)nc + 1, s);
     CK(cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)nc + 1), s));
     k_agg_count<<<grid_for(n), kBlock, 0, s>>>(n, agg, cnt);
-    exclusive_scan_total(cnt, aptr, nc, s);
+    exclusive_scan(cnt, aptr, nc, s);  // aptr[nc] = n
     CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)nc, s));
     k_agg_place<<<grid_for(n), kBlock, 0, s>>>(n, agg, aptr, cnt, perm);
     g_launches += 2;
