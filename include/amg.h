@@ -75,8 +75,10 @@ typedef struct {
     int64_t  gather_rows;   /* amg_setup_dist only: the first level with fewer than gather_rows rows
                                (and always the coarsest) is gathered onto every rank, which runs the
                                rest of the hierarchy redundantly; default 50000 */
-    int32_t  tail_smem;     /* 1 = the coarse-tail kernel keeps every vector of its levels in shared
-                               memory when they fit (200 KB); default 0 (measured no gain) */
+    int32_t  tail_smem;     /* coarse-tail kernel's shared memory (200 KB): 0 = none; 1 = every vector of its
+                               levels when they all fit; 2 = greedy by access frequency -- each level's
+                               matrix (copied in per call), the smoother / transfer vectors, the aggregate
+                               maps, then the inner-FCG vectors, the rest global; default 2 */
     int32_t  cycle;         /* coarse-level correction: 0 = N-AMLI / k-cycle, nu inner
                                FCG iterations (the paper's NPCG column; default); 2 = stationary AMLI:
                                e = q(B A) B rho with q the degree-(nu-1) best uniform approximation to

@@ -220,6 +220,9 @@ struct TLevel {
     // shared-memory mode: offsets (in doubles) of X, XA, RES, RHO, E, Z, D, Q inside the kernel's
     // dynamic shared memory; -1 = the global vector above
     int off[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+    // tail_smem = 2: the same for the read-only level data rp, ci, v, agg, perm, aptr (copied into
+    // shared memory at kernel start); -1 = global
+    int moff[6] = {-1, -1, -1, -1, -1, -1};
 };
 struct TailArgs {
     int l0 = 0;       // level the call starts at

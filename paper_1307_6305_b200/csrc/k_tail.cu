@@ -94,12 +94,16 @@ __device__ void t_step(const TLevel& L, const double* xg, double cgs, const doub
     csync<CL>();
 }
 
+// dense coarsest apply, one warp per row (lanes stride the columns, a fixed-order warp sum): a
+// thread per row left 32x fewer loads in flight on the coarsest levels' few rows
 template <bool CL>
 __device__ void t_gemv(int n, const double* M, const double* r, double* e, TCtx c) {
-    for (int i = c.t; i < n; i += c.T) {
+    const int lane = c.t & 31, w = c.t >> 5, nw = c.T >> 5;
+    for (int i = w; i < n; i += nw) {
         double s = 0.0;
-        for (int j = 0; j < n; ++j) s = fma(M[(size_t)i * n + j], r[j], s);
-        e[i] = s;
+        for (int j = lane; j < n; j += 32) s = fma(M[(size_t)i * n + j], r[j], s);
+        s = t_warp_sum(s);
+        if (lane == 0) e[i] = s;
     }
     csync<CL>();
 }
@@ -235,11 +239,40 @@ __global__ void __launch_bounds__(kTailBlock, 1) k_tail(TailArgs a) {
                 double** ptr[8] = {&t.X, &t.XA, &t.RES, &t.RHO, &t.E, &t.Z, &t.D, &t.Q};
                 for (int j = 0; j < 8; ++j)
                     if (t.off[j] >= 0) *ptr[j] = tsv + t.off[j];
+                // tail_smem = 2: read-only level data placed in shared memory too (copied below)
+                const int** iptr[5] = {&t.rp, &t.ci, &t.agg, &t.perm, &t.aptr};
+                const int imap[5] = {0, 1, 3, 4, 5};
+                for (int j = 0; j < 5; ++j)
+                    if (t.moff[imap[j]] >= 0) *iptr[j] = reinterpret_cast<const int*>(tsv + t.moff[imap[j]]);
+                if (t.moff[2] >= 0) t.v = tsv + t.moff[2];
                 slev[k] = t;
             }
             __syncthreads();
+            for (int k = 0; k < nl; ++k) {
+                const TLevel& g = a.lev[a.l0 - a.lbase + k];
+                const TLevel& sl = slev[k];
+                if (sl.moff[0] >= 0 || sl.moff[1] >= 0 || sl.moff[2] >= 0) {
+                    const int nnz = g.rp[g.n];
+                    auto cp_i = [&](const int* src, const int* dst, int len) {
+                        int* d = const_cast<int*>(dst);
+                        for (int i = threadIdx.x; i < len; i += blockDim.x) d[i] = src[i];
+                    };
+                    if (sl.moff[0] >= 0) cp_i(g.rp, sl.rp, g.n + 1);
+                    if (sl.moff[1] >= 0) cp_i(g.ci, sl.ci, nnz);
+                    if (sl.moff[2] >= 0) {
+                        double* d = const_cast<double*>(sl.v);
+                        for (int i = threadIdx.x; i < nnz; i += blockDim.x) d[i] = g.v[i];
+                    }
+                }
+                if (sl.moff[3] >= 0)
+                    for (int i = threadIdx.x; i < g.n; i += blockDim.x) const_cast<int*>(sl.agg)[i] = g.agg[i];
+                if (sl.moff[4] >= 0)
+                    for (int i = threadIdx.x; i < g.n; i += blockDim.x) const_cast<int*>(sl.perm)[i] = g.perm[i];
+                if (sl.moff[5] >= 0)
+                    for (int i = threadIdx.x; i <= g.nc; i += blockDim.x) const_cast<int*>(sl.aptr)[i] = g.aptr[i];
+            }
             const TLevel& g0 = a.lev[a.l0 - a.lbase];
-            if (a.mode == 1)
+            if (a.mode == 1 && slev[0].RHO != g0.RHO)
                 for (int i = threadIdx.x; i < g0.n; i += blockDim.x) slev[0].RHO[i] = g0.RHO[i];
             a.lev = slev;
             a.lbase = a.l0;
@@ -248,7 +281,8 @@ __global__ void __launch_bounds__(kTailBlock, 1) k_tail(TailArgs a) {
                 t_B<CL>(a, a.l0, a.rin, a.out, c);
             } else {
                 t_fcg<CL>(a, a.l0, c);
-                for (int i = threadIdx.x; i < g0.n; i += blockDim.x) g0.E[i] = slev[0].E[i];
+                if (slev[0].E != g0.E)
+                    for (int i = threadIdx.x; i < g0.n; i += blockDim.x) g0.E[i] = slev[0].E[i];
             }
             return;
         }

@@ -336,13 +336,14 @@ def test_smoother_tma_path_parity(amg, gen_mod, oracle_mod):
         amg.amg_free(h)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("tail_nnz", [8192, 10 ** 6])
-def test_tail_shared_memory_mode_parity(amg, gen_mod, oracle_mod, tail_nnz):
+def test_tail_shared_memory_mode_parity(amg, gen_mod, oracle_mod, tail_nnz, mode):
     """The coarse-tail kernel with its vectors in shared memory (opt-in tail_smem) gives the same
     B_0(r) as the oracle and the same iterations; tail_nnz 1e6 puts every level >= 1 of C1 in the tail."""
     p = gen_mod.problem("C1")
     hier = oracle_mod.setup_problem(p)
-    o = amg.amg_options_default(coarsest_size=100, tail_nnz=tail_nnz, tail_smem=1)
+    o = amg.amg_options_default(coarsest_size=100, tail_nnz=tail_nnz, tail_smem=mode)
     h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 2, 2, o)
     try:
         r = np.random.default_rng(5).uniform(-1, 1, p.n)

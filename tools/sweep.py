@@ -1,6 +1,6 @@
 """Sweep one amg_options field (or env knob) over values for several configs; prints device solve/setup ms.
 
-    python tools/sweep.py --configs C1,C3 --field tail_nnz --values 0,8192,32768 [--reps 3] [--env AMG_TAIL_CLUSTER=8]
+    python tools/sweep.py --configs C1,C3 --field tail_nnz --values 0,8192,32768 [--reps 3] [--set tail_smem=2]
 """
 import argparse
 import os
@@ -14,6 +14,7 @@ ap.add_argument("--configs", default="C3")
 ap.add_argument("--field", default="tail_nnz")
 ap.add_argument("--values", default="8192")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--set", action="append", default=[], help="extra option key=value (repeatable)")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -29,6 +30,9 @@ for cfg in a.configs.split(","):
     x = torch.zeros(p.n, dtype=torch.float64, device=dev)
     for v in a.values.split(","):
         o = amg.amg_options_default(coarsest_size=prm["coarsest_size"])
+        for kv in a.set:
+            k_, v_ = kv.split("=")
+            setattr(o, k_, type(getattr(o, k_))(float(v_)))
         setattr(o, a.field, type(getattr(o, a.field))(float(v)) if a.field != "kappa" else float(v))
         best = None
         for r in range(a.reps + 1):
