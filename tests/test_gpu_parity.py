@@ -586,3 +586,48 @@ def test_kcycle_nu_regimes_parity(amg, gen_mod, oracle_mod, nu):
         assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_invalid_inputs_above_coarsest(amg, gen_mod, where):
+    """Invalid CSR inputs large enough to be coarsened: with host arrays the pattern is checked
+    before the overlapped level-0 matching (ranges, order, pattern symmetry), the values after the
+    join; every case is AMG_E_INPUT and nothing is left behind (a valid setup follows)."""
+    import torch
+
+    p = gen_mod.grid2d(30)
+    n = p.n
+
+    def run(rp, ci, v, d):
+        if where == "device":
+            dev = torch.device("cuda", 0)
+            rp, ci, v = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (rp, ci, v))
+            d = torch.from_numpy(d).to(dev) if d is not None else None
+        return amg.amg_setup(rp, ci, v, d, 2, 3)
+
+    cases = []
+    ci = p.ci.copy()
+    ci[p.rp[5] + 1] = n + 7  # column out of range
+    cases.append((p.rp, ci, p.val, p.d))
+    ci = p.ci.copy()
+    a0 = p.rp[40]
+    ci[a0], ci[a0 + 1] = ci[a0 + 1], ci[a0]  # unsorted row
+    cases.append((p.rp, ci, p.val, p.d))
+    # asymmetric pattern: drop one off-diagonal entry of row 100 (its transpose stays)
+    r0, r1 = p.rp[100], p.rp[101]
+    k = next(q for q in range(r0, r1) if p.ci[q] != 100)
+    keep = np.ones(len(p.ci), bool)
+    keep[k] = False
+    rp2 = p.rp.copy()
+    rp2[101:] -= 1
+    cases.append((rp2, p.ci[keep], p.val[keep], p.d))
+    bad = p.val.copy()
+    bad[p.rp[7]] = 0.5  # positive off-diagonal (row 7's first entry is off-diagonal)
+    cases.append((p.rp, p.ci, bad, p.d))
+    cases.append((p.rp, p.ci, p.val, -np.abs(p.d) - 1.0))  # d < 0
+    for rp, ci_, v, d in cases:
+        with pytest.raises(amg.AmgError) as e:
+            run(rp, ci_, v, d)
+        assert e.value.code == amg.AMG_E_INPUT
+    h = run(p.rp, p.ci, p.val, p.d)
+    amg.amg_free(h)
