@@ -1303,6 +1303,7 @@ template <class Epi, bool DOTS, int VM, int CM, int W, int SPW, int NS>
 static void launch_tma_w(const SpOp& op, const double* xg, const Epi& e, double* part, unsigned* tk, DotOut dot_out,
                          cudaStream_t s) {
     using Lay = TmaLayout<VM, CM, W, SPW, NS>;
+    static_assert(Lay::BYTES <= 227 * 1024, "TMA stage ring exceeds the 227 KB of shared memory per CTA");
     static int res = 0;  // resident grid per instance
     if (!res) {
         CK(cudaFuncSetAttribute(k_sell_tma<Epi, DOTS, VM, CM, W, SPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1353,7 +1354,8 @@ static void launch_tma_fmt(const SpOp& op, const double* xg, const Epi& e, doubl
         default:
             if (op.S.wmax <= 12) launch_tma_w<Epi, DOTS, VM, CM, 12, 1, 3>(op, xg, e, part, tk, d, s);
             else if (op.S.wmax <= 16) launch_tma_w<Epi, DOTS, VM, CM, 16, 1, 3>(op, xg, e, part, tk, d, s);
-            else if constexpr (tma_wide_fmt(VM, CM)) launch_tma_w<Epi, DOTS, VM, CM, 32, 1, 3>(op, xg, e, part, tk, d, s);
+            else if constexpr (tma_wide_fmt(VM, CM))  // fp64 values: a 2-stage ring fits the 227 KB
+                launch_tma_w<Epi, DOTS, VM, CM, 32, 1, (VM == 0 ? 2 : 3)>(op, xg, e, part, tk, d, s);
     }
 }
 

@@ -631,3 +631,37 @@ def test_invalid_inputs_above_coarsest(amg, gen_mod, where):
         assert e.value.code == amg.AMG_E_INPUT
     h = run(p.rp, p.ci, p.val, p.d)
     amg.amg_free(h)
+
+
+def test_smoother_tma_wide_fp64_values_parity(amg, gen_mod, oracle_mod):
+    """Wide slices (> 16) with > 256 distinct values (fp64 value stream, int16 column offsets) and
+    > 9472 slices: the W = 32 TMA instance with its 2-stage ring.  RGG pattern, random symmetric
+    weights; one smoother application and B_0(r) against the oracle."""
+    p = gen_mod.rgg(400000, seed=5)
+    n = len(p.rp) - 1
+    rows = np.repeat(np.arange(n), np.diff(p.rp))
+    lo, hi = np.minimum(rows, p.ci).astype(np.uint64), np.maximum(rows, p.ci).astype(np.uint64)
+    w = 1.0 + ((lo * np.uint64(2654435761) + hi * np.uint64(40503)) % np.uint64(1000)).astype(np.float64) / 1000.0
+    off = rows != p.ci
+    v = np.where(off, -w, 0.0)
+    diag = np.zeros(n)
+    np.add.at(diag, rows[off], w[off])
+    v[~off] = diag[rows[~off]]
+    d = np.full(n, 0.01)
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, v, d, 4, 4, coarsest_size=100)
+    h = amg.amg_setup(p.rp, p.ci, v, d, 4, 4, amg.amg_options_default(coarsest_size=100))
+    try:
+        rng = np.random.default_rng(6)
+        f = rng.uniform(-1, 1, n)
+        x0 = rng.uniform(-1, 1, n)
+        x = np.empty(n)
+        amg.amg_level_smooth(h, 0, f, x0, x)
+        ref = hier.smooth(0, f, x0)
+        assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+        r = rng.uniform(-1, 1, n)
+        z = np.empty(n)
+        amg.amg_level_precond(h, 0, 2, r, z)
+        zr = hier.precond(r, nu=2, level=0)
+        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+    finally:
+        amg.amg_free(h)
