@@ -665,3 +665,31 @@ def test_smoother_tma_wide_fp64_values_parity(amg, gen_mod, oracle_mod):
         assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+@pytest.mark.parametrize("mis_k", [0, 4])
+def test_full_size_configs_converge(amg, gen_mod, cfg, mis_k):
+    """Every BASELINE config at full size, with the paper's matching (BASELINE) and with MIS-4: all
+    level formats and kernel instances they select run, the solve converges to tol and the true
+    residual agrees.  Pairwise iteration counts are the oracle's where it was run at full size
+    (C3: 33) or the recorded B200 counts (C4 17, C5 78)."""
+    import torch
+
+    p = gen_mod.problem(cfg)
+    prm = p.params
+    dev = torch.device("cuda", 0)
+    arrs = [torch.from_numpy(x).to(dev) if x is not None else None for x in (p.rp, p.ci, p.val, p.d)]
+    b = torch.from_numpy(gen_mod.rhs(p.n, prm["seed"])).to(dev)
+    x = torch.zeros(p.n, dtype=torch.float64, device=dev)
+    o = amg.amg_options_default(coarsest_size=prm["coarsest_size"], mis_k=mis_k)
+    h = amg.amg_setup(*arrs, prm["passes"], prm["degree"], o)
+    try:
+        st, it, rr = amg.amg_solve(h, b, x, prm["tol"], prm["k_inner"])
+        info = amg.amg_get_info(h)
+        assert st == 0 and rr <= prm["tol"]
+        assert info["last_true_relres"] <= 2 * prm["tol"]
+        if mis_k == 0:
+            assert it == {"C3": 33, "C4": 17, "C5": 78}[cfg]
+    finally:
+        amg.amg_free(h)
