@@ -693,3 +693,30 @@ def test_full_size_configs_converge(amg, gen_mod, cfg, mis_k):
             assert it == {"C3": 33, "C4": 17, "C5": 78}[cfg]
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.parametrize("opts", [dict(compress=0), dict(cycle=2), dict(lanczos_steps=10), dict(use_graphs=0),
+                                  dict(tail_smem=0), dict(tail_nnz=0)])
+def test_full_size_c3_option_paths(amg, gen_mod, opts):
+    """C3 at full size through the other option paths (uncompressed SELL streams, the AMLI cycle, the
+    Lanczos lambda_max, eager launches, no tail shared memory, no tail): converges, true residual
+    agrees; the options that do not change the arithmetic keep the 33 iterations."""
+    import torch
+
+    p = gen_mod.problem("C3")
+    prm = p.params
+    dev = torch.device("cuda", 0)
+    arrs = [torch.from_numpy(x).to(dev) if x is not None else None for x in (p.rp, p.ci, p.val, p.d)]
+    b = torch.from_numpy(gen_mod.rhs(p.n, prm["seed"])).to(dev)
+    x = torch.zeros(p.n, dtype=torch.float64, device=dev)
+    o = amg.amg_options_default(coarsest_size=prm["coarsest_size"], **opts)
+    h = amg.amg_setup(*arrs, prm["passes"], prm["degree"], o)
+    try:
+        st, it, rr = amg.amg_solve(h, b, x, prm["tol"], prm["k_inner"])
+        info = amg.amg_get_info(h)
+        assert st == 0 and rr <= prm["tol"]
+        assert info["last_true_relres"] <= 2 * prm["tol"]
+        if not ({"cycle", "lanczos_steps"} & set(opts)):
+            assert it == 33
+    finally:
+        amg.amg_free(h)
