@@ -549,11 +549,13 @@ void amg::finish_build(amg_hierarchy* h) {
     for (int k = 0; k < h->L; ++k) {
         Level& Lv = h->lev[k];
         if (k < h->L - 1 || k == 0) {
-            Lv.T = build_tiles(Lv.A, 0, s);
-            pt.mark("tiles", k);
             if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
             if (Lv.S.sptr) Lv.S.chi = Lv.A.n + Lv.H.nhi - 1;
             pt.mark("sell", k);
+            if (!Lv.S.sptr) {  // CSR row tiles: only the levels too irregular for SELL use them
+                Lv.T = build_tiles(Lv.A, 0, s);
+                pt.mark("tiles", k);
+            }
             if (Lv.S.sptr && h->opt.compress) compress_sell(Lv.S, Lv.A, s);
             pt.mark("compress", k);
         }
