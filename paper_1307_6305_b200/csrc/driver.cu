@@ -300,6 +300,14 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     const bool host_vals = (v_in && !is_device_ptr(v_in)) || (d_in && !is_device_ptr(d_in));
     cudaStream_t cs = nullptr;
     cudaEvent_t ev_vals = nullptr;
+    struct SideStream {  // released on every exit path (an exception while staging included)
+        cudaStream_t& cs;
+        cudaEvent_t& ev;
+        ~SideStream() {
+            if (cs) { cudaStreamSynchronize(cs); cudaStreamDestroy(cs); }
+            if (ev) cudaEventDestroy(ev);
+        }
+    } side_guard{cs, ev_vals};
     const double *v, *d;
     if (host_vals) {
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -321,6 +329,7 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         CK(cudaStreamWaitEvent(s, ev_vals, 0));
         CK(cudaStreamSynchronize(cs));
         CK(cudaEventDestroy(ev_vals));
+        ev_vals = nullptr;
         CK(cudaStreamDestroy(cs));
         cs = nullptr;
     };
