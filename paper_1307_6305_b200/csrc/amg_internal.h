@@ -179,6 +179,8 @@ void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, 
 // prolongation + axpy: x[i] += eH[agg[i]]
 void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s);
 // dense coarse apply e = M r (M row-major n x n)
+void launch_gemv_prolong(int nf, const int* agg, int cb, int nL, const double* M, const double* r, double* x,
+                         cudaStream_t s);
 void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_t s);
 // c[j] = z . Q_j for j < w  (Q_j = Q[j], pointers in a device array)
 void launch_multidot(int n, const double* z, const double* const* Q, int w, double* c, const DotScratch& ds,

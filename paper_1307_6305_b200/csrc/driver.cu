@@ -1010,13 +1010,15 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO + cb, s);
     if (gather) allgatherv_d(h, C.RHO, C.offs);
     // coarse correction (A12: exact solve when the next level is the coarsest)
-    if (l + 1 == h->L - 1)
-        launch_gemv(C.A.n, h->Minv, C.RHO, C.E, s);
-    else if (h->opt.cycle == 2)
-        amli_correction(h, l + 1, nu);
-    else
-        fcg_inner(h, l + 1, nu);
-    launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
+    if (l + 1 == h->L - 1) {  // exact coarsest solve fused with the prolongation
+        launch_gemv_prolong(Lv.A.n, Lv.agg, (int)cb, C.A.n, h->Minv, C.RHO, cur, s);
+    } else {
+        if (h->opt.cycle == 2)
+            amli_correction(h, l + 1, nu);
+        else
+            fcg_inner(h, l + 1, nu);
+        launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
+    }
     // post-smoothing S(r, x): x_{-1} = x_0 = cur
     double* other = (cur == Lv.X) ? Lv.XA : Lv.X;
     std::vector<SmStep> st;

@@ -1541,6 +1541,36 @@ void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_
     ++g_launches;
 }
 
+// Coarsest apply fused with the prolongation into the level above (one launch instead of two on every
+// visit of level L-2): warp w takes fine rows i = w, w + nwarp, ...; it computes e_I, I = agg(i) + cb,
+// exactly as k_gemv does for row I (the same lane split and warp_sum tree: bitwise the same e_I) and
+// adds it to x_i (the same single add as k_prolong).  Each fine row recomputes its aggregate's dot:
+// n_{L-2} * n_L fma, negligible next to the saved launch.
+__global__ void __launch_bounds__(kBlock) k_gemv_prolong(int nf, const int* __restrict__ agg, int cb, int nL,
+                                                         const double* __restrict__ M, const double* __restrict__ r,
+                                                         double* __restrict__ x) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int nwarp = (gridDim.x * blockDim.x) >> 5;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nf; i += nwarp) {
+        const int I = __ldg(agg + i) + cb;
+        double s = 0.0;
+        for (int j = lane; j < nL; j += 32) s = fma(M[(size_t)I * nL + j], __ldg(r + j), s);
+        s = warp_sum(s);
+        if (lane == 0) x[i] += s;
+    }
+}
+
+void launch_gemv_prolong(int nf, const int* agg, int cb, int nL, const double* M, const double* r, double* x,
+                         cudaStream_t s) {
+    int grid = (int)(((int64_t)nf * 32 + kBlock - 1) / kBlock);
+    if (grid > vector_grid()) grid = vector_grid();
+    launch_k(k_gemv_prolong, dim3(grid), dim3(kBlock), 0, s, nf, agg, cb, nL, M, r, x);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
 // ------------------------------------------------------------------ FCG vector kernels
 struct PtrArr {
     const double* p[kMaxWin];
