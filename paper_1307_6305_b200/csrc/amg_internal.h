@@ -15,6 +15,7 @@ namespace amg {
 
 constexpr int kMaxDeg = 16;      // poly_degree m <= kMaxDeg
 constexpr int kMaxLevels = 48;
+constexpr int kFuseRestrictRows = 40000;  // levels below this fuse residual + restriction (k_resid_restrict; C2 -4%)
 constexpr int kMaxWin = 16;      // restart window / inner nu <= kMaxWin
 constexpr int kBlock = 256;      // threads per block of the tile / vector kernels
 
@@ -179,6 +180,8 @@ void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, 
 // prolongation + axpy: x[i] += eH[agg[i]]
 void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s);
 // dense coarse apply e = M r (M row-major n x n)
+void launch_resid_restrict(int nc, const int* aptr, const int* perm, const Csr& A, const double* x, const double* f,
+                           double* rho, cudaStream_t s);
 void launch_gemv_prolong(int nf, const int* agg, int cb, int nL, const double* M, const double* r, double* x,
                          cudaStream_t s);
 void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_t s);

@@ -1001,13 +1001,18 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
         run_steps(h, l, rin, st, false);
     }
     // residual + restriction
-    spmv_pass(h, l, cur, [&](const SpOp& op, int) { launch_resid(op, cur, rin, Lv.RES, nullptr, h->ds, s); });
     Level& C = h->lev[l + 1];
     // the level below the last row-partitioned one is replicated: restrict into this rank's block of
     // it and allgather the blocks (C-gather); prolong from the same block
     const bool gather = Lv.dist && !C.dist;
     const int64_t cb = gather ? C.offs[h->comm->rank] : 0;
-    launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO + cb, s);
+    static const int rr_rows = getenv("AMG_FUSE_RR_ROWS") ? atoi(getenv("AMG_FUSE_RR_ROWS")) : kFuseRestrictRows;
+    if (!Lv.dist && Lv.A.n < rr_rows) {  // small level: one fused launch
+        launch_resid_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.A, cur, rin, C.RHO, s);
+    } else {
+        spmv_pass(h, l, cur, [&](const SpOp& op, int) { launch_resid(op, cur, rin, Lv.RES, nullptr, h->ds, s); });
+        launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO + cb, s);
+    }
     if (gather) allgatherv_d(h, C.RHO, C.offs);
     // coarse correction (A12: exact solve when the next level is the coarsest)
     if (l + 1 == h->L - 1) {  // exact coarsest solve fused with the prolongation

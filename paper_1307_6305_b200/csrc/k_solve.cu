@@ -1541,6 +1541,49 @@ void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_
     ++g_launches;
 }
 
+// Residual fused with the restriction on the small (L2-resident, launch-latency-bound) levels: one
+// warp per aggregate, lane = member (chunks of 32): each lane forms its row's residual f_i - (A x)_i
+// with the fma chain in CSR order (the SELL kernels' order: the same r_i), then every lane sums the
+// chunk's r in member order through shuffles starting from 0.0 (k_restrict's order): bitwise the same
+// rho_I, one launch and the residual vector's round trip less per visit.
+__global__ void __launch_bounds__(kBlock) k_resid_restrict(int nc, const int* __restrict__ aptr,
+                                                           const int* __restrict__ perm, const int* __restrict__ rp,
+                                                           const int* __restrict__ ci, const double* __restrict__ v,
+                                                           const double* __restrict__ x, const double* __restrict__ f,
+                                                           double* __restrict__ rho) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int nwarp = (gridDim.x * blockDim.x) >> 5;
+    for (int I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; I < nc; I += nwarp) {
+        const int t0 = aptr[I], t1 = aptr[I + 1];
+        double s = 0.0;
+        for (int tb = t0; tb < t1; tb += 32) {
+            const int t = tb + lane;
+            double r = 0.0;
+            if (t < t1) {
+                const int i = perm[t];
+                double acc = 0.0;
+                for (int p = rp[i]; p < rp[i + 1]; ++p) acc = fma(v[p], ld_gather(x + ci[p]), acc);
+                r = ld_nc(f + i) - acc;
+            }
+            const int cnt = min(32, t1 - tb);
+            for (int k = 0; k < cnt; ++k) s += __shfl_sync(0xffffffffu, r, k);
+        }
+        if (lane == 0) rho[I] = s;
+    }
+}
+
+void launch_resid_restrict(int nc, const int* aptr, const int* perm, const Csr& A, const double* x, const double* f,
+                           double* rho, cudaStream_t s) {
+    int grid = (int)(((int64_t)nc * 32 + kBlock - 1) / kBlock);
+    if (grid > vector_grid()) grid = vector_grid();
+    launch_k(k_resid_restrict, dim3(grid), dim3(kBlock), 0, s, nc, aptr, perm, (const int*)A.rp, (const int*)A.ci,
+             (const double*)A.v, x, f, rho);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
 // Coarsest apply fused with the prolongation into the level above (one launch instead of two on every
 // visit of level L-2): warp w takes fine rows i = w, w + nwarp, ...; it computes e_I, I = agg(i) + cb,
 // exactly as k_gemv does for row I (the same lane split and warp_sum tree: bitwise the same e_I) and
