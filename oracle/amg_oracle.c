@@ -787,7 +787,8 @@ static void ofcg_inner(const orc_h *h, int l, int nu, const double *b, double *e
         oB(h, l, nu, rho, z);
         memcpy(d, z, sizeof(double) * n);
         for (int j = 0; j < i; ++j) {
-            double beta = odot(n, z, Q + (int64_t)j * n) / dq[j];
+            /* d_j = 0 (only when rho was 0, reading A13) gives d_j.q_j = 0: that direction adds nothing */
+            double beta = dq[j] != 0.0 ? odot(n, z, Q + (int64_t)j * n) / dq[j] : 0.0;
             for (int64_t k = 0; k < n; ++k) d[k] -= beta * D[(int64_t)j * n + k];
         }
         ospmv(A, d, q);

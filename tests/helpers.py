@@ -167,3 +167,39 @@ def edge_key(w, a, b, seed, level, pas):
     lo, hi = min(a, b), max(a, b)
     h = splitmix64(((lo << 32) | hi) ^ salt)
     return (int(w), h, lo, hi)
+
+
+def fcg_restarted(A, b, Bop, tol, maxit, restart, x0=None, anorm_stop=None):
+    """Flexible CG with a window of at most `restart` stored directions (PAPER.md l.322-323:
+    "restart ... every five iterations"), written from the method's definition:
+    every new direction is B(r) made A-orthogonal to the directions of the current window; after
+    `restart` directions the window is emptied (x and r kept).  Returns the list of iterates
+    x_0, x_1, ... and the iteration count at the stop.  anorm_stop = (x*, ) switches to the paper's
+    relative A-norm error test ||x_k - x*||_A <= tol ||x_0 - x*||_A, evaluated densely."""
+    x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=float)
+    r = b - A @ x
+    bn = np.linalg.norm(b)
+    win = []  # (d, Ad, d.Ad)
+    xs = [x.copy()]
+
+    def aerr(v):
+        e = v - anorm_stop
+        return np.sqrt(max(e @ (A @ e), 0.0))
+
+    e0 = aerr(x) if anorm_stop is not None else None
+    for k in range(maxit + 1):
+        done = aerr(x) <= tol * e0 if anorm_stop is not None else np.linalg.norm(r) <= tol * bn
+        if done or k == maxit:
+            return xs, k
+        z = Bop(r)
+        d = z - sum(((z @ Ad) / dAd) * dj for dj, Ad, dAd in win) if win else z.copy()
+        q = A @ d
+        dq = d @ q
+        a = (d @ r) / dq
+        x = x + a * d
+        r = r - a * q
+        xs.append(x.copy())
+        win.append((d, q, dq))
+        if len(win) == restart:
+            win = []
+    return xs, maxit

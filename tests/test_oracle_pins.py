@@ -778,3 +778,127 @@ def test_kcycle_three_and_four_levels_pinned(oracle_mod, gen_mod):
             x2 = x1 + R @ (r - A @ x1)
             z1 = hk.precond(r, nu=1)
             assert np.linalg.norm(z1 - x2) <= 1e-12 * np.linalg.norm(x2)
+
+
+# ----------------------------------------------------------------- sub-rules pinned independently
+def test_attach_rule_recomputed(oracle_mod):
+    """Reading A3 (SURVEY 8(c) O3c 'Attach'; matching named at P:71-73): every vertex left unmatched
+    by the maximal matching joins the pair of its MAX-key neighbour (all its neighbours are matched);
+    isolated vertices stay singletons; ids are leader ranks (A4).  Recomputed here with the test's own
+    key function (tests/helpers.py edge_key, docs/keys.md) from the matching alone (itself pinned by
+    brute force above), and checked to discriminate: on these graphs a first-neighbour or min-key
+    attach gives different aggregates."""
+    rng = np.random.default_rng(77)
+    discriminating = 0
+    for trial in range(60):
+        n = int(rng.integers(6, 250))
+        rp, ci, w, _, _ = _random_pass_graph(rng, n, rng.uniform(1.5, 6), int(rng.integers(1, 4)))
+        seed, level, pas = trial * 7 + 1, trial % 4, trial % 3
+        mate, _ = oracle_mod.match(rp, ci, w, seed=seed, level=level, pass_=pas, rule=1)
+        got, nc = oracle_mod.aggregate_pass(rp, ci, w, seed=seed, level=level, pass_=pas, rule=1)
+
+        def expected(choose):
+            leader = np.empty(n, np.int64)
+            for v in range(n):
+                nb = list(range(rp[v], rp[v + 1]))
+                if mate[v] >= 0:
+                    leader[v] = min(v, mate[v])
+                elif not nb:
+                    leader[v] = v
+                else:
+                    u = choose(v, nb)
+                    assert mate[u] >= 0  # maximality
+                    leader[v] = min(u, mate[u])
+            leaders = sorted(set(leader.tolist()))
+            rank = {L: k for k, L in enumerate(leaders)}
+            return np.array([rank[L] for L in leader], np.int32), len(leaders)
+
+        def by_key(sign):
+            def choose(v, nb):
+                keys = [H.edge_key(w[p], v, ci[p], seed, level, pas) for p in nb]
+                best = max(range(len(nb)), key=lambda k: keys[k]) if sign > 0 else \
+                    min(range(len(nb)), key=lambda k: keys[k])
+                return int(ci[nb[best]])
+            return choose
+
+        ref, ncr = expected(by_key(+1))
+        assert nc == ncr and np.array_equal(got, ref), f"trial {trial}"
+        for alt in (by_key(-1), lambda v, nb: int(ci[nb[0]])):
+            a, _ = expected(alt)
+            discriminating += int(not np.array_equal(a, ref))
+    assert discriminating >= 40  # the pin would catch a min-key or first-neighbour attach
+
+
+def test_restart_window_iterates(oracle_mod, gen_mod):
+    """Restart every five iterations: the oracle's outer FCG equals an
+    independent numpy FCG (tests/helpers.py fcg_restarted) with the oracle's preconditioner used as
+    a black box, iterate by iterate (orc_solve stopped after k iterations by max_iter = k), for
+    restart 5 and 3 and for the linear V-cycle (cycle 1) and the nonlinear k-cycle (cycle 0).  The
+    same reference with the window cleared one step late, or never, differs by far more than the
+    tolerance, so an off-by-one or a missing clear fails."""
+    p = gen_mod.grid2d(24)
+    A = H.A0_dense(p)
+    b = gen_mod.rhs(p.n, 3)
+    K = 13
+    for cycle in (1, 0):
+        for W in (5, 3):
+            hb = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=30, cycle=cycle, restart=W)
+            Bop = lambda r: hb.precond(r, nu=2)  # noqa: E731
+            xs, _ = H.fcg_restarted(A, b, Bop, 1e-30, K, W)
+            late, _ = H.fcg_restarted(A, b, Bop, 1e-30, K, W + 1)
+            never, _ = H.fcg_restarted(A, b, Bop, 1e-30, K, 10 ** 6)
+            sep = 0.0
+            for k in range(1, K + 1):
+                hk = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=30, cycle=cycle, restart=W,
+                                          max_iter=k)
+                res = hk.solve(b, tol=1e-30, nu=2)
+                assert res["status"] == oracle_mod.ORC_NOT_CONVERGED and res["iters"] == k
+                scale = max(np.linalg.norm(xs[k]), 1e-300)
+                assert np.linalg.norm(res["x"] - xs[k]) <= 1e-9 * scale, (cycle, W, k)
+                sep = max(sep, np.linalg.norm(late[k] - xs[k]) / scale, np.linalg.norm(never[k] - xs[k]) / scale)
+            assert sep > 1e-6, (cycle, W, sep)
+
+
+def test_anorm_stop_rule_dense(oracle_mod, gen_mod):
+    """The paper's stopping test, relative A-norm error reduction 1e-8, evaluated with a
+    dense A: the oracle stops at the FIRST k with ||x_k - x*||_A <= tol ||x_0 - x*||_A, i.e. at k
+    the dense ratio is <= tol and at k - 1 (same hierarchy stopped by max_iter) it is > tol; the
+    iteration count equals the independent numpy FCG's with the same dense test."""
+    for name, p, d in (("grid", gen_mod.grid2d(24), True), ("rgg", gen_mod.rgg(1500, seed=4), False)):
+        A = H.A0_dense(p)
+        rng = np.random.default_rng(5)
+        xstar = rng.standard_normal(p.n)
+        if not d:
+            xstar -= xstar.mean()
+        b = A @ xstar
+        dd = p.d if d else None
+        for tol in (1e-4, 1e-8):
+            h = oracle_mod.Hierarchy(p.rp, p.ci, p.val, dd, 2, 3, coarsest_size=30)
+            res = h.solve(b, tol=tol, nu=2, xstar=xstar)
+            assert res["status"] == 0
+            k = res["iters"]
+
+            def ratio(x):
+                e = x - xstar
+                return np.sqrt(e @ (A @ e)) / np.sqrt(xstar @ (A @ xstar))
+
+            assert ratio(res["x"]) <= tol * (1 + 1e-9), name
+            hp = oracle_mod.Hierarchy(p.rp, p.ci, p.val, dd, 2, 3, coarsest_size=30, max_iter=k - 1)
+            prev = hp.solve(b, tol=tol, nu=2, xstar=xstar)
+            assert prev["status"] == oracle_mod.ORC_NOT_CONVERGED and ratio(prev["x"]) > tol, name
+            xs, kref = H.fcg_restarted(A, b, lambda r: h.precond(r, nu=2) - (0 if d else h.precond(r, nu=2).mean()),
+                                       tol, 200, 5, anorm_stop=xstar)
+            assert kref == k, (name, tol, kref, k)
+
+
+def test_zero_residual_inner_fcg(oracle_mod, gen_mod):
+    """Reading A13 (inner FCG): rho = 0 gives d = 0 and d.q = 0; the step and every later
+    orthogonalisation against that direction contribute nothing, so B_l(0) = 0 exactly (no 0/0) for
+    nu = 1, 2, 3 on a hierarchy with inner FCG levels (L >= 3); B is positively homogeneous, so the
+    zero vector is its only fixed output for r = 0."""
+    p = gen_mod.grid2d(24)
+    h = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, 2, 3, coarsest_size=10)
+    assert h.nlev >= 3
+    for nu in (1, 2, 3):
+        z = h.precond(np.zeros(p.n), nu=nu)
+        assert np.all(np.isfinite(z)) and not np.any(z), nu
