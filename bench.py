@@ -47,8 +47,41 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--per-config-steps", type=int, default=3)
     ap.add_argument("--dist", action="store_true", help="use the row-partitioned path even on one GPU")
     return ap.parse_args()
+
+
+def relaunch_if_needed(a):
+    """--gpus N > 1 outside torchrun: re-exec this script as N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 and exit with its status.  Under torchrun the world size must
+    equal --gpus."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != a.gpus:
+            print(json.dumps({"error": f"WORLD_SIZE={world_env} but --gpus {a.gpus}"}), flush=True)
+            sys.exit(2)
+        return
+    if a.gpus <= 1 or a.impl == "reference":
+        return
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(json.dumps({"error": f"--gpus {a.gpus} but only {have} visible CUDA device(s)"}), flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init log (rank count) stays visible on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def dist_env():
@@ -121,6 +154,33 @@ def oracle_sample(cfg_name: str, size: int):
                 value=p.n * r["iters"] / (t2 - t0), status=r["status"])
 
 
+def host_cpu():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+def committed_full_size(cfg_name: str):
+    """The oracle's full-size run of this config, committed by tools/oracle_golden.py (calls only
+    oracle/ and inputs/): setup + solve seconds, iterations, and the host it ran on."""
+    path = os.path.join(ROOT, "tests", "golden", "oracle_iters.json")
+    try:
+        g = json.load(open(path))[cfg_name]
+    except Exception:
+        return None
+    tot = g["oracle_setup_s"] + g["oracle_solve_s"]
+    n = g["levels"][0]
+    return {"value": n * g["iters"] / tot, "unit": UNIT, "n": n, "iters": g["iters"], "setup_s": g["oracle_setup_s"],
+            "solve_s": g["oracle_solve_s"], "host": g.get("host"), "threads": 1,
+            "source": "tests/golden/oracle_iters.json (tools/oracle_golden.py, single-threaded oracle)"}
+
+
 def sample_size(cfg_name: str, steps: int) -> int:
     """Bounded sample of the workload for the oracle: the same recipe at a reduced grid/point count,
     sized so the whole run stays within a few minutes."""
@@ -132,6 +192,12 @@ def sample_size(cfg_name: str, steps: int) -> int:
     if cfg_name == "C5":
         return 1_000_000 if steps <= 16 else 500_000
     return 1024 if steps <= 16 else 512
+
+
+def cpu_sample_size(cfg_name: str) -> int:
+    """cpu_baseline leg of our arm (one run): the largest sample of the recipe that stays within
+    ~10-40 s single-threaded, so the per-unknown cost is close to the full-size run's."""
+    return {"C1": 64, "C2": 512, "C3": 2048, "C4": 128, "C5": 2_000_000}[cfg_name]
 
 
 def model_bytes_per_iter(n, nnz, m, nu, W=5):
@@ -166,15 +232,89 @@ def run_reference(a):
     tot = sum(r["total_s"] for r in res)
     units = sum(r["n"] * r["iters"] for r in res)
     value = units / tot
+    model, nproc = host_cpu()
     sample = (f"{a.config} recipe at size {size} (n={res[0]['n']}), oracle setup+solve to tol, "
-              f"{res[0]['iters']} iters, single thread")
+              f"{res[0]['iters']} iters, single thread on {model} ({nproc} logical CPUs)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[a.config], "sample": sample},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu_model": model, "nproc": nproc,
+                             "full_size_committed": committed_full_size(a.config)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ other BASELINE configs (per_config)
+CEILING = {"C3": 6.2e9, "C4": 4.8e9, "C5": 4.3e9}  # SURVEY 8(d) unknowns*iter/s at 8 TB/s (uncompressed model)
+
+
+def run_config(amg, torch, dev, stream, cfg, steps, **opt_over):
+    """One BASELINE config at full size on this GPU: 1 warm-up + `steps` timed steps (setup + solve
+    + free, inputs resident in HBM, CUDA events on the caller's stream); the library's own device
+    timings split setup / solve."""
+    from inputs import gen
+
+    p = gen.problem(cfg)
+    prm = p.params
+    arrs = [None if v is None else torch.from_numpy(v).to(dev) for v in (p.rp, p.ci, p.val, p.d)]
+    b = torch.from_numpy(gen.rhs(p.n, prm["seed"])).to(dev)
+    x = torch.zeros(p.n, dtype=torch.float64, device=dev)
+    opts = amg.amg_options_default(coarsest_size=prm["coarsest_size"], seed=prm["seed"],
+                                   stream=stream.cuda_stream, **opt_over)
+
+    def step():
+        h = amg.amg_setup(*arrs, prm["passes"], prm["degree"], opts)
+        x.zero_()
+        st, it, rr = amg.amg_solve(h, b, x, prm["tol"], prm["k_inner"])
+        info = amg.amg_get_info(h)
+        amg.amg_free(h)
+        return st, it, rr, info
+
+    step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = [step() for _ in range(steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    inf = res[-1][3]
+    its = [r[1] for r in res]
+    it = statistics.median(its)
+    setup_ms = statistics.median(r[3]["setup_ms"] for r in res)
+    solve_ms = statistics.median(r[3]["solve_ms"] for r in res)
+    pm = sum(r[3]["prof_smoother_ms"] for r in res)
+    pn = sum(r[3]["prof_smoother_launches"] for r in res)
+    step_us = 1e3 * pm / pn if pn else None
+    m = prm["degree"]
+    gold = None
+    try:
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_iters.json")))[cfg]["iters"]
+    except Exception:
+        pass
+    mb = model_bytes_per_iter(inf["n"], inf["nnz"], m, prm["k_inner"])
+    out = {
+        "n": p.n, "nnz": p.nnz, "levels": inf["levels"], "n_levels": inf["n"],
+        "value": p.n * it / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+        "setup_ms": setup_ms, "solve_ms": solve_ms, "iters": its, "status": [r[0] for r in res],
+        "oracle_iters": gold, "iters_within_1": (gold is not None and all(abs(i - gold) <= 1 for i in its)),
+        "ms_per_iter": solve_ms / it, "us_per_iter": 1e3 * solve_ms / it,
+        "launches_per_iter": inf["launches_per_iter"], "true_relres": inf["last_true_relres"],
+        "level0_step_us": step_us, "level0_step_bytes": inf["prof_smoother_bytes"],
+        "level0_step_GBps": (inf["prof_smoother_bytes"] / (step_us * 1e-6) / 1e9) if step_us else None,
+        "level0_smoother_share": ((2 * m + 1) * it * step_us * 1e-3 / solve_ms) if step_us else None,
+        "solve_model_GBps": mb * it / (solve_ms / 1e3) / 1e9,
+        "survey_ceiling_unknowns_iter_s": CEILING.get(cfg),
+        "format": {0: "CSR tiles", 1: "SELL-32 fp64/int32", 2: "SELL-32 compressed"}.get(inf["level0_format"]),
+    }
+    if opt_over:
+        out["options"] = dict(opt_over)
+    del arrs, b, x
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------ our arm
@@ -342,11 +482,31 @@ def main_ours(a):
     # ---- cpu baseline: the oracle on a bounded sample of the same workload
     cpu = None
     if not a.no_cpu_baseline and world == 1:
-        size = sample_size(a.config, 1)
+        size = cpu_sample_size(a.config)
         r = oracle_sample(a.config, size)
+        model, nproc = host_cpu()
         cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{a.config} recipe at size {size} (n={r['n']}): oracle setup {r['setup_s']:.2f}s + "
-                         f"solve {r['solve_s']:.2f}s, {r['iters']} iters, single thread; value = n*iters/total"}
+                         f"solve {r['solve_s']:.2f}s, {r['iters']} iters, single thread; value = n*iters/total",
+               "cpu_model": model, "nproc": nproc,
+               "full_size_committed": committed_full_size(a.config)}
+
+    # ---- the other BASELINE configs at full size (and C3 with uncompressed streams), N = 1 only
+    per_config = None
+    if not a.no_per_config and world == 1:
+        per_config = {}
+        for cfg, over in (("C1", {}), ("C2", {}), ("C4", {}), ("C5", {}), ("C3", {"compress": 0})):
+            key = cfg if not over else cfg + "_uncompressed"
+            if cfg == a.config and not over:
+                continue
+            try:
+                per_config[key] = run_config(amg, torch, dev, stream, cfg, a.per_config_steps, **over)
+            except Exception as e:  # noqa: BLE001 -- reported, not hidden
+                per_config[key] = {"error": repr(e)}
+        if "C3_uncompressed" in per_config and per_config["C3_uncompressed"].get("level0_step_us"):
+            u = per_config["C3_uncompressed"]
+            u["level0_step_survey_model_bytes"] = 12 * u["nnz"] + 36 * u["n"]
+            u["level0_step_survey_model_GBps"] = u["level0_step_survey_model_bytes"] / (u["level0_step_us"] * 1e-6) / 1e9
 
     mb = model_bytes_per_iter(last["n"], last["nnz"], prm["degree"], prm["k_inner"])
     line = {
@@ -368,7 +528,7 @@ def main_ours(a):
         "solve_model": {"bytes_per_iter": mb, "effective_GBps": mb * statistics.mean(iters) / (solve_ms / 1e3) / 1e9,
                         "model": "SURVEY 8(d) uncompressed byte model (int32/fp64) of one outer iteration"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "launches_per_iter": last["launches_per_iter"], "clocks": clk,
+        "launches_per_iter": last["launches_per_iter"], "clocks": clk, "per_config": per_config,
         "final_relres": infos[-1][2], "true_relres": last["last_true_relres"],
     }
     print(json.dumps(line), flush=True)
@@ -381,6 +541,7 @@ def main_ours(a):
 
 if __name__ == "__main__":
     args = parse()
+    relaunch_if_needed(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -22,8 +22,10 @@
  * part of the call).  All computation runs in the library's CUDA kernels; no
  * step of setup or solve runs on the CPU.
  *
- * Threading.  A handle is used by one host thread at a time.  Calls block until
- * their GPU work is complete (setup and solve synchronise their stream).
+ * Threading.  A handle is used by one host thread at a time; different handles
+ * may be used concurrently from different threads (each handle owns its own
+ * library stream).  Calls block until their GPU work is complete (setup and
+ * solve synchronise their stream).
  *
  * Errors.  Every call returns an int status (table below); no C++ exception
  * crosses the ABI.  amg_last_error() returns a thread-local message for the
@@ -127,7 +129,8 @@ typedef struct {
     int32_t  level0_format;           /* 0 CSR tiles, 1 SELL-32 fp64/int32, 2 SELL-32 compressed */
     int32_t  nranks;                  /* ranks of the communicator (1 for amg_setup) */
     int32_t  dist_levels;             /* number of row-partitioned levels g (levels >= g are replicated) */
-    int32_t  reserved1;
+    int32_t  level0_path;             /* bit 0: level 0's SpMV-class passes (its interior view when split) take the
+                                         TMA-staged kernel; bit 1: halo/compute overlap split (row-partitioned) */
 } amg_info;
 
 /* Fills *o with the defaults listed above.  Returns AMG_E_ARG if o == NULL. */

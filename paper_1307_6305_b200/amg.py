@@ -45,7 +45,7 @@ class amg_info(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("prof_smoother_ms", ctypes.c_double),
                 ("prof_smoother_launches", ctypes.c_int64), ("prof_smoother_bytes", ctypes.c_int64),
                 ("level0_format", ctypes.c_int32), ("nranks", ctypes.c_int32), ("dist_levels", ctypes.c_int32),
-                ("reserved1", ctypes.c_int32)]
+                ("level0_path", ctypes.c_int32)]
 
 
 class AmgError(RuntimeError):
@@ -109,6 +109,36 @@ def _ptr(a, dtype):
     return a.ctypes.data
 
 
+def _len(a):
+    if a is None:
+        return None
+    return int(a.numel()) if hasattr(a, "numel") else int(a.shape[0])
+
+
+def _last(a) -> int:
+    v = a[-1]
+    return int(v.item() if hasattr(v, "item") else v)
+
+
+def _check_csr(row_ptr, col, val, d, n):
+    """Lengths only (the library validates the contents): col and val hold row_ptr[n] entries, d has
+    n; a shorter buffer would otherwise be read past its end by the staging copies."""
+    if n < 1:
+        raise ValueError("row_ptr must have at least 2 entries")
+    nnz = _last(row_ptr)
+    if _len(col) != nnz or _len(val) != nnz:
+        raise ValueError(f"col/val must have row_ptr[-1] = {nnz} entries, got {_len(col)}/{_len(val)}")
+    if d is not None and _len(d) != n:
+        raise ValueError(f"d must have n = {n} entries, got {_len(d)}")
+
+
+def _check_vec(h, **vecs):
+    n = getattr(h, "n_local", None)
+    for k, v in vecs.items():
+        if n is not None and v is not None and _len(v) != n:
+            raise ValueError(f"{k} must have n = {n} entries (this handle's rows), got {_len(v)}")
+
+
 def _check(st: int, what: str):
     if st not in (AMG_OK, AMG_NOT_CONVERGED):
         raise AmgError(st, f"{what}: {amg_last_error()}")
@@ -131,15 +161,18 @@ def amg_setup(row_ptr, col, val, d, n_match_passes: int, poly_degree: int, opts:
     """Build the hierarchy; returns an opaque handle (ctypes.c_void_p)."""
     h = ctypes.c_void_p()
     n = (row_ptr.shape[0] if hasattr(row_ptr, "shape") else len(row_ptr)) - 1
+    _check_csr(row_ptr, col, val, d, n)
     st = load().amg_setup(ctypes.byref(h), n, _ptr(row_ptr, np.int64), _ptr(col, np.int32), _ptr(val, np.float64),
                           _ptr(d, np.float64), n_match_passes, poly_degree,
                           ctypes.byref(opts) if opts is not None else None)
     _check(st, "amg_setup")
+    h.n_local = n
     return h
 
 
 def amg_solve(h, b, x, tol: float, k_inner: int):
     """Solve A x = b in place of x; returns (status, iters, relres)."""
+    _check_vec(h, b=b, x=x)
     it = ctypes.c_int32()
     rr = ctypes.c_double()
     st = load().amg_solve(h, _ptr(b, np.float64), _ptr(x, np.float64), tol, k_inner, ctypes.byref(it),
@@ -167,7 +200,7 @@ def amg_get_info(h) -> dict:
                 launches_last_setup=inf.launches_last_setup, device_bytes=inf.device_bytes,
                 prof_smoother_ms=inf.prof_smoother_ms, prof_smoother_launches=inf.prof_smoother_launches,
                 prof_smoother_bytes=inf.prof_smoother_bytes, level0_format=inf.level0_format, nranks=inf.nranks,
-                dist_levels=inf.dist_levels)
+                dist_levels=inf.dist_levels, level0_path=inf.level0_path)
 
 
 # ---------------------------------------------------------------- parity hooks (test-only)
@@ -247,10 +280,12 @@ def amg_setup_dist(comm, n_global: int, row_begin: int, row_ptr, col_global, val
     """Collective setup of this rank's row block [row_begin, row_begin + n_local) (global column ids)."""
     h = ctypes.c_void_p()
     n_local = (row_ptr.shape[0] if hasattr(row_ptr, "shape") else len(row_ptr)) - 1
+    _check_csr(row_ptr, col_global, val, d, n_local)
     st = load().amg_setup_dist(ctypes.byref(h), comm, n_global, row_begin, n_local, _ptr(row_ptr, np.int64),
                                _ptr(col_global, np.int32), _ptr(val, np.float64), _ptr(d, np.float64),
                                n_match_passes, poly_degree, ctypes.byref(opts) if opts is not None else None)
     _check(st, "amg_setup_dist")
+    h.n_local = n_local
     return h
 
 

@@ -79,6 +79,8 @@ struct SpOp {          // the operator of one level as the SpMV-class kernels se
     bool sell = false;     // true: SELL-32 warp-per-slice kernel; false: CSR row-tile kernel
 };
 
+bool tma_eligible(const SpOp& op);  // format/size part of the TMA-staged kernel's eligibility
+
 struct DotScratch {    // deterministic two-stage reductions (per-block partials + last-block sum)
     double* partials = nullptr;  // [kMaxWin+2][max grid]
     unsigned* ticket = nullptr;  // zero-initialised counter, reset by the last block
@@ -99,8 +101,8 @@ void dfree(void* p, cudaStream_t s);
 
 // validation of the user CSR (reading A17).  Returns bit flags (0 = valid).
 // Columns must lie in [cmin, cmax) ([0, n) on one GPU; [-nlo, n+nhi) relative on a row-partitioned level).
-int pattern_rp32(int n, const int64_t* rp, const int32_t* ci, int* rp32, cudaStream_t s);
-int validate_input(int n, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v, const double* d,
+int pattern_rp32(int n, int64_t nnz, const int64_t* rp, const int32_t* ci, int* rp32, cudaStream_t s);
+int validate_input(int n, int64_t nnz, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v, const double* d,
                    cudaStream_t s);
 // A_0 = L + diag(d) with inserted missing diagonals; returns a fresh Csr.
 Csr form_A0(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s);

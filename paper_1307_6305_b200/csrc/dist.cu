@@ -42,15 +42,22 @@ static int gridn(int64_t n) {
 
 // ------------------------------------------------------------------ kernels
 // global column ids outside the own block [gbeg, gend) (halo candidates; duplicates allowed)
-__global__ void k_halo_collect(int n, const int64_t* __restrict__ rp, const int* __restrict__ ci, int64_t gbeg,
-                               int64_t gend, int64_t nglob, int* __restrict__ out, int* __restrict__ cnt,
+// (row ranges outside [0, nnz] set *bad = VF_RP (64) and are skipped; bad columns set VF_RANGE (1))
+__global__ void k_halo_collect(int n, int64_t nnz, const int64_t* __restrict__ rp, const int* __restrict__ ci,
+                               int64_t gbeg, int64_t gend, int64_t nglob, int* __restrict__ out, int* __restrict__ cnt,
                                int* __restrict__ bad) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t p0 = rp[i], p1 = rp[i + 1];
+        if (p0 < 0 || p1 < p0 || p1 > nnz || (i == 0 && p0 != 0) || (i == n - 1 && p1 != nnz)) {
+            atomicOr(bad, 64);
+            continue;
+        }
+        for (int64_t p = p0; p < p1; ++p) {
             const int c = ci[p];
-            if (c < 0 || (int64_t)c >= nglob) { *bad = 1; continue; }
+            if (c < 0 || (int64_t)c >= nglob) { atomicOr(bad, 1); continue; }
             if ((int64_t)c < gbeg || (int64_t)c >= gend) out[atomicAdd(cnt, 1)] = c;
         }
+    }
 }
 
 __device__ __forceinline__ int lower_bound_i(const int* a, int n, int x) {
@@ -543,7 +550,7 @@ void build_dist(amg_hierarchy* h, int64_t n_global, int64_t row_begin, int n_loc
     int* cand = dalloc<int>((size_t)nnz_in + 1, s);
     int* cnt = dalloc<int>(2, s);
     CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), s));
-    k_halo_collect<<<gridn(n), kBlock, 0, s>>>(n, rp, ci_g, gbeg, gend, n_global, cand, cnt, cnt + 1);
+    k_halo_collect<<<gridn(n), kBlock, 0, s>>>(n, nnz_in, rp, ci_g, gbeg, gend, n_global, cand, cnt, cnt + 1);
     ++g_launches;
     CK(cudaGetLastError());
     int hc[2] = {0, 0};
@@ -558,7 +565,7 @@ void build_dist(amg_hierarchy* h, int64_t n_global, int64_t row_begin, int n_loc
     L0.nglob = n_global;
     L0.offs = offs;
     std::vector<std::vector<int>> req;
-    int vf = hc[1] ? 1 : 0;  // VF_RANGE
+    int vf = hc[1];  // VF_RANGE / VF_RP
     int* ci_r = dalloc<int>((size_t)nnz_in + 8, s);
     if (!vf) {
         plan_halo(gbeg, n, offs, me, hid, L0.H, req);
@@ -572,7 +579,7 @@ void build_dist(amg_hierarchy* h, int64_t n_global, int64_t row_begin, int n_loc
         ++g_launches;
         CK(cudaGetLastError());
         dfree(dh, s);
-        vf |= validate_input(n, -L0.H.nlo, n + L0.H.nhi, rp, ci_r, v, d, s);
+        vf |= validate_input(n, nnz_in, -L0.H.nlo, n + L0.H.nhi, rp, ci_r, v, d, s);
     }
     const int nonzero_d = (d && any_nonzero(n, d, s)) ? 1 : 0;
     const std::vector<int> flags = allgather_vec_host(c, std::vector<int>{vf, nonzero_d}, s);

@@ -217,6 +217,33 @@ static void pinned_give(double* p) {
     g_pin_free.push_back(p);
 }
 
+// Library streams: every live handle owns one (two handles may be used concurrently from different
+// host threads), checked out of a per-device free list at setup and returned at amg_free after the
+// handle's work has drained.  Reusing the stream (LIFO) keeps the memory a handle freed
+// (stream-ordered) immediately reusable by the next setup without growing the pool.
+static std::mutex g_stream_mu;
+static std::vector<cudaStream_t> g_stream_free[64];
+
+static cudaStream_t stream_acquire(int dev) {
+    {
+        std::lock_guard<std::mutex> lk(g_stream_mu);
+        if (!g_stream_free[dev].empty()) {
+            cudaStream_t s = g_stream_free[dev].back();
+            g_stream_free[dev].pop_back();
+            return s;
+        }
+    }
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+static void stream_release(int dev, cudaStream_t s) {
+    if (!s) return;
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    g_stream_free[dev].push_back(s);
+}
+
 static void release(amg_hierarchy* h) {
     if (!h) return;
     static const bool trace = getenv("AMG_FREE_TRACE") != nullptr;
@@ -235,7 +262,7 @@ static void release(amg_hierarchy* h) {
         for (void* p : h->ws_allocs) dfree(p, h->s);
     }
     const double t2 = trace ? now_ms() : 0.0;
-    if (h->s) cudaStreamSynchronize(h->s);  // the stream itself is the thread's persistent library stream
+    if (h->s) cudaStreamSynchronize(h->s);  // drained: the stream goes back to the free list below
     const double t3 = trace ? now_ms() : 0.0;
     if (trace) fprintf(stderr, "[amg free] graphs %.3f ms, frees %.3f ms, sync %.3f ms\n", t1 - t0, t2 - t1, t3 - t2);
     if (h->hsc) pinned_give(h->hsc);
@@ -246,6 +273,7 @@ static void release(amg_hierarchy* h) {
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
     if (h->ev_halo) cudaEventDestroy(h->ev_halo);
     if (h->cs) cudaStreamDestroy(h->cs);
+    if (h->s) stream_release(h->dev, h->s);
     delete h;
 }
 
@@ -339,7 +367,7 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     int nc0 = 0;
     if (host_vals && n > h->opt.coarsest_size) {
         int* rp32 = dalloc<int>((size_t)n + 8, s);
-        const int pf = pattern_rp32(n, rp, ci, rp32, s);
+        const int pf = pattern_rp32(n, nnz_in, rp, ci, rp32, s);
         if (pf) {
             dfree(rp32, s);
             join_vals();
@@ -364,7 +392,7 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
         dfree(rp32, s);
     }
     join_vals();
-    int vf = validate_input(n, 0, n, rp, ci, v, d, s);
+    int vf = validate_input(n, nnz_in, 0, n, rp, ci, v, d, s);
     pt.mark("validate");
     if (vf) {
         dfree(agg0, s);
@@ -1301,16 +1329,12 @@ static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t 
         h->m = poly_degree;
         h->p = n_match_passes;
         h->user = (cudaStream_t)o.stream;
-        // One persistent non-blocking stream per host thread and device, shared by that thread's
-        // handles: memory a handle frees (stream-ordered) is then always reusable by the next
-        // setup without growing the pool (blocks freed on destroyed streams are not reliably reused).
-        {
-            static thread_local cudaStream_t streams[64] = {};
+        {   // the handle's own non-blocking library stream (recycled, see stream_acquire)
             int dev = 0;
             CK(cudaGetDevice(&dev));
             if (dev < 0 || dev >= 64) throw Error(AMG_E_ARG, "device ordinal out of range");
-            if (!streams[dev]) CK(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
-            h->s = streams[dev];
+            h->dev = dev;
+            h->s = stream_acquire(dev);
         }
         CK(cudaEventCreate(&h->e0));
         CK(cudaEventCreate(&h->e1));
@@ -1420,6 +1444,7 @@ int amg_get_info(amg_handle h, amg_info* info) {
     {
         const Level& L0 = h->lev[0];
         r.level0_format = !L0.op.sell ? 0 : ((L0.S.vmode || L0.S.cmode) ? 2 : 1);
+        r.level0_path = (tma_eligible(L0.split ? L0.op_int : L0.op) ? 1 : 0) | (L0.split ? 2 : 0);
     }
     *info = r;
     return AMG_OK;

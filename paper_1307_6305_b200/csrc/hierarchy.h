@@ -69,7 +69,8 @@ struct Level {
 }  // namespace amg
 
 struct amg_hierarchy {
-    cudaStream_t s = nullptr;
+    cudaStream_t s = nullptr;     // this handle's library stream (stream_acquire / stream_release)
+    int dev = 0;                  // device the handle was created on
     cudaStream_t user = nullptr;
     int L = 0, m = 0, p = 0;
     bool singular = false;

@@ -113,12 +113,17 @@ enum : int {
 // Columns must lie in [cmin, cmax): [0, n) on one GPU; [-nlo, n + nhi) on a row-partitioned level
 // (columns relative to the first own row, halo outside [0, n)).  Symmetry is checked for pairs of
 // own rows (a cross-block pair is split between two ranks: the caller's contract).
-__global__ void k_validate(int n, int cmin, int cmax, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                           const double* __restrict__ v, const double* __restrict__ d, int* flags) {
+// Every row range is checked against [0, nnz] before it is read (a non-monotone row_ptr must give
+// AMG_E_INPUT, not an out-of-bounds read); so is the neighbour row searched for the symmetric entry.
+__device__ __forceinline__ bool row_ok(int64_t p0, int64_t p1, int64_t nnz) { return 0 <= p0 && p0 <= p1 && p1 <= nnz; }
+
+__global__ void k_validate(int n, int64_t nnz, int cmin, int cmax, const int64_t* __restrict__ rp,
+                           const int32_t* __restrict__ ci, const double* __restrict__ v, const double* __restrict__ d,
+                           int* flags) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         int f = 0;
         const int64_t p0 = rp[i], p1 = rp[i + 1];
-        if (p1 < p0 || (i == 0 && p0 != 0)) { atomicOr(flags, VF_RP); continue; }
+        if (!row_ok(p0, p1, nnz) || (i == 0 && p0 != 0) || (i == n - 1 && p1 != nnz)) { atomicOr(flags, VF_RP); continue; }
         double off = 0.0, dv = 0.0;
         bool has = false;
         for (int64_t p = p0; p < p1; ++p) {
@@ -130,11 +135,13 @@ __global__ void k_validate(int n, int cmin, int cmax, const int64_t* __restrict_
             off += -v[p];
             if (c < 0 || c >= n) continue;
             int64_t lo = rp[c], hi = rp[c + 1];
+            const int64_t end = hi;
+            if (!row_ok(lo, hi, nnz)) { f |= VF_RP; continue; }
             while (lo < hi) {
                 int64_t mid = (lo + hi) >> 1;
                 if (ci[mid] < i) lo = mid + 1; else hi = mid;
             }
-            if (!(lo < rp[c + 1] && ci[lo] == i && v[lo] == v[p])) f |= VF_ASYM;
+            if (!(lo < end && ci[lo] == i && v[lo] == v[p])) f |= VF_ASYM;
         }
         if (has && fabs(dv - off) > 1e-10 * (fabs(dv) + off)) f |= VF_DIAG;
         if (d && !(d[i] >= 0.0)) f |= VF_D;
@@ -145,13 +152,13 @@ __global__ void k_validate(int n, int cmin, int cmax, const int64_t* __restrict_
 // The pattern part of the checks (row_ptr monotone, columns in [0, n) and strictly increasing,
 // pattern symmetry) and the int32 row pointers of the pattern: enough to run the value-free matching passes of level 0
 // safely while the values are still being copied in (e2e path).
-__global__ void k_pattern_rp32(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+__global__ void k_pattern_rp32(int n, int64_t nnz, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                int* __restrict__ rp32, int* flags) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
         rp32[i] = (int)rp[i];
         if (i == n) continue;
         const int64_t p0 = rp[i], p1 = rp[i + 1];
-        if (p1 < p0 || (i == 0 && p0 != 0)) { atomicOr(flags, VF_RP); continue; }
+        if (!row_ok(p0, p1, nnz) || (i == 0 && p0 != 0) || (i == n - 1 && p1 != nnz)) { atomicOr(flags, VF_RP); continue; }
         int f = 0;
         for (int64_t p = p0; p < p1; ++p) {
             const int c = ci[p];
@@ -159,20 +166,22 @@ __global__ void k_pattern_rp32(int n, const int64_t* __restrict__ rp, const int3
             if (p > p0 && c <= ci[p - 1]) f |= VF_UNSORTED;
             if (c == i) continue;
             int64_t lo = rp[c], hi = rp[c + 1];  // the pattern must be symmetric (the matching relies on it)
+            const int64_t end = hi;
+            if (!row_ok(lo, hi, nnz)) { f |= VF_RP; continue; }
             while (lo < hi) {
                 const int64_t mid = (lo + hi) >> 1;
                 if (ci[mid] < i) lo = mid + 1; else hi = mid;
             }
-            if (!(lo < rp[c + 1] && ci[lo] == i)) f |= VF_ASYM;
+            if (!(lo < end && ci[lo] == i)) f |= VF_ASYM;
         }
         if (f) atomicOr(flags, f);
     }
 }
 
-int pattern_rp32(int n, const int64_t* rp, const int32_t* ci, int* rp32, cudaStream_t s) {
+int pattern_rp32(int n, int64_t nnz, const int64_t* rp, const int32_t* ci, int* rp32, cudaStream_t s) {
     int* fl = dalloc<int>(1, s);
     CK(cudaMemsetAsync(fl, 0, sizeof(int), s));
-    k_pattern_rp32<<<grid_for((int64_t)n + 1), kBlock, 0, s>>>(n, rp, ci, rp32, fl);
+    k_pattern_rp32<<<grid_for((int64_t)n + 1), kBlock, 0, s>>>(n, nnz, rp, ci, rp32, fl);
     ++g_launches;
     CK(cudaGetLastError());
     int f = read_scalar(fl, s);
@@ -180,11 +189,11 @@ int pattern_rp32(int n, const int64_t* rp, const int32_t* ci, int* rp32, cudaStr
     return f;
 }
 
-int validate_input(int n, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v, const double* d,
-                   cudaStream_t s) {
+int validate_input(int n, int64_t nnz, int cmin, int cmax, const int64_t* rp, const int32_t* ci, const double* v,
+                   const double* d, cudaStream_t s) {
     int* fl = dalloc<int>(1, s);
     CK(cudaMemsetAsync(fl, 0, sizeof(int), s));
-    k_validate<<<grid_for(n), kBlock, 0, s>>>(n, cmin, cmax, rp, ci, v, d, fl);
+    k_validate<<<grid_for(n), kBlock, 0, s>>>(n, nnz, cmin, cmax, rp, ci, v, d, fl);
     ++g_launches;
     CK(cudaGetLastError());
     int f = read_scalar(fl, s);

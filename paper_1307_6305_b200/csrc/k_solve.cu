@@ -29,12 +29,16 @@ void init_device_props() {
 
 int vector_grid() { return g_num_sms * 4; }
 
-// grid of a grid-stride vector kernel over n elements: ~4 elements per thread, at most 4 CTAs/SM
+// grid of a grid-stride vector kernel over n elements: >= 8 elements per thread, at most 8 CTAs of
+// 256 threads per SM (the full 2048 threads: measured on the C3 level-0 vectors, tools/vec_micro.cu,
+// 4 CTAs/SM left too few loads in flight -- fcg_update 160 -> 125 us, multidot(4) 219 -> 97 us)
 static int vgrid(int64_t n) {
-    int64_t g = (n + 4 * kBlock - 1) / (4 * kBlock);
-    if (g > vector_grid()) g = vector_grid();
+    int64_t g = (n + 8 * kBlock - 1) / (8 * kBlock);
+    if (g > 2 * vector_grid()) g = 2 * vector_grid();
     return g < 1 ? 1 : (int)g;
 }
+
+static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 bool pdl_enabled() {
     static int on = -1;
@@ -1363,17 +1367,20 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 // TMA-staged path: SELL level with slices <= 8 wide, large enough to be bandwidth bound, and 16-byte
 // aligned streams (bulk copies move 16-byte multiples).  Returns false if not eligible.
-template <class Epi, bool DOTS>
-static bool launch_tma(const SpOp& op, const double* xg, const Epi& e, const double* v0, const double* v1,
-                       const DotScratch* ds, DotOut d, cudaStream_t s) {
+// the operator's format/size part of the TMA eligibility (the launch also needs 16-byte aligned vectors)
+bool tma_eligible(const SpOp& op) {
     static int min_slices = -1;  // AMG_TMA_MIN_SLICES (experiments)
     if (min_slices < 0) min_slices = getenv("AMG_TMA_MIN_SLICES") ? atoi(getenv("AMG_TMA_MIN_SLICES")) : 8 * 148 * kTmaWarps;
     static int max_w = -1;  // AMG_TMA_MAX_W (experiments)
     if (max_w < 0) max_w = getenv("AMG_TMA_MAX_W") ? atoi(getenv("AMG_TMA_MAX_W")) : 32;
     const int wcap = tma_wide_fmt(op.S.vmode, op.S.cmode) ? 32 : 16;  // W = 32 instances: wide formats only
-    if (!(tma_enabled() && op.sell && op.S.wmax <= std::min(max_w, wcap) && op.S.nslices >= min_slices && aligned16(xg) &&
-          (!v0 || aligned16(v0)) && (!v1 || aligned16(v1))))
-        return false;
+    return tma_enabled() && op.sell && op.S.wmax <= std::min(max_w, wcap) && op.S.nslices >= min_slices;
+}
+
+template <class Epi, bool DOTS>
+static bool launch_tma(const SpOp& op, const double* xg, const Epi& e, const double* v0, const double* v1,
+                       const DotScratch* ds, DotOut d, cudaStream_t s) {
+    if (!(tma_eligible(op) && aligned16(xg) && (!v0 || aligned16(v0)) && (!v1 || aligned16(v1)))) return false;
     double* part = ds ? ds->partials : nullptr;
     unsigned* tk = ds ? ds->ticket : nullptr;
     switch (op.S.vmode * 4 + op.S.cmode) {
@@ -1504,16 +1511,43 @@ void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, 
     ++g_launches;
 }
 
+// x_i += eH[agg_i].  V: quads of rows per thread and step (one int4 of agg, two double2 of x, four
+// L2-resident gathers of eH), two quads in flight per thread; the scalar loop takes the tail.
+template <bool V>
 __global__ void __launch_bounds__(kBlock) k_prolong(int n, const int* __restrict__ agg,
                                                     const double* __restrict__ eH, double* __restrict__ x) {
     pdl_trigger();
     pdl_wait();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += __ldg(eH + agg[i]);
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if constexpr (V) {
+        const int64_t n4 = n >> 2;
+        const int4* A4 = reinterpret_cast<const int4*>(agg);
+        double2* X2 = reinterpret_cast<double2*>(x);
+        int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; q + st < n4; q += 2 * st) {
+            const int4 a0 = A4[q], a1 = A4[q + st];
+            double2 x0 = X2[2 * q], x1 = X2[2 * q + 1], x2 = X2[2 * (q + st)], x3 = X2[2 * (q + st) + 1];
+            const double e0 = __ldg(eH + a0.x), e1 = __ldg(eH + a0.y), e2 = __ldg(eH + a0.z), e3 = __ldg(eH + a0.w);
+            const double e4 = __ldg(eH + a1.x), e5 = __ldg(eH + a1.y), e6 = __ldg(eH + a1.z), e7 = __ldg(eH + a1.w);
+            x0.x += e0; x0.y += e1; x1.x += e2; x1.y += e3;
+            x2.x += e4; x2.y += e5; x3.x += e6; x3.y += e7;
+            X2[2 * q] = x0; X2[2 * q + 1] = x1; X2[2 * (q + st)] = x2; X2[2 * (q + st) + 1] = x3;
+        }
+        for (; q < n4; q += st) {
+            const int4 a0 = A4[q];
+            double2 x0 = X2[2 * q], x1 = X2[2 * q + 1];
+            x0.x += __ldg(eH + a0.x); x0.y += __ldg(eH + a0.y); x1.x += __ldg(eH + a0.z); x1.y += __ldg(eH + a0.w);
+            X2[2 * q] = x0; X2[2 * q + 1] = x1;
+        }
+        i0 = n4 << 2;
+    }
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) x[i] += __ldg(eH + agg[i]);
 }
 
 void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s) {
-    const int grid = vgrid(n);
-    launch_k(k_prolong, dim3(grid), dim3(kBlock), 0, s, n, agg, eH, x);
+    if (al16(agg) && al16(x)) launch_k(k_prolong<true>, dim3(vgrid((n + 3) / 4)), dim3(kBlock), 0, s, n, agg, eH, x);
+    else launch_k(k_prolong<false>, dim3(vgrid(n)), dim3(kBlock), 0, s, n, agg, eH, x);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -1544,8 +1578,10 @@ void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_
 // Residual fused with the restriction on the small (L2-resident, launch-latency-bound) levels: one
 // warp per aggregate, lane = member (chunks of 32): each lane forms its row's residual f_i - (A x)_i
 // with the fma chain in CSR order (the SELL kernels' order: the same r_i), then every lane sums the
-// chunk's r in member order through shuffles starting from 0.0 (k_restrict's order): bitwise the same
-// rho_I, one launch and the residual vector's round trip less per visit.
+// chunk's r in member order through shuffles starting from 0.0 (k_restrict's order): on a SELL level
+// (and on a CSR-tile level whose rows all fit one thread's chain) bitwise the same rho_I as the
+// unfused pair; k_tiled's block-summed long rows round differently (within the parity tolerance).
+// One launch and the residual vector's round trip less per visit.
 __global__ void __launch_bounds__(kBlock) k_resid_restrict(int nc, const int* __restrict__ aptr,
                                                            const int* __restrict__ perm, const int* __restrict__ rp,
                                                            const int* __restrict__ ci, const double* __restrict__ v,
@@ -1619,23 +1655,65 @@ struct PtrArr {
     const double* p[kMaxWin];
 };
 
+// Vector kernels of the FCG iterations (outer: O8, inner: O7).  The level-0 vectors are 134 MB each
+// on C3, so these are HBM streams: double2 loads, two steps in flight per thread, 8 CTAs/SM
+// (tools/vec_micro.cu).  Each kernel has a scalar instance for vectors that are not 16-byte aligned
+// (never on the library's own buffers) and the scalar loop takes the odd tail element.
+
+// c_j = z . Q_j, j < W (deterministic two-stage reduction); W = 0: runtime w <= kMaxWin, scalar
+template <int W, bool V>
 __global__ void __launch_bounds__(kBlock) k_multidot(int n, const double* __restrict__ z, PtrArr Q, int w,
                                                      double* partials, unsigned* ticket, double* c) {
     pdl_trigger();
     pdl_wait();
-    double acc[kMaxWin];
+    constexpr int NA = W ? W : kMaxWin;
+    double acc[NA];
 #pragma unroll
-    for (int j = 0; j < kMaxWin; ++j) acc[j] = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        double zi = z[i];
+    for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if constexpr (V && W > 0) {
+        const int64_t n2 = n >> 1;
+        const double2* Z2 = reinterpret_cast<const double2*>(z);
+        int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; i + st < n2; i += 2 * st) {
+            const double2 za = Z2[i], zb = Z2[i + st];
+            double2 qa[W], qb[W];
 #pragma unroll
-        for (int j = 0; j < kMaxWin; ++j)
-            if (j < w) acc[j] += zi * Q.p[j][i];
+            for (int j = 0; j < W; ++j) {
+                qa[j] = reinterpret_cast<const double2*>(Q.p[j])[i];
+                qb[j] = reinterpret_cast<const double2*>(Q.p[j])[i + st];
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                acc[j] += za.x * qa[j].x;
+                acc[j] += za.y * qa[j].y;
+                acc[j] += zb.x * qb[j].x;
+                acc[j] += zb.y * qb[j].y;
+            }
+        }
+        for (; i < n2; i += st) {
+            const double2 za = Z2[i];
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const double2 q = reinterpret_cast<const double2*>(Q.p[j])[i];
+                acc[j] += za.x * q.x;
+                acc[j] += za.y * q.y;
+            }
+        }
+        i0 = n2 << 1;
     }
-    // reduce only the first w accumulators (w is uniform)
+    const int ww = W ? W : w;
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) {
+        const double zi = z[i];
+#pragma unroll
+        for (int j = 0; j < NA; ++j)
+            if (j < ww) acc[j] += zi * Q.p[j][i];
+    }
+    // reduce only the first ww accumulators (ww is uniform)
     __shared__ bool amlast;
     const int G = gridDim.x;
-    for (int j = 0; j < w; ++j) {
+    for (int j = 0; j < ww; ++j) {
         double b = block_sum(acc[j]);
         if (threadIdx.x == 0) partials[j * G + blockIdx.x] = b;
     }
@@ -1645,7 +1723,7 @@ __global__ void __launch_bounds__(kBlock) k_multidot(int n, const double* __rest
     __syncthreads();
     if (amlast) {
         __threadfence();
-        for (int j = 0; j < w; ++j) {
+        for (int j = 0; j < ww; ++j) {
             double v = 0.0;
             for (int b = threadIdx.x; b < G; b += blockDim.x) v += __ldcg(partials + j * G + b);
             v = block_sum(v);
@@ -1655,28 +1733,83 @@ __global__ void __launch_bounds__(kBlock) k_multidot(int n, const double* __rest
     }
 }
 
+static bool all_al16(const double* const* P, int w) {
+    for (int j = 0; j < w; ++j)
+        if (!al16(P[j])) return false;
+    return true;
+}
+
 void launch_multidot(int n, const double* z, const double* const* Q, int w, double* c, const DotScratch& ds,
                      cudaStream_t s) {
     PtrArr a{};
     for (int j = 0; j < w; ++j) a.p[j] = Q[j];
-    launch_k(k_multidot, dim3(vgrid(n)), dim3(kBlock), 0, s, n, z, a, w, ds.partials, ds.ticket, c);
+    const dim3 g(vgrid(n)), b(kBlock);
+    const bool v = al16(z) && all_al16(Q, w);
+    switch (v ? w : 0) {
+        case 1: launch_k(k_multidot<1, true>, g, b, 0, s, n, z, a, w, ds.partials, ds.ticket, c); break;
+        case 2: launch_k(k_multidot<2, true>, g, b, 0, s, n, z, a, w, ds.partials, ds.ticket, c); break;
+        case 3: launch_k(k_multidot<3, true>, g, b, 0, s, n, z, a, w, ds.partials, ds.ticket, c); break;
+        case 4: launch_k(k_multidot<4, true>, g, b, 0, s, n, z, a, w, ds.partials, ds.ticket, c); break;
+        default: launch_k(k_multidot<0, false>, g, b, 0, s, n, z, a, w, ds.partials, ds.ticket, c); break;
+    }
     CK(cudaGetLastError());
     ++g_launches;
 }
 
+// d = z - sum_{j<W} beta_j D_j, beta_j = c_j / (d_j.q_j) (0 when d_j.q_j = 0, reading A13)
+template <int W, bool V>
 __global__ void __launch_bounds__(kBlock) k_direction(int n, const double* __restrict__ z, PtrArr D,
                                                       const double* __restrict__ c, const double* __restrict__ dq,
                                                       int w, double* __restrict__ d) {
     pdl_trigger();
     pdl_wait();
-    double beta[kMaxWin];
+    constexpr int NA = W ? W : kMaxWin;
+    const int ww = W ? W : w;
+    double beta[NA];
 #pragma unroll
-    for (int j = 0; j < kMaxWin; ++j) beta[j] = j < w ? c[j] / dq[j] : 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (int j = 0; j < NA; ++j) beta[j] = (j < ww && dq[j] != 0.0) ? c[j] / dq[j] : 0.0;  // d_j = 0: no term (A13)
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if constexpr (V && W > 0) {
+        const int64_t n2 = n >> 1;
+        const double2* Z2 = reinterpret_cast<const double2*>(z);
+        double2* O2 = reinterpret_cast<double2*>(d);
+        int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; i + st < n2; i += 2 * st) {
+            double2 va = Z2[i], vb = Z2[i + st];
+            double2 pa[W], pb[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                pa[j] = reinterpret_cast<const double2*>(D.p[j])[i];
+                pb[j] = reinterpret_cast<const double2*>(D.p[j])[i + st];
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                va.x -= beta[j] * pa[j].x;
+                va.y -= beta[j] * pa[j].y;
+                vb.x -= beta[j] * pb[j].x;
+                vb.y -= beta[j] * pb[j].y;
+            }
+            O2[i] = va;
+            O2[i + st] = vb;
+        }
+        for (; i < n2; i += st) {
+            double2 va = Z2[i];
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const double2 p = reinterpret_cast<const double2*>(D.p[j])[i];
+                va.x -= beta[j] * p.x;
+                va.y -= beta[j] * p.y;
+            }
+            O2[i] = va;
+        }
+        i0 = n2 << 1;
+    }
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) {
         double v = z[i];
 #pragma unroll
-        for (int j = 0; j < kMaxWin; ++j)
-            if (j < w) v -= beta[j] * D.p[j][i];
+        for (int j = 0; j < NA; ++j)
+            if (j < ww) v -= beta[j] * D.p[j][i];
         d[i] = v;
     }
 }
@@ -1685,12 +1818,21 @@ void launch_direction(int n, const double* z, const double* const* D, const doub
                       double* d, cudaStream_t s) {
     PtrArr a{};
     for (int j = 0; j < w; ++j) a.p[j] = D[j];
-    launch_k(k_direction, dim3(vgrid(n)), dim3(kBlock), 0, s, n, z, a, c, dq, w, d);
+    const dim3 g(vgrid(n)), b(kBlock);
+    const bool v = al16(z) && al16(d) && all_al16(D, w);
+    switch (v ? w : 0) {
+        case 1: launch_k(k_direction<1, true>, g, b, 0, s, n, z, a, c, dq, w, d); break;
+        case 2: launch_k(k_direction<2, true>, g, b, 0, s, n, z, a, c, dq, w, d); break;
+        case 3: launch_k(k_direction<3, true>, g, b, 0, s, n, z, a, c, dq, w, d); break;
+        case 4: launch_k(k_direction<4, true>, g, b, 0, s, n, z, a, c, dq, w, d); break;
+        default: launch_k(k_direction<0, false>, g, b, 0, s, n, z, a, c, dq, w, d); break;
+    }
     CK(cudaGetLastError());
     ++g_launches;
 }
 
-template <bool ASSIGN, bool UPD_R, bool RR>
+// x (+)= alpha d; r -= alpha q; rr = r.r;  alpha = d.r / d.q (outer: d.q <= 0 or NaN is a breakdown)
+template <bool ASSIGN, bool UPD_R, bool RR, bool V>
 __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __restrict__ dr,
                                                        const double* __restrict__ dq, const double* __restrict__ d,
                                                        const double* __restrict__ q, double* __restrict__ x,
@@ -1707,7 +1849,33 @@ __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __re
         alpha = (den != 0.0) ? (*dr) / den : 0.0;
     }
     double acc[1] = {0.0};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if constexpr (V) {
+        const int64_t n2 = n >> 1;
+        const double2* D2 = reinterpret_cast<const double2*>(d);
+        const double2* Q2 = reinterpret_cast<const double2*>(q);
+        double2* X2 = reinterpret_cast<double2*>(x);
+        double2* R2 = reinterpret_cast<double2*>(r);
+        int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; i < n2; i += st) {
+            const double2 di = D2[i];
+            double2 xi;
+            if (!ASSIGN) xi = X2[i];
+            double2 ri, qi;
+            if (UPD_R) { ri = R2[i]; qi = Q2[i]; }
+            if (ASSIGN) { xi.x = alpha * di.x; xi.y = alpha * di.y; } else { xi.x += alpha * di.x; xi.y += alpha * di.y; }
+            X2[i] = xi;
+            if (UPD_R) {
+                ri.x = ri.x - alpha * qi.x;
+                ri.y = ri.y - alpha * qi.y;
+                R2[i] = ri;
+                if (RR) { acc[0] += ri.x * ri.x; acc[0] += ri.y * ri.y; }
+            }
+        }
+        i0 = n2 << 1;
+    }
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) {
         double di = d[i];
         if (ASSIGN) x[i] = alpha * di; else x[i] += alpha * di;
         if (UPD_R) {
@@ -1719,37 +1887,64 @@ __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __re
     if (RR) finalize_dots<1>(acc, partials, ticket, DotOut{{rr}});
 }
 
-void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
-                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s) {
-    dim3 g(vgrid(n)), b(kBlock);
+template <bool V>
+static void fcg_update_v(dim3 g, dim3 b, cudaStream_t s, int n, const double* dr, const double* dq, const double* d,
+                         const double* q, double* x, bool assign_x, double* r, double* rr, int* breakdown,
+                         const DotScratch& ds) {
     double* np = nullptr;
     unsigned* nt = nullptr;
     if (assign_x) {
-        if (r) launch_k(k_fcg_update<true, true, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
-        else   launch_k(k_fcg_update<true, false, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        if (r) launch_k(k_fcg_update<true, true, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        else   launch_k(k_fcg_update<true, false, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
     } else if (r && rr) {
-        launch_k(k_fcg_update<false, true, true>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, ds.partials, ds.ticket, rr);
+        launch_k(k_fcg_update<false, true, true, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, ds.partials, ds.ticket, rr);
     } else if (r) {
-        launch_k(k_fcg_update<false, true, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        launch_k(k_fcg_update<false, true, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
     } else {
-        launch_k(k_fcg_update<false, false, false>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        launch_k(k_fcg_update<false, false, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
     }
+}
+
+void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
+                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s) {
+    const dim3 g(vgrid(n)), b(kBlock);
+    if (al16(d) && al16(x) && (!r || (al16(r) && al16(q))))
+        fcg_update_v<true>(g, b, s, n, dr, dq, d, q, x, assign_x, r, rr, breakdown, ds);
+    else
+        fcg_update_v<false>(g, b, s, n, dr, dq, d, q, x, assign_x, r, rr, breakdown, ds);
     CK(cudaGetLastError());
     ++g_launches;
 }
 
+// sum_i x_i y_i (y = null: sum_i x_i), deterministic two-stage reduction
+template <bool V>
 __global__ void __launch_bounds__(kBlock) k_dot(int n, const double* __restrict__ x, const double* __restrict__ y,
                                                 double* partials, unsigned* ticket, double* out) {
     pdl_trigger();
     pdl_wait();
     double acc[1] = {0.0};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if constexpr (V) {
+        const int64_t n2 = n >> 1;
+        const double2* X2 = reinterpret_cast<const double2*>(x);
+        const double2* Y2 = reinterpret_cast<const double2*>(y);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += st) {
+            const double2 a = X2[i];
+            const double2 bb = y ? Y2[i] : make_double2(1.0, 1.0);
+            acc[0] += a.x * bb.x;
+            acc[0] += a.y * bb.y;
+        }
+        i0 = n2 << 1;
+    }
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st)
         acc[0] += x[i] * (y ? y[i] : 1.0);
     finalize_dots<1>(acc, partials, ticket, DotOut{{out}});
 }
 
 void launch_dot(int n, const double* x, const double* y, double* out, const DotScratch& ds, cudaStream_t s) {
-    launch_k(k_dot, dim3(vgrid(n)), dim3(kBlock), 0, s, n, x, y, ds.partials, ds.ticket, out);
+    if (al16(x) && (!y || al16(y))) launch_k(k_dot<true>, dim3(vgrid(n)), dim3(kBlock), 0, s, n, x, y, ds.partials, ds.ticket, out);
+    else launch_k(k_dot<false>, dim3(vgrid(n)), dim3(kBlock), 0, s, n, x, y, ds.partials, ds.ticket, out);
     CK(cudaGetLastError());
     ++g_launches;
 }

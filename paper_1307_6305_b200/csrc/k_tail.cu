@@ -191,7 +191,7 @@ __device__ __noinline__ void t_fcg(const TailArgs& A, int l, TCtx c) {
             cluster_sums<CL>(cj, i);
             for (int r = c.t; r < n; r += c.T) {
                 double v = L.Z[r];
-                for (int j = 0; j < i; ++j) v -= (cj[j] / dq[j]) * L.D[(size_t)j * n + r];
+                for (int j = 0; j < i; ++j) v -= (dq[j] != 0.0 ? cj[j] / dq[j] : 0.0) * L.D[(size_t)j * n + r];
                 Di[r] = v;
             }
             csync<CL>();

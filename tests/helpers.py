@@ -203,3 +203,18 @@ def fcg_restarted(A, b, Bop, tol, maxit, restart, x0=None, anorm_stop=None):
         if len(win) == restart:
             win = []
     return xs, maxit
+
+
+def assert_close(got, ref, tol, what=""):
+    """Parity bar, element by element and in norm: max_i |got_i - ref_i| <= tol * max_i |ref_i| and
+    ||got - ref||_2 <= tol ||ref||_2 (a handful of wrong rows cannot hide inside the 2-norm)."""
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    assert np.all(np.isfinite(got)), f"{what}: non-finite entries"
+    d = np.abs(got - ref)
+    scale = np.max(np.abs(ref)) if ref.size else 0.0
+    imax = int(np.argmax(d)) if d.size else 0
+    assert (d.max() if d.size else 0.0) <= tol * scale, \
+        f"{what}: max elementwise error {d.max():.3e} at {imax} > {tol:g} * max|ref| = {tol * scale:.3e}"
+    assert np.linalg.norm(got - ref) <= tol * np.linalg.norm(ref), f"{what}: 2-norm error"

@@ -92,3 +92,26 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(//|#).*", "", txt).lower() or f.endswith(".h"), f
                 assert "liboracle" not in txt and "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_binding_checks_buffer_lengths(amg_mod):
+    """The binding rejects buffers shorter than the CSR / handle sizes before calling into C (a short
+    host buffer would otherwise be read or written past its end by the library's copies)."""
+    import numpy as np
+    import pytest
+
+    rp = np.array([0, 2, 4], np.int64)
+    ci = np.array([0, 1, 0, 1], np.int32)
+    v = np.array([1.0, -1.0, -1.0, 1.0])
+    with pytest.raises(ValueError):
+        amg_mod.amg_setup(rp, ci[:3], v, None, 1, 2)
+    with pytest.raises(ValueError):
+        amg_mod.amg_setup(rp, ci, v[:3], None, 1, 2)
+    with pytest.raises(ValueError):
+        amg_mod.amg_setup(rp, ci, v, np.zeros(3), 1, 2)
+    h = ctypes.c_void_p(1)
+    h.n_local = 2
+    with pytest.raises(ValueError):
+        amg_mod.amg_solve(h, np.zeros(2), np.zeros(1), 1e-8, 2)
+    with pytest.raises(ValueError):
+        amg_mod.amg_solve(h, np.zeros(3), np.zeros(2), 1e-8, 2)

@@ -10,6 +10,8 @@ import os
 import numpy as np
 import pytest
 
+import helpers as H
+
 pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -122,20 +124,20 @@ def test_smoother_precond_coarse_parity(amg, gen_mod, oracle_mod, name):
             x = np.empty(n)
             amg.amg_level_smooth(h, l, f, x0, x)
             ref = hier.smooth(l, f, x0)
-            assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref), f"smoother level {l}"
+            H.assert_close(x, ref, 1e-12, f"smoother level {l}")
         for l in range(hier.nlev):
             n = hier.level_info(l)["n"]
             r = rng.uniform(-1, 1, n)
             z = np.empty(n)
             amg.amg_level_precond(h, l, 2, r, z)
             ref = hier.precond(r, nu=2, level=l)
-            assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref), f"B_{l}(r)"
+            H.assert_close(z, ref, 1e-10, f"B_{l}(r)")
         nL = hier.level_info(hier.nlev - 1)["n"]
         r = rng.uniform(-1, 1, nL)
         e = np.empty(nL)
         amg.amg_coarse_solve(h, r, e)
         ref = hier.coarse_solve(r)
-        assert np.linalg.norm(e - ref) <= 1e-10 * np.linalg.norm(ref)
+        H.assert_close(e, ref, 1e-10)
     finally:
         amg.amg_free(h)
 
@@ -171,7 +173,7 @@ def test_full_solve_parity(amg, gen_mod, oracle_mod, name):
             info = amg.amg_get_info(h)
             assert st == 0 and rr <= 1e-8 and info["last_true_relres"] <= 2e-8
             assert abs(it - ref["iters"]) <= 1, (it, ref["iters"])
-            assert np.linalg.norm(x - ref["x"]) <= 1e-6 * np.linalg.norm(ref["x"])
+            H.assert_close(x, ref["x"], 1e-6)
         # determinism: a second solve is bitwise identical (T6)
         x1 = np.zeros(p.n)
         x2 = np.zeros(p.n)
@@ -268,7 +270,7 @@ def test_full_size_hierarchy_and_precond(amg, gen_mod, oracle_mod, name):
         z = np.empty(p.n)
         amg.amg_level_precond(h, 0, 2, r, z)
         ref = hier.precond(r, nu=2)
-        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        H.assert_close(z, ref, 1e-10)
         b = gen_mod.rhs(p.n, 0)
         x = np.zeros(p.n)
         st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
@@ -296,7 +298,7 @@ def test_coarse_tail_kernel_parity(amg, gen_mod, oracle_mod, tail_nnz):
             z = np.empty(n)
             amg.amg_level_precond(h, l, 2, r, z)
             ref = hier.precond(r, nu=2, level=l)
-            assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref), f"B_{l}(r), tail_nnz={tail_nnz}"
+            H.assert_close(z, ref, 1e-10, f"B_{l}(r), tail_nnz={tail_nnz}")
         b = gen_mod.rhs(p.n, 0)
         ref = hier.solve(b, tol=1e-8, nu=2)
         x = np.zeros(p.n)
@@ -326,12 +328,12 @@ def test_smoother_tma_path_parity(amg, gen_mod, oracle_mod):
         x = np.empty(n)
         amg.amg_level_smooth(h, 0, f, x0, x)
         ref = hier.smooth(0, f, x0)
-        assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+        H.assert_close(x, ref, 1e-12)
         r = rng.uniform(-1, 1, n)
         z = np.empty(n)
         amg.amg_level_precond(h, 0, 2, r, z)
         zr = hier.precond(r, nu=2, level=0)
-        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+        H.assert_close(z, zr, 1e-10)
     finally:
         amg.amg_free(h)
 
@@ -350,7 +352,7 @@ def test_tail_shared_memory_mode_parity(amg, gen_mod, oracle_mod, tail_nnz, mode
         z = np.empty(p.n)
         amg.amg_level_precond(h, 0, 2, r, z)
         ref = hier.precond(r, nu=2, level=0)
-        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        H.assert_close(z, ref, 1e-10)
         b = gen_mod.rhs(p.n, 0)
         x = np.zeros(p.n)
         st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
@@ -383,15 +385,15 @@ def test_amli_cycle_parity(amg, gen_mod, oracle_mod, name):
             z = np.empty(n)
             amg.amg_level_precond(h, l, 2, r, z)
             ref = hier.precond(r, nu=2, level=l)
-            assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref), f"AMLI B_{l}(r)"
+            H.assert_close(z, ref, 1e-10, f"AMLI B_{l}(r)")
         r = rng.uniform(-1, 1, p.n)
         z3 = np.empty(p.n)
         amg.amg_level_precond(h, 0, 3, r, z3)
         ref3 = hier.precond(r, nu=3, level=0)
-        assert np.linalg.norm(z3 - ref3) <= 1e-10 * np.linalg.norm(ref3), "AMLI nu=3"
+        H.assert_close(z3, ref3, 1e-10, "AMLI nu=3")
         z4 = np.empty(p.n)
         amg.amg_level_precond(h, 0, 3, 2.5 * r, z4)
-        assert np.linalg.norm(z4 - 2.5 * z3) <= 1e-12 * np.linalg.norm(z4)  # linear operator
+        H.assert_close(z4, 2.5 * z3, 1e-12, "linear operator")
         b = gen_mod.rhs(p.n, 0)
         x = np.zeros(p.n)
         st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
@@ -422,7 +424,7 @@ def test_lanczos_lambda_parity(amg, gen_mod, oracle_mod, name):
         z = np.empty(p.n)
         amg.amg_level_precond(h, 0, 2, r, z)
         ref = hier.precond(r, nu=2, level=0)
-        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        H.assert_close(z, ref, 1e-10)
         b = gen_mod.rhs(p.n, 0)
         x = np.zeros(p.n)
         st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
@@ -465,7 +467,7 @@ def test_structural_zeros_fe_pattern(amg, oracle_mod):
         z = np.empty(n)
         amg.amg_level_precond(h, 0, 2, r, z)
         ref = hier.precond(r, nu=2, level=0)
-        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        H.assert_close(z, ref, 1e-10)
     finally:
         amg.amg_free(h)
 
@@ -519,7 +521,7 @@ def test_mis_k_parity(amg, gen_mod, oracle_mod, case, k):
         z = np.empty(n)
         amg.amg_level_precond(h, 0, 2, r, z)
         ref = hier.precond(r, nu=2, level=0)
-        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        H.assert_close(z, ref, 1e-10)
         b = gen_mod.rhs(n, 0)
         if d is None or not np.any(d):
             b = b - b.mean()
@@ -559,13 +561,13 @@ def test_smoother_tma_wide_slices_parity(amg, gen_mod, oracle_mod):
         x = np.empty(n)
         amg.amg_level_smooth(h, 0, f, x0, x)
         ref = hier.smooth(0, f, x0)
-        assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+        H.assert_close(x, ref, 1e-12)
         r = rng.uniform(-1, 1, n)
         r -= r.mean()
         z = np.empty(n)
         amg.amg_level_precond(h, 0, 2, r, z)
         zr = hier.precond(r, nu=2, level=0)
-        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+        H.assert_close(z, zr, 1e-10)
     finally:
         amg.amg_free(h)
 
@@ -583,7 +585,7 @@ def test_kcycle_nu_regimes_parity(amg, gen_mod, oracle_mod, nu):
         z = np.empty(p.n)
         amg.amg_level_precond(h, 0, nu, r, z)
         ref = hier.precond(r, nu=nu, level=0)
-        assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+        H.assert_close(z, ref, 1e-10)
     finally:
         amg.amg_free(h)
 
@@ -625,6 +627,11 @@ def test_invalid_inputs_above_coarsest(amg, gen_mod, where):
     bad[p.rp[7]] = 0.5  # positive off-diagonal (row 7's first entry is off-diagonal)
     cases.append((p.rp, p.ci, bad, p.d))
     cases.append((p.rp, p.ci, p.val, -np.abs(p.d) - 1.0))  # d < 0
+    # non-monotone row_ptr: an interior entry far past rp[n], a negative one, a decrease
+    for k, val in ((50, 10 ** 9), (50, -5), (51, int(p.rp[49]))):
+        rpx = p.rp.copy()
+        rpx[k] = val
+        cases.append((rpx, p.ci, p.val, p.d))
     for rp, ci_, v, d in cases:
         with pytest.raises(amg.AmgError) as e:
             run(rp, ci_, v, d)
@@ -657,12 +664,12 @@ def test_smoother_tma_wide_fp64_values_parity(amg, gen_mod, oracle_mod):
         x = np.empty(n)
         amg.amg_level_smooth(h, 0, f, x0, x)
         ref = hier.smooth(0, f, x0)
-        assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+        H.assert_close(x, ref, 1e-12)
         r = rng.uniform(-1, 1, n)
         z = np.empty(n)
         amg.amg_level_precond(h, 0, 2, r, z)
         zr = hier.precond(r, nu=2, level=0)
-        assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+        H.assert_close(z, zr, 1e-10)
     finally:
         amg.amg_free(h)
 
@@ -690,7 +697,14 @@ def test_full_size_configs_converge(amg, gen_mod, cfg, mis_k):
         assert st == 0 and rr <= prm["tol"]
         assert info["last_true_relres"] <= 2 * prm["tol"]
         if mis_k == 0:
-            assert it == {"C3": 33, "C4": 17, "C5": 78}[cfg]
+            g = json.load(open(os.path.join(GOLD, "oracle_iters.json")))[cfg]
+            assert abs(it - g["iters"]) <= 1, (it, g["iters"])
+            # the full-size solution against the oracle's (tools/oracle_golden.py, 4096 evenly spaced
+            # rows), element by element
+            idx = np.asarray(g["x_sample_idx"], np.int64)
+            xs = x[torch.from_numpy(idx).to(dev)].cpu().numpy()
+            H.assert_close(xs, np.asarray(g["x_sample"]), 1e-6, f"{cfg} solution samples")
+            assert abs(float(torch.linalg.norm(x)) - g["x_norm"]) <= 1e-6 * g["x_norm"]
     finally:
         amg.amg_free(h)
 
@@ -720,3 +734,22 @@ def test_full_size_c3_option_paths(amg, gen_mod, opts):
             assert it == 33
     finally:
         amg.amg_free(h)
+
+
+def test_zero_rhs_precond_is_zero(amg, gen_mod, oracle_mod):
+    """Reading A13: B_l(0) with nu = 2, 3 runs the inner FCG on rho = 0 (d = 0, d.q = 0):
+    every level returns exactly 0, no 0/0 -- the launch path and the coarse tail kernel."""
+    p = gen_mod.grid2d(64)
+    for tail in (0, 8192):
+        h = amg.amg_setup(p.rp, p.ci, p.val, p.d, 2, 3, amg.amg_options_default(coarsest_size=10, tail_nnz=tail))
+        try:
+            L = amg.amg_get_info(h)["levels"]
+            assert L >= 4
+            for l in range(L - 1):
+                n = amg.amg_level_sizes(h, l, 3)["n"]
+                for nu in (2, 3):
+                    z = np.full(n, np.nan)
+                    amg.amg_level_precond(h, l, nu, np.zeros(n), z)
+                    assert not np.any(z), (tail, l, nu)
+        finally:
+            amg.amg_free(h)
