@@ -58,7 +58,6 @@ struct Sell {          // SELL-32: 32-row slices, entries column-major inside a 
     // slices while the halo is in flight, then the boundary slices): sptr/nslices describe the
     // view's slices and srow0 is the absolute first row of its first slice (0 for the whole level)
     int srow0 = 0;
-    int maxoff = 0;        // max |col - row| over the stored entries (halo of the fused step pair)
     // lossless compressed streams (same slice layout), chosen per level at setup:
     int vmode = 0;         // 0: val (fp64); 1: vcode (uint8) into vdict (<= 256 distinct values)
     int cmode = 0;         // 0: col (int32); 1: ccode (uint8) into cdict of offsets col-row; 2: coff (int16 col-row);
@@ -111,7 +110,6 @@ double inf_norm(const Csr& A, cudaStream_t s);
 // true if some d_i != 0
 bool any_nonzero(int n, const double* d, cudaStream_t s);
 // max |col - row| over the stored entries (0 if only a diagonal)
-int max_col_offset(const Csr& A, cudaStream_t s);
 // Lanczos start vector of reading A24: out_i = 2 U(z ^ i) - 1, U(y) = (splitmix64(y) >> 11) 2^-53
 void launch_lanczos_start(int n, uint64_t z, double* out, cudaStream_t s);
 
@@ -167,9 +165,6 @@ void launch_smooth(const SpOp& op, const double* xg, double cg, const double* f,
 //  two consecutive general steps in one launch (x_{k+1} into out1, x_{k+2} into out2; out2 may alias xk,
 //  out1 may alias xkm1); flags [>= slices/8 + 1] and sync [3] are zero-initialised level scratch.
 //  Returns false (nothing launched) when the level is not eligible.
-bool fuse2_enabled();
-bool launch_smooth2(const SpOp& op, const double* xk, const double* xkm1, const double* f, double* out1, double* out2,
-                    double a1, double b1, double a2, double b2, int* flags, int* sync, cudaStream_t s);
 //  resid: out = f - A xg; optional dot r.r into dots[0]
 void launch_resid(const SpOp& op, const double* xg, const double* f, double* out, double* dot_rr,
                   const DotScratch& ds, cudaStream_t s);
@@ -214,6 +209,7 @@ void launch_dot(int n, const double* x, const double* y, double* out, const DotS
 // cluster barriers between dependent phases and cluster-wide (DSMEM) deterministic reductions.
 struct TLevel {
     int n = 0, nc = 0;
+    int ld = 0;  // slot stride of the inner-FCG D / Q arrays (global or shared)
     const int* rp = nullptr;
     const int* ci = nullptr;
     const double* v = nullptr;
@@ -247,20 +243,9 @@ constexpr int kTailMaxLev = 12;   // shared-memory mode: at most this many tail 
 constexpr int kTailSmemBytes = 200 * 1024;  // shared-memory mode budget for the tail vectors
 constexpr int kTailMaxNu = 4;  // the tail kernel supports nu <= 4
 // cluster size actually used (16 if the device allows non-portable clusters, else 8)
-int tail_cluster_size();
 void launch_tail(const TailArgs& a, cudaStream_t s);
 
-// ---------------------------------------------------------------- programmatic dependent launch
-// Every solve kernel is launched with programmatic stream serialization: it triggers its
-// dependents at entry (so the next kernel of the k-cycle is already resident) and waits for its
-// predecessor's completion + memory visibility (griddepcontrol.wait) before touching any data the
-// predecessor may have written.  Captured into the CUDA graphs as programmatic edges.
-#ifdef __CUDACC__
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-#endif
-bool pdl_enabled();
-int pdl_max_grid();
+// Kernel launch through cudaLaunchKernelEx (stream-ordered, capturable into the CUDA graphs).
 template <class... KArgs, class... Args>
 void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
     cudaLaunchConfig_t cfg{};
@@ -268,12 +253,7 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    const int mg = pdl_max_grid();
-    cfg.numAttrs = (pdl_enabled() && (mg == 0 || (int)(grid.x * grid.y * grid.z) <= mg)) ? 1 : 0;
+    cfg.numAttrs = 0;
     CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 

@@ -97,8 +97,6 @@ __global__ void k_rel_to_glob(int64_t m, const int* __restrict__ ci, int64_t gbe
 
 template <class T>
 __global__ void k_pack(int m, const int* __restrict__ sidx, const T* __restrict__ x, T* __restrict__ buf) {
-    pdl_trigger();
-    pdl_wait();
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) buf[k] = x[sidx[k]];
 }
 
@@ -139,8 +137,6 @@ struct ScalarPtrs {
 };
 // local partial = main (+ the boundary views' partials of a split pass, added in this fixed order)
 __global__ void k_ar_pack(ScalarPtrs sp, ScalarPtrs e1, ScalarPtrs e2, double* __restrict__ buf) {
-    pdl_trigger();
-    pdl_wait();
     for (int j = threadIdx.x; j < sp.k; j += blockDim.x) {
         double v = *sp.p[j];
         if (j < e1.k) v += *e1.p[j];
@@ -150,8 +146,6 @@ __global__ void k_ar_pack(ScalarPtrs sp, ScalarPtrs e1, ScalarPtrs e2, double* _
 }
 // rank-order sum of the gathered partials: identical bits on every rank
 __global__ void k_ar_sum(ScalarPtrs sp, const double* __restrict__ g, int P) {
-    pdl_trigger();
-    pdl_wait();
     for (int j = threadIdx.x; j < sp.k; j += blockDim.x) {
         double s = 0.0;
         for (int r = 0; r < P; ++r) s += g[(size_t)r * sp.k + j];

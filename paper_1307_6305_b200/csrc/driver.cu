@@ -601,18 +601,9 @@ void amg::finish_build(amg_hierarchy* h) {
         Lv.op.S = Lv.S;
         Lv.op.sell = Lv.S.sptr != nullptr;
         if (Lv.dist) build_split(h, k);
-        if (fuse2_enabled() && Lv.op.sell && !Lv.dist && k < h->L - 1) {  // fused step pairs (k_smooth2_tma) scratch
-            Lv.S.maxoff = Lv.op.S.maxoff = max_col_offset(Lv.A, s);
-            const size_t nf = (size_t)Lv.S.nslices / 8 + 2;
-            Lv.fflags = halloc<int>(h, nf);
-            Lv.fsync = halloc<int>(h, 4);
-            CK(cudaMemsetAsync(Lv.fflags, 0, sizeof(int) * nf, s));
-            CK(cudaMemsetAsync(Lv.fsync, 0, sizeof(int) * 4, s));
-            pt.mark("max offset", k);
-        }
         // vector layout [pad | lower halo | own | upper halo]
         Lv.lo_pad = (Lv.H.nlo + 3) & ~3;
-        Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : Lv.A.n;
+        Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : ((Lv.A.n + 3) & ~3);  // 32-byte aligned slots
     }
     pt.mark("formats");
     // level workspaces
@@ -660,7 +651,6 @@ void amg::finish_build(amg_hierarchy* h) {
         for (int k = std::max(1, h->g); k < h->L; ++k)
             if (h->lev[k].A.nnz <= h->opt.tail_nnz) { h->l_tail = k; break; }
     if (h->l_tail < h->L) {
-        tail_cluster_size();
         size_t cur = 0;
         CK(cudaDeviceGetLimit(&cur, cudaLimitStackSize));
         if (cur < 4096) CK(cudaDeviceSetLimit(cudaLimitStackSize, 4096));  // t_B/t_fcg recursion
@@ -688,6 +678,7 @@ static void upload_tail_levels(amg_hierarchy* h) {
         const Level& Lv = h->lev[k];
         TLevel& d = t[k];
         d.n = Lv.A.n;
+        d.ld = Lv.ld;
         d.nc = Lv.nc;
         d.rp = Lv.A.rp;
         d.ci = Lv.A.ci;
@@ -703,7 +694,7 @@ static void upload_tail_levels(amg_hierarchy* h) {
     // memory when they fit (nu inner slots), so each phase of the recursion costs L1/shared-memory
     // latencies instead of L2 round trips
     h->tail_smem = 0;
-    if (h->l_tail < h->L && h->opt.tail_smem && tail_cluster_size() == 1 && h->L - h->l_tail <= kTailMaxLev &&
+    if (h->l_tail < h->L && h->opt.tail_smem && h->L - h->l_tail <= kTailMaxLev &&
         h->nu_ws >= 1) {
         int64_t off = 0;
         auto take = [&](int64_t len) {
@@ -719,8 +710,8 @@ static void upload_tail_levels(amg_hierarchy* h) {
                 d.off[1] = take(n);
                 d.off[2] = take(n);
                 d.off[5] = take(n);
-                d.off[6] = take(n * h->nu_ws);
-                d.off[7] = take(n * h->nu_ws);
+                d.off[6] = take((int64_t)d.ld * h->nu_ws);
+                d.off[7] = take((int64_t)d.ld * h->nu_ws);
             }
             d.off[3] = take(n);
             d.off[4] = take(n);
@@ -776,8 +767,8 @@ static void upload_tail_levels(amg_hierarchy* h) {
             for (int k = h->l_tail; k < h->L - 1; ++k) {  // tier 4: inner FCG vectors
                 TLevel& d = t[k];
                 d.off[5] = place(d.n);
-                d.off[6] = place(d.n * h->nu_ws);
-                d.off[7] = place(d.n * h->nu_ws);
+                d.off[6] = place((int64_t)d.ld * h->nu_ws);
+                d.off[7] = place((int64_t)d.ld * h->nu_ws);
             }
             h->tail_smem = (int)off;
         }
@@ -950,9 +941,8 @@ static void amli_correction(amg_hierarchy* h, int l, int nu) {
 }
 
 // A chain of general smoothing steps x_out = a x_g + (1 - a) x_prev + b (f - A x_g) on level l, each the
-// next one's x_prev / x_g.  Consecutive pairs are fused into one launch (k_smooth2_tma: the matrix
-// and f stream from HBM once per pair) on a non-partitioned level when eligible.  When `prof`, the
-// algorithmic bytes and launches are added to the live-profile window counters.
+// next one's x_prev / x_g, one launch per step.  When `prof`, the algorithmic bytes and launches are
+// added to the live-profile window counters.
 struct SmStep {
     const double* xg;
     const double* xprev;
@@ -960,35 +950,15 @@ struct SmStep {
     double* out;
 };
 static int64_t smoother_bytes(const Level& Lv);
-static int64_t pair_bytes(const Level& Lv) {  // fused pair: codes once, x_k, x_{k-1}, f read, 2 writes
-    const int64_t n = Lv.A.n;
-    return smoother_bytes(Lv) - 32 * n + 40 * n;
-}
 static void run_steps(amg_hierarchy* h, int l, const double* f, const std::vector<SmStep>& st, bool prof) {
-    Level& Lv = h->lev[l];
-    for (size_t q = 0; q < st.size();) {
-        const SmStep& s1 = st[q];
-        if (q + 1 < st.size() && !Lv.dist && Lv.fflags) {
-            const SmStep& s2 = st[q + 1];
-            if (s2.xg == s1.out && s2.xprev == s1.xg &&
-                launch_smooth2(Lv.op, s1.xg, s1.xprev, f, s1.out, s2.out, s1.a, s1.b, s2.a, s2.b, Lv.fflags, Lv.fsync,
-                               h->s)) {
-                if (prof) {
-                    h->prof_win_bytes += pair_bytes(Lv);
-                    h->prof_win_launches += 1;
-                }
-                q += 2;
-                continue;
-            }
-        }
+    for (const SmStep& s1 : st) {
         spmv_pass(h, l, const_cast<double*>(s1.xg), [&](const SpOp& op, int) {
             launch_smooth(op, s1.xg, 1.0, f, s1.xprev, 0.0, s1.a, s1.b, s1.out, h->s);
         });
         if (prof) {
-            h->prof_win_bytes += smoother_bytes(Lv);
+            h->prof_win_bytes += smoother_bytes(h->lev[l]);
             h->prof_win_launches += 1;
         }
-        ++q;
     }
 }
 

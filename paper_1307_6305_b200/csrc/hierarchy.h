@@ -61,8 +61,6 @@ struct Level {
     // is in flight; the boundary slices (the ranges around it) after it has arrived
     bool split = false;
     SpOp op_int, op_lo, op_hi;   // slice views: interior, boundary before it, boundary after it
-    int* fflags = nullptr;       // fused step-pair scratch (k_smooth2_tma): per-chunk epochs, sync words
-    int* fsync = nullptr;
     int ld = 0;                  // vector slot stride (lo_pad + n + nhi, rounded up to 4)
 };
 

@@ -284,25 +284,6 @@ void launch_lanczos_start(int n, uint64_t z, double* out, cudaStream_t s) {
     CK(cudaGetLastError());
 }
 
-__global__ void k_max_off(int n, const int* __restrict__ rp, const int* __restrict__ ci, int* out) {
-    int m = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        for (int p = rp[i]; p < rp[i + 1]; ++p) m = max(m, abs(ci[p] - i));
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
-}
-
-int max_col_offset(const Csr& A, cudaStream_t s) {
-    int* o = dalloc<int>(1, s);
-    CK(cudaMemsetAsync(o, 0, sizeof(int), s));
-    k_max_off<<<grid_red(A.n), kBlock, 0, s>>>(A.n, A.rp, A.ci, o);
-    ++g_launches;
-    CK(cudaGetLastError());
-    const int r = read_scalar(o, s);
-    dfree(o, s);
-    return r;
-}
-
 // ------------------------------------------------------------------ lambda_1 (a1)
 __global__ void k_rowabs_max(int n, const int* __restrict__ rp, const double* __restrict__ v,
                              unsigned long long* out) {
