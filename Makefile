@@ -6,7 +6,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 LIB := paper_1307_6305_b200/lib/libamg_b200.so
-SRCS := paper_1307_6305_b200/csrc/driver.cu paper_1307_6305_b200/csrc/k_solve.cu paper_1307_6305_b200/csrc/k_setup.cu paper_1307_6305_b200/csrc/k_tail.cu paper_1307_6305_b200/csrc/comm.cu paper_1307_6305_b200/csrc/dist.cu
+SRCS := paper_1307_6305_b200/csrc/driver.cu paper_1307_6305_b200/csrc/k_solve.cu paper_1307_6305_b200/csrc/k_dense.cu paper_1307_6305_b200/csrc/k_setup.cu paper_1307_6305_b200/csrc/k_tail.cu paper_1307_6305_b200/csrc/comm.cu paper_1307_6305_b200/csrc/dist.cu
 OBJS := $(patsubst paper_1307_6305_b200/csrc/%.cu,build/%.o,$(SRCS))
 HDRS := paper_1307_6305_b200/csrc/amg_internal.h paper_1307_6305_b200/csrc/hierarchy.h include/amg.h
 

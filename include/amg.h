@@ -94,7 +94,11 @@ typedef struct {
                                8(f) item 2): each level is aggregated once by the MIS of
                                the graph of A^k grown into neighbourhood aggregates, p is ignored; k <= 8,
                                amg_setup only */
-    int64_t  reserved[1];
+    int32_t  dense_b_rows;  /* the k-cycle operator B_{L-2} of the level above the coarsest is linear (exact
+                               coarse solve, reading A12): when n_{L-2} <= dense_b_rows (and the level is
+                               not row-partitioned) it is formed once at setup as a dense n x n matrix and
+                               each application is one GEMV; 0 disables; default 4096 */
+    int32_t  reserved0;
 } amg_options;
 
 typedef struct {

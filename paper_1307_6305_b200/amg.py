@@ -30,7 +30,7 @@ class amg_options(ctypes.Structure):
                 ("use_graphs", ctypes.c_int32), ("compress", ctypes.c_int32), ("tail_nnz", ctypes.c_int64),
                 ("gather_rows", ctypes.c_int64), ("tail_smem", ctypes.c_int32), ("cycle", ctypes.c_int32),
                 ("amli_kappa", ctypes.c_double), ("lanczos_steps", ctypes.c_int32), ("mis_k", ctypes.c_int32),
-                ("reserved", ctypes.c_int64 * 1)]
+                ("dense_b_rows", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 class amg_info(ctypes.Structure):

@@ -151,6 +151,9 @@ void compress_sell(Sell& S, const Csr& A, cudaStream_t s);
 void free_sell(Sell& S, cudaStream_t s);
 // dense (pseudo-)inverse of the coarsest operator, row-major n x n
 double* coarse_inverse(const Csr& A, bool singular, double shift, cudaStream_t s);
+// dense B_l (n_l x n_l, row-major) of the level above the coarsest (k_dense.cu)
+void dense_level_operator(const Csr& A, int m, const double* alpha, const double* beta, int nc, const int* agg,
+                          const int* perm, const int* aptr, const double* Minv, double* Bd, cudaStream_t s);
 void free_csr(Csr& A, cudaStream_t s);
 
 // ---------------------------------------------------------------- solve launchers (k_solve.cu)
@@ -181,6 +184,7 @@ void launch_resid_restrict(int nc, const int* aptr, const int* perm, const Csr& 
                            double* rho, cudaStream_t s);
 void launch_gemv_prolong(int nf, const int* agg, int cb, int nL, const double* M, const double* r, double* x,
                          cudaStream_t s);
+void launch_gemv_dense(int n, const double* M, const double* r, double* e, cudaStream_t s);
 void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_t s);
 // c[j] = z . Q_j for j < w  (Q_j = Q[j], pointers in a device array)
 void launch_multidot(int n, const double* z, const double* const* Q, int w, double* c, const DotScratch& ds,
@@ -235,13 +239,16 @@ struct TailArgs {
     int smem = 0;     // doubles of dynamic shared memory holding the tail levels' vectors (0 = global)
     int lbase = 0;    // lev[k] describes level lbase + k
     const double* Minv = nullptr;
+    const double* Bd = nullptr;   // dense B of level dense_l (k_dense.cu), or null
+    int dense_l = -1;
     const double* rin = nullptr;
     double* out = nullptr;
     const TLevel* lev = nullptr;  // device array
 };
 constexpr int kTailMaxLev = 12;   // shared-memory mode: at most this many tail levels
 constexpr int kTailSmemBytes = 200 * 1024;  // shared-memory mode budget for the tail vectors
-constexpr int kTailMaxNu = 4;  // the tail kernel supports nu <= 4
+constexpr int kTailMaxNu = 4;
+constexpr int64_t kTailDenseEntries = 100000;  // dense B_{L-2} inside the tail only up to this many entries  // the tail kernel supports nu <= 4
 // cluster size actually used (16 if the device allows non-portable clusters, else 8)
 void launch_tail(const TailArgs& a, cudaStream_t s);
 

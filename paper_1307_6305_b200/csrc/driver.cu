@@ -666,6 +666,22 @@ void amg::finish_build(amg_hierarchy* h) {
             poly_coeffs(Lv.lambda1, Lv.kappa, h->m, Lv.alpha, Lv.beta);
         }
     }
+    // the level above the coarsest: B_{L-2} is linear (exact coarse solve, reading A12); formed
+    // densely on small replicated levels and applied as one GEMV per visit (k_dense.cu)
+    // Inside the one-CTA coarse tail a GEMV streams all n^2 entries through one SM, so there it is
+    // formed only when small (C4's 267 rows: faster; C5's 591: slower than the sparse phases).
+    h->dense_l = -1;
+    if (h->L >= 2 && h->opt.dense_b_rows > 0) {
+        Level& Lv = h->lev[h->L - 2];
+        const bool in_tail = h->L - 2 >= h->l_tail;
+        if (!Lv.dist && Lv.A.n <= h->opt.dense_b_rows &&
+            (!in_tail || (int64_t)Lv.A.n * Lv.A.n <= kTailDenseEntries)) {
+            h->Bd = halloc<double>(h, (size_t)Lv.A.n * Lv.A.n);
+            dense_level_operator(Lv.A, h->m, Lv.alpha, Lv.beta, Lv.nc, Lv.agg, Lv.perm, Lv.aptr, h->Minv, h->Bd, s);
+            h->dense_l = h->L - 2;
+            pt.mark("dense B", h->L - 2);
+        }
+    }
     CK(cudaStreamSynchronize(s));
     pt.mark("workspaces");
 }
@@ -805,6 +821,8 @@ static void tail_call(amg_hierarchy* h, int mode, int l, int nu, const double* r
     a.nu = nu;
     a.mode = mode;
     a.Minv = h->Minv;
+    a.Bd = h->Bd;
+    a.dense_l = h->dense_l;
     a.rin = rin;
     a.out = out;
     a.lev = h->d_tlev;
@@ -969,6 +987,10 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     cudaStream_t s = h->s;
     if (l == h->L - 1) {
         launch_gemv(h->lev[l].A.n, h->Minv, rin, out, s);
+        return;
+    }
+    if (l == h->dense_l) {  // the linear B_{L-2} as one dense GEMV (k_dense.cu)
+        launch_gemv_dense(h->lev[l].A.n, h->Bd, rin, out, s);
         return;
     }
     if (use_tail(h, l, nu)) {
@@ -1249,6 +1271,7 @@ int amg_options_default(amg_options* o) {
     o->stream = nullptr;
     o->use_graphs = 1;
     o->tail_nnz = 8192;
+    o->dense_b_rows = 4096;
     o->tail_smem = 2;  // greedy placement, matrices first: C4 -5%, C1/C2 -2%, C3/C5 neutral
     o->compress = 1;
     o->gather_rows = 50000;

@@ -75,6 +75,8 @@ struct amg_hierarchy {
     amg_options opt{};
     amg::Level lev[amg::kMaxLevels];
     double* Minv = nullptr;
+    double* Bd = nullptr;   // dense B_{L-2} (k_dense.cu) when n_{L-2} <= opt.dense_b_rows
+    int dense_l = -1;       // its level (-1: none)
     // outer FCG (level 0 own rows)
     int n = 0, W = 5;
     double *b = nullptr, *x = nullptr, *r = nullptr, *Z = nullptr, *D = nullptr, *Q = nullptr;

@@ -29,11 +29,13 @@ void init_device_props() {
 
 int vector_grid() { return g_num_sms * 4; }
 
-// grid of a grid-stride vector kernel over n elements: >= 8 elements per thread, at most 8 CTAs of
-// 256 threads per SM (the full 2048 threads: measured on the C3 level-0 vectors, tools/vec_micro.cu,
-// 4 CTAs/SM left too few loads in flight -- fcg_update 160 -> 125 us, multidot(4) 219 -> 97 us)
+// grid of a grid-stride vector kernel over n work units (elements, double2 pairs, int4 quads, or
+// aggregates): one unit per thread while that fits in 8 CTAs of 256 threads per SM, grid-stride
+// beyond.  Small (coarse-level) vectors are latency-bound: spreading them over every SM is what
+// helps; large ones want the full 2048 threads per SM in flight (tools/vec_micro.cu: 4 CTAs/SM left
+// too few loads in flight on C3's level 0 -- fcg_update 160 -> 125 us, multidot(4) 219 -> 97 us).
 static int vgrid(int64_t n) {
-    int64_t g = (n + 8 * kBlock - 1) / (8 * kBlock);
+    int64_t g = (n + kBlock - 1) / kBlock;
     if (g > 2 * vector_grid()) g = 2 * vector_grid();
     return g < 1 ? 1 : (int)g;
 }
@@ -1116,6 +1118,47 @@ void launch_gemv(int n, const double* M, const double* r, double* e, cudaStream_
     ++g_launches;
 }
 
+// Dense B_{L-2} r (k_dense.cu): one CTA per row, each thread a strided share of the columns with
+// four independent loads in flight, then a fixed-order block sum (deterministic).  A warp per row
+// (k_gemv) kept too few loads in flight for the 1328^2 (C3) .. 2316^2 (C2) matrices: 15 us cold.
+template <int T>
+__global__ void __launch_bounds__(T) k_gemv_rows(int n, const double* __restrict__ M, const double* __restrict__ r,
+                                                 double* __restrict__ e) {
+    __shared__ double red[T / 32];
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const double* row = M + (size_t)i * n;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int j = threadIdx.x;
+        for (; j + 3 * T < n; j += 4 * T) {
+            const double a0 = __ldg(row + j), a1 = __ldg(row + j + T), a2 = __ldg(row + j + 2 * T),
+                         a3 = __ldg(row + j + 3 * T);
+            s0 = fma(a0, __ldg(r + j), s0);
+            s1 = fma(a1, __ldg(r + j + T), s1);
+            s2 = fma(a2, __ldg(r + j + 2 * T), s2);
+            s3 = fma(a3, __ldg(r + j + 3 * T), s3);
+        }
+        for (; j < n; j += T) s0 = fma(__ldg(row + j), __ldg(r + j), s0);
+        double v = warp_sum((s0 + s1) + (s2 + s3));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double t = threadIdx.x < T / 32 ? red[threadIdx.x] : 0.0;
+            t = warp_sum(t);
+            if (threadIdx.x == 0) e[i] = t;
+        }
+        __syncthreads();
+    }
+}
+
+void launch_gemv_dense(int n, const double* M, const double* r, double* e, cudaStream_t s) {
+    const int grid = n < 148 * 8 ? n : 148 * 8;
+    if (n >= 1024) launch_k(k_gemv_rows<256>, dim3(grid), dim3(256), 0, s, n, M, r, e);
+    else if (n >= 256) launch_k(k_gemv_rows<128>, dim3(grid), dim3(128), 0, s, n, M, r, e);
+    else launch_k(k_gemv_rows<64>, dim3(grid), dim3(64), 0, s, n, M, r, e);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
 // Residual fused with the restriction on the small (L2-resident, launch-latency-bound) levels: one
 // warp per aggregate, lane = member (chunks of 32): each lane forms its row's residual f_i - (A x)_i
 // with the fma chain in CSR order (the SELL kernels' order: the same r_i), then every lane sums the
@@ -1278,8 +1321,8 @@ void launch_multidot(int n, const double* z, const double* const* Q, int w, doub
                      cudaStream_t s) {
     PtrArr a{};
     for (int j = 0; j < w; ++j) a.p[j] = Q[j];
-    const dim3 g(vgrid(n)), b(kBlock);
     const bool v = al16(z) && all_al16(Q, w);
+    const dim3 g(vgrid(v && w <= 4 ? (n + 1) / 2 : n)), b(kBlock);
     switch (v ? w : 0) {
         case 1: launch_k(k_multidot<1, true>, g, b, 0, s, n, z, a, w, ds.partials, ds.ticket, c); break;
         case 2: launch_k(k_multidot<2, true>, g, b, 0, s, n, z, a, w, ds.partials, ds.ticket, c); break;
@@ -1351,8 +1394,8 @@ void launch_direction(int n, const double* z, const double* const* D, const doub
                       double* d, cudaStream_t s) {
     PtrArr a{};
     for (int j = 0; j < w; ++j) a.p[j] = D[j];
-    const dim3 g(vgrid(n)), b(kBlock);
     const bool v = al16(z) && al16(d) && all_al16(D, w);
+    const dim3 g(vgrid(v && w <= 4 ? (n + 1) / 2 : n)), b(kBlock);
     switch (v ? w : 0) {
         case 1: launch_k(k_direction<1, true>, g, b, 0, s, n, z, a, c, dq, w, d); break;
         case 2: launch_k(k_direction<2, true>, g, b, 0, s, n, z, a, c, dq, w, d); break;
@@ -1438,8 +1481,9 @@ static void fcg_update_v(dim3 g, dim3 b, cudaStream_t s, int n, const double* dr
 
 void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
                        bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s) {
-    const dim3 g(vgrid(n)), b(kBlock);
-    if (al16(d) && al16(x) && (!r || (al16(r) && al16(q))))
+    const bool v = al16(d) && al16(x) && (!r || (al16(r) && al16(q)));
+    const dim3 g(vgrid(v ? (n + 1) / 2 : n)), b(kBlock);
+    if (v)
         fcg_update_v<true>(g, b, s, n, dr, dq, d, q, x, assign_x, r, rr, breakdown, ds);
     else
         fcg_update_v<false>(g, b, s, n, dr, dq, d, q, x, assign_x, r, rr, breakdown, ds);
@@ -1472,7 +1516,7 @@ __global__ void __launch_bounds__(kBlock) k_dot(int n, const double* __restrict_
 }
 
 void launch_dot(int n, const double* x, const double* y, double* out, const DotScratch& ds, cudaStream_t s) {
-    if (al16(x) && (!y || al16(y))) launch_k(k_dot<true>, dim3(vgrid(n)), dim3(kBlock), 0, s, n, x, y, ds.partials, ds.ticket, out);
+    if (al16(x) && (!y || al16(y))) launch_k(k_dot<true>, dim3(vgrid((n + 1) / 2)), dim3(kBlock), 0, s, n, x, y, ds.partials, ds.ticket, out);
     else launch_k(k_dot<false>, dim3(vgrid(n)), dim3(kBlock), 0, s, n, x, y, ds.partials, ds.ticket, out);
     CK(cudaGetLastError());
     ++g_launches;

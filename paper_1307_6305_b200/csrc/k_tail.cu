@@ -94,6 +94,10 @@ __device__ __noinline__ void t_B(const TailArgs& A, int l, const double* r, doub
         t_gemv(A.lev[l - A.lbase].n, A.Minv, r, out, c);
         return;
     }
+    if (l == A.dense_l && A.Bd) {  // the linear B_{L-2} as its dense matrix (k_dense.cu)
+        t_gemv(A.lev[l - A.lbase].n, A.Bd, r, out, c);
+        return;
+    }
     const TLevel& L = A.lev[l - A.lbase];
     const int m = A.m;
     double* cur = L.X;
