@@ -76,6 +76,7 @@ struct SpOp {          // the operator of one level as the SpMV-class kernels se
     Tiles T;
     Sell S;
     bool sell = false;     // true: SELL-32 warp-per-slice kernel; false: CSR row-tile kernel
+    int vg = 0;            // > 0: vector-CSR kernel with vg lanes per row (wide-row coarse levels; k_vcsr)
 };
 
 bool tma_eligible(const SpOp& op);  // format/size part of the TMA-staged kernel's eligibility

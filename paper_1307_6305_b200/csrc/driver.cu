@@ -601,6 +601,20 @@ void amg::finish_build(amg_hierarchy* h) {
         Lv.op.S = Lv.S;
         Lv.op.sell = Lv.S.sptr != nullptr;
         if (Lv.dist) build_split(h, k);
+        // wide-row levels (generic SELL width) that the TMA kernel does not take, small enough for the
+        // fp64/int32 CSR to stay L2-resident (<= 6M entries): vector-CSR kernel with G lanes per row,
+        // G ~ mean row length / 5.  C4 levels 2-4 (18-21 entries per row): solve 94.3 -> 83.9 ms
+        // (3 entries per lane: 85.8, 8: 87.0); on C4's level 1 (24.7M entries) the CSR lost to the
+        // compressed SELL, with fp64 values (121.7 ms) and with 1-byte value codes (100.5 ms).
+        if (k < h->L - 1 && !Lv.dist && Lv.op.sell && Lv.S.wmax > 16 && !tma_eligible(Lv.op)) {
+            static const double min_avg = getenv("AMG_VCSR_MIN_AVG") ? atof(getenv("AMG_VCSR_MIN_AVG")) : 12.0;
+            const double avg = (double)Lv.A.nnz / std::max(1, Lv.A.n);
+            if (min_avg > 0.0 && avg >= min_avg && Lv.A.nnz <= 6000000) {
+                int g = 4;
+                while (g < 32 && 5.0 * g < avg) g <<= 1;
+                Lv.op.vg = g;
+            }
+        }
         // vector layout [pad | lower halo | own | upper halo]
         Lv.lo_pad = (Lv.H.nlo + 3) & ~3;
         Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : ((Lv.A.n + 3) & ~3);  // 32-byte aligned slots
@@ -650,6 +664,11 @@ void amg::finish_build(amg_hierarchy* h) {
     if (h->opt.tail_nnz > 0)
         for (int k = std::max(1, h->g); k < h->L; ++k)
             if (h->lev[k].A.nnz <= h->opt.tail_nnz) { h->l_tail = k; break; }
+    // When the tail would only hold the level above the coarsest (and the coarsest), the dense B_{L-2}
+    // applied by full-GPU launches is faster than the one-CTA tail (C4 99.8 -> 94.2 ms, C5 203 -> 190 ms)
+    if (h->l_tail >= h->L - 2 && h->L >= 2 && h->opt.dense_b_rows > 0 && !h->lev[h->L - 2].dist &&
+        h->lev[h->L - 2].A.n <= h->opt.dense_b_rows)
+        h->l_tail = h->L;
     if (h->l_tail < h->L) {
         size_t cur = 0;
         CK(cudaDeviceGetLimit(&cur, cudaLimitStackSize));

@@ -879,12 +879,68 @@ static void launch_sell(const SpOp& op, const double* xg, const Epi& epi, double
     else launch_sell_w<Epi, DOTS, VM, CM, 0>(op, xg, epi, part, tk, dot_out, s);
 }
 
+// ------------------------------------------------------------------ vector-CSR kernel
+// The wide-row coarse levels (3D Galerkin levels: 18-21 entries per row, slices up to 38 wide) are
+// latency-bound in the SELL kernel, whose lane-per-row chain walks a wide slice in dependent 8-entry
+// chunks.  Here G lanes share a row of the CSR: the row's entries are read contiguously (coalesced),
+// all gathers of the row are in flight at once, and the G partial sums are combined by a fixed
+// shuffle tree (deterministic; a different summation order than the CSR chain, within the parity
+// tolerance).  The loop over rows is warp-uniform so every lane takes part in the shuffles.
+template <class Epi, bool DOTS, int G>
+__global__ void __launch_bounds__(kBlock) k_vcsr(Csr A, const double* __restrict__ xg, Epi epi, double* partials,
+                                                 unsigned* ticket, DotOut dot_out) {
+    double acc[Epi::ND > 0 ? Epi::ND : 1];
+#pragma unroll
+    for (int k = 0; k < (Epi::ND > 0 ? Epi::ND : 1); ++k) acc[k] = 0.0;
+    constexpr int RPW = 32 / G;  // rows per warp
+    const int lane = threadIdx.x & 31, sub = lane % G, grp = lane / G;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int* __restrict__ rp = A.rp;
+    const int* __restrict__ ci = A.ci;
+    const double* __restrict__ va = A.v;
+    for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW; r0 < A.n; r0 += nwarps * RPW) {
+        const int i = r0 + grp;
+        const bool act = i < A.n;
+        typename Epi::Pre pre{};
+        double xi = 0.0, s = 0.0;
+        if (act) {
+            if (sub == 0) {
+                pre = epi.load(i);
+                xi = ld_gather(xg + i);
+            }
+            const int p1 = rp[i + 1];
+            for (int p = rp[i] + sub; p < p1; p += G) s = fma(va[p], ld_gather(xg + ci[p]), s);
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+        if (act && sub == 0) epi.store(i, s, xi, pre, acc);
+    }
+    if constexpr (DOTS) finalize_dots<Epi::ND>(acc, partials, ticket, dot_out);
+}
+
+template <class Epi, bool DOTS>
+static void launch_vcsr(const SpOp& op, const double* xg, const Epi& epi, double* part, unsigned* tk, DotOut dot_out,
+                        cudaStream_t s) {
+    const int64_t threads = (int64_t)op.A.n * op.vg;
+    int g = (int)std::min<int64_t>((threads + kBlock - 1) / kBlock, 148 * 8);
+    if constexpr (DOTS) g = std::min(g, 4096);
+    if (g < 1) g = 1;
+    switch (op.vg) {
+        case 4: launch_k(k_vcsr<Epi, DOTS, 4>, dim3(g), dim3(kBlock), 0, s, op.A, xg, epi, part, tk, dot_out); break;
+        case 8: launch_k(k_vcsr<Epi, DOTS, 8>, dim3(g), dim3(kBlock), 0, s, op.A, xg, epi, part, tk, dot_out); break;
+        case 16: launch_k(k_vcsr<Epi, DOTS, 16>, dim3(g), dim3(kBlock), 0, s, op.A, xg, epi, part, tk, dot_out); break;
+        default: launch_k(k_vcsr<Epi, DOTS, 32>, dim3(g), dim3(kBlock), 0, s, op.A, xg, epi, part, tk, dot_out); break;
+    }
+}
+
 template <class Epi, bool DOTS>
 static void launch_op(const SpOp& op, const double* xg, const Epi& epi, const DotScratch* ds, DotOut dot_out,
                       cudaStream_t s) {
     double* part = ds ? ds->partials : nullptr;
     unsigned* tk = ds ? ds->ticket : nullptr;
-    if (op.sell) {
+    if (op.vg > 0) {
+        launch_vcsr<Epi, DOTS>(op, xg, epi, part, tk, dot_out, s);
+    } else if (op.sell) {
         const int fmt = op.S.vmode * 4 + op.S.cmode;
         switch (fmt) {
             case 0: launch_sell<Epi, DOTS, 0, 0>(op, xg, epi, part, tk, dot_out, s); break;
@@ -988,7 +1044,7 @@ bool tma_eligible(const SpOp& op) {
     static int max_w = -1;  // AMG_TMA_MAX_W (experiments)
     if (max_w < 0) max_w = getenv("AMG_TMA_MAX_W") ? atoi(getenv("AMG_TMA_MAX_W")) : 32;
     const int wcap = tma_wide_fmt(op.S.vmode, op.S.cmode) ? 32 : 16;  // W = 32 instances: wide formats only
-    return tma_enabled() && op.sell && op.S.wmax <= std::min(max_w, wcap) && op.S.nslices >= min_slices;
+    return tma_enabled() && op.sell && op.vg == 0 && op.S.wmax <= std::min(max_w, wcap) && op.S.nslices >= min_slices;
 }
 
 template <class Epi, bool DOTS>
