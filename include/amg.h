@@ -98,7 +98,11 @@ typedef struct {
                                coarse solve, reading A12): when n_{L-2} <= dense_b_rows (and the level is
                                not row-partitioned) it is formed once at setup as a dense n x n matrix and
                                each application is one GEMV; 0 disables; default 4096 */
-    int32_t  reserved0;
+    int32_t  global_agg;    /* amg_setup_dist only: 0 = decoupled aggregation (reading A20: the matching passes
+                               of a row-partitioned level see the edges inside each block; default); 1 = global
+                               aggregation: the passes see every edge, matching by halo
+                               rounds across the blocks, aggregates owned by their leader's rank -- the
+                               single-GPU hierarchy for any number of ranks */
 } amg_options;
 
 typedef struct {

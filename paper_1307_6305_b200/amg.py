@@ -30,7 +30,7 @@ class amg_options(ctypes.Structure):
                 ("use_graphs", ctypes.c_int32), ("compress", ctypes.c_int32), ("tail_nnz", ctypes.c_int64),
                 ("gather_rows", ctypes.c_int64), ("tail_smem", ctypes.c_int32), ("cycle", ctypes.c_int32),
                 ("amli_kappa", ctypes.c_double), ("lanczos_steps", ctypes.c_int32), ("mis_k", ctypes.c_int32),
-                ("dense_b_rows", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("dense_b_rows", ctypes.c_int32), ("global_agg", ctypes.c_int32)]
 
 
 class amg_info(ctypes.Structure):
@@ -219,7 +219,8 @@ def amg_level_export(h, level: int, m: int, with_agg: bool = True):
     rp = np.empty(s["n"] + 1, np.int64)
     ci = np.empty(s["nnz"], np.int32)
     v = np.empty(s["nnz"], np.float64)
-    agg = np.empty(s["n"], np.int32) if (with_agg and s["nc"] > 0) else None
+    last = level == amg_get_info(h)["levels"] - 1
+    agg = np.empty(s["n"], np.int32) if (with_agg and not last) else None
     _check(load().amg_level_export(h, level, rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
                                    agg.ctypes.data if agg is not None else None), "amg_level_export")
     return rp, ci, v, agg

@@ -137,6 +137,14 @@ struct ThreadComm final : Comm {
         sh->cv.notify_all();
     }
     void sendrecv(const std::vector<P2P>& sends, const std::vector<P2P>& recvs, cudaStream_t s) override {
+        static const bool trace = getenv("AMG_COMM_TRACE") != nullptr;
+        if (trace) {
+            std::string m = "[comm] rank " + std::to_string(rank) + " sends";
+            for (const P2P& p : sends) m += " " + std::to_string(p.peer) + ":" + std::to_string(p.bytes);
+            m += " recvs";
+            for (const P2P& p : recvs) m += " " + std::to_string(p.peer) + ":" + std::to_string(p.bytes);
+            fprintf(stderr, "%s\n", m.c_str());
+        }
         try {
             {
                 std::lock_guard<std::mutex> lk(sh->mu);
@@ -151,7 +159,10 @@ struct ThreadComm final : Comm {
                 for (size_t j = 0; j < ps.size(); ++j)
                     if (ps[j].peer == rank && k-- == 0) { found = (int)j; break; }
                 if (found < 0 || ps[found].bytes != r.bytes)
-                    throw Error(AMG_E_NCCL, "thread communicator: unmatched or mis-sized message");
+                    throw Error(AMG_E_NCCL, "thread communicator: unmatched or mis-sized message (rank " +
+                                                std::to_string(rank) + " <- " + std::to_string(r.peer) + ": expected " +
+                                                std::to_string(r.bytes) + " bytes, posted " +
+                                                (found < 0 ? std::string("none") : std::to_string(ps[found].bytes)) + ")");
                 if (r.bytes) CK(cudaMemcpyAsync(r.ptr, ps[found].ptr, r.bytes, cudaMemcpyDeviceToDevice, s));
             }
             CK(cudaStreamSynchronize(s));

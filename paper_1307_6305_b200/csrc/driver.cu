@@ -1050,18 +1050,26 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
         launch_resid_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.A, cur, rin, C.RHO, s);
     } else {
         spmv_pass(h, l, cur, [&](const SpOp& op, int) { launch_resid(op, cur, rin, Lv.RES, nullptr, h->ds, s); });
-        launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO + cb, s);
+        if (Lv.gx) restrict_global(h, l, Lv.RES, C.RHO + cb);  // members on other ranks included
+        else launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO + cb, s);
     }
     if (gather) allgatherv_d(h, C.RHO, C.offs);
     // coarse correction (A12: exact solve when the next level is the coarsest)
+    // (global aggregation: agg holds global ids of a replicated coarse level, or coarse relative
+    // indices -- remote aggregates in the coarse halo -- of a row-partitioned one)
     if (l + 1 == h->L - 1) {  // exact coarsest solve fused with the prolongation
-        launch_gemv_prolong(Lv.A.n, Lv.agg, (int)cb, C.A.n, h->Minv, C.RHO, cur, s);
+        launch_gemv_prolong(Lv.A.n, Lv.agg, Lv.gx ? 0 : (int)cb, C.A.n, h->Minv, C.RHO, cur, s);
     } else {
         if (h->opt.cycle == 2)
             amli_correction(h, l + 1, nu);
         else
             fcg_inner(h, l + 1, nu);
-        launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
+        if (Lv.gx) {
+            if (C.dist) halo_exchange(h, l + 1, C.E);
+            launch_prolong(Lv.A.n, Lv.agg, C.E, cur, s);
+        } else {
+            launch_prolong(Lv.A.n, Lv.agg, C.E + cb, cur, s);
+        }
     }
     // post-smoothing S(r, x): x_{-1} = x_0 = cur
     double* other = (cur == Lv.X) ? Lv.XA : Lv.X;
@@ -1291,6 +1299,7 @@ int amg_options_default(amg_options* o) {
     o->use_graphs = 1;
     o->tail_nnz = 8192;
     o->dense_b_rows = 4096;
+    o->global_agg = 0;
     o->tail_smem = 2;  // greedy placement, matrices first: C4 -5%, C1/C2 -2%, C3/C5 neutral
     o->compress = 1;
     o->gather_rows = 50000;

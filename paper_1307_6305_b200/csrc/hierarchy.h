@@ -57,6 +57,14 @@ struct Level {
     std::vector<int64_t> offs;   // block offsets of all ranks (P+1): the partition this level's rows came in
     Halo H;
     int lo_pad = 0;              // own element offset inside a vector allocation (>= H.nlo, multiple of 4)
+    // global (non-decoupled) aggregation on a row-partitioned level (amg_options.global_agg, SURVEY
+    // 8(f) item 4): aggregates may span ranks and are owned by the rank of their leader
+    bool gx = false;
+    int* aggG = nullptr;         // own rows: global coarse id (export); agg holds the prolongation index
+    Halo XP;                     // restriction export plan: own rows of remote aggregates -> their owners
+    double* RB = nullptr;        // received fine residual values of remote members of own aggregates
+    int* perm_x = nullptr;       // own aggregates' members in increasing global row order: < n own row,
+    int* aptr_x = nullptr;       //   >= n: RB[perm - n]
     // halo overlap: the SELL slices that read no halo column (interior, one range) run while the halo
     // is in flight; the boundary slices (the ranges around it) after it has arrived
     bool split = false;
@@ -158,5 +166,8 @@ void warm_comm(amg_hierarchy* h);
 // export helpers for the parity hooks: relative columns -> global ids, own agg -> global coarse ids
 void export_dist_cols(amg_hierarchy* h, int l, int* out_dev);
 void export_dist_agg(amg_hierarchy* h, int l, int* out_dev);
+// global aggregation (Lv.gx): rH (own aggregates of level l+1) = P^T r over every member, the remote
+// members' values received through the export plan, summed in increasing global row order
+void restrict_global(amg_hierarchy* h, int l, const double* r, double* rH);
 
 }  // namespace amg

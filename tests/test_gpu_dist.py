@@ -61,14 +61,15 @@ def run_ranks(amg, P, fn):
 
 
 def dist_case(amg, p, P, gather_rows, oracle_mod, nu=2, check_solve=True, exact_values=True, cycle=0,
-              overlap=(True,), expect_path=None):
+              overlap=(True,), expect_path=None, global_agg=False):
     """GPU row-partitioned run(s) vs the oracle's nparts = P hierarchy; `overlap` lists the halo
     overlap settings to run (True: interior/boundary split, False: AMG_NO_OVERLAP=1); expect_path:
     required amg_info level0_path bits on every rank (1 = TMA interior kernel, 2 = split)."""
     import os
 
     res = None
-    hier = oracle_mod.setup_problem(p, nparts=P, gather_rows=gather_rows, cycle=cycle)
+    # global aggregation (SURVEY 8(f) item 4): the single-GPU rule, i.e. the oracle's nparts = 1
+    hier = oracle_mod.setup_problem(p, nparts=1 if global_agg else P, gather_rows=gather_rows, cycle=cycle)
     oref = None
     for ov in overlap:
         if ov:
@@ -76,7 +77,8 @@ def dist_case(amg, p, P, gather_rows, oracle_mod, nu=2, check_solve=True, exact_
         else:
             os.environ["AMG_NO_OVERLAP"] = "1"
         try:
-            res, oref = _dist_case(amg, p, P, gather_rows, hier, nu, check_solve, exact_values, cycle, oref)
+            res, oref = _dist_case(amg, p, P, gather_rows, hier, nu, check_solve, exact_values, cycle, oref,
+                                   global_agg)
         finally:
             os.environ.pop("AMG_NO_OVERLAP", None)
         if expect_path is not None:
@@ -86,7 +88,7 @@ def dist_case(amg, p, P, gather_rows, oracle_mod, nu=2, check_solve=True, exact_
     return res
 
 
-def _dist_case(amg, p, P, gather_rows, hier, nu, check_solve, exact_values, cycle, oref):
+def _dist_case(amg, p, P, gather_rows, hier, nu, check_solve, exact_values, cycle, oref, global_agg=False):
     from paper_1307_6305_b200 import dist
 
     prm = p.params
@@ -102,7 +104,7 @@ def _dist_case(amg, p, P, gather_rows, hier, nu, check_solve, exact_values, cycl
         beg, end = offs[rank], offs[rank + 1]
         lrp, lci, lv, ld = dist.local_block(p.rp, p.ci, p.val, p.d, beg, end)
         o = amg.amg_options_default(coarsest_size=prm.get("coarsest_size", 100), seed=prm.get("seed", 0),
-                                    gather_rows=gather_rows, cycle=cycle)
+                                    gather_rows=gather_rows, cycle=cycle, global_agg=int(global_agg))
         h = amg.amg_setup_dist(comm, p.n, beg, lrp, lci, lv, ld, prm["passes"], m, o)
         try:
             info = amg.amg_get_info(h)
@@ -224,6 +226,33 @@ def test_dist_fully_replicated(amg, gen_mod, oracle_mod):
     p = gen_mod.problem("C1")
     res = dist_case(amg, p, 2, 10 ** 9, oracle_mod)
     assert res[0]["info"]["dist_levels"] == 0
+
+
+@pytest.mark.parametrize("case", ["c1_p2", "c1_p3_deep", "3d_p4", "rand_p3", "rgg_p2", "c2_p4", "c1_p2_amli"])
+def test_dist_global_aggregation(amg, gen_mod, oracle_mod, case):
+    """global (non-decoupled) aggregation across the ranks -- matching by halo
+    rounds over the inter-block edges, aggregates owned by their leader's rank, coarse rows formed
+    from members on several ranks, restriction with the remote members' residuals, prolongation from
+    the coarse halo.  Every level concatenated over the ranks equals the oracle's single-GPU (nparts
+    = 1) hierarchy bit for bit; B_0(r) element-wise <= 1e-10; iterations +-1."""
+    if case.startswith("c1"):
+        p = gen_mod.problem("C1")
+    elif case == "3d_p4":
+        p = gen_mod.problem("C4", size=14)
+        p.params["coarsest_size"] = 30
+    elif case == "rand_p3":
+        p = gen_mod.random_graph(3000, 7, seed=9, weighted=True, dirichlet=True)
+        p.params = dict(passes=2, degree=2, coarsest_size=50, seed=0)
+    elif case == "rgg_p2":
+        p = gen_mod.rgg(12000, seed=7)
+        p.params = dict(passes=3, degree=4, coarsest_size=60, seed=0)
+    else:
+        p = gen_mod.problem("C2", size=128)
+    P, G = {"c1_p2": (2, 300), "c1_p3_deep": (3, 0), "3d_p4": (4, 200), "rand_p3": (3, 400), "rgg_p2": (2, 1000),
+            "c2_p4": (4, 2000), "c1_p2_amli": (2, 0)}[case]
+    res = dist_case(amg, p, P, G, oracle_mod, global_agg=True, cycle=2 if case.endswith("amli") else 0,
+                    overlap=(True, False) if case == "c2_p4" else (True,))
+    assert res[0]["info"]["dist_levels"] >= 1
 
 
 @pytest.mark.slow
