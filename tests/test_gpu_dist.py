@@ -256,6 +256,16 @@ def test_dist_global_aggregation(amg, gen_mod, oracle_mod, case):
 
 
 @pytest.mark.slow
+def test_dist_global_aggregation_production_size(amg, gen_mod, oracle_mod):
+    """Global aggregation on the production configuration: C3 recipe 2048^2 over 4 ranks (compressed
+    level 0, TMA interior views, aggregates crossing the block boundaries): bit-exact hierarchy vs
+    the oracle's single-GPU one, B_0(r) element-wise <= 1e-10, iterations +-1."""
+    p = gen_mod.problem("C3", size=2048)
+    res = dist_case(amg, p, 4, 50000, oracle_mod, global_agg=True, expect_path=3)
+    assert all(r["info"]["level0_format"] == 2 for r in res)
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("case", ["c3_2048_p2", "c3_2048_p4", "c4_128_p2"])
 def test_dist_production_size(amg, gen_mod, oracle_mod, case):
     """The configuration every rank runs at P = 8 on C3: level 0 large enough per rank
