@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--per-config-steps", type=int, default=3)
     ap.add_argument("--dist", action="store_true", help="use the row-partitioned path even on one GPU")
+    ap.add_argument("--global-agg", action="store_true",
+                    help="row-partitioned path with global aggregation (SURVEY 8(f) item 4) instead of decoupled")
     return ap.parse_args()
 
 
@@ -339,7 +341,7 @@ def main_ours(a):
     b_np = gen.rhs(n, prm["seed"])
     stream = torch.cuda.current_stream(dev)
     opts = amg.amg_options_default(coarsest_size=prm["coarsest_size"], seed=prm["seed"],
-                                   stream=stream.cuda_stream)
+                                   stream=stream.cuda_stream, global_agg=int(a.global_agg))
     comm = None
     beg, end = 0, n
     arrs = (prob.rp, prob.ci, prob.val, prob.d)
@@ -518,7 +520,8 @@ def main_ours(a):
                    "levels": last["levels"], "n_levels": last["n"], "iters": iters, "status": status,
                    "grid_complexity": last["grid_complexity"], "operator_complexity": last["operator_complexity"],
                    "l2": "inputs larger than L2 (CSR+vectors >> 126 MB); no flush",
-                   "parallelism": (f"row-partitioned x{world} over NCCL (decoupled aggregation, halo per SpMV pass, "
+                   "parallelism": (f"row-partitioned x{world} over NCCL ({'global' if a.global_agg else 'decoupled'} "
+                                   f"aggregation, halo per SpMV pass, "
                                    f"rank-order dot allreduce, levels < {opts.gather_rows} rows gathered; "
                                    f"{last['dist_levels']} partitioned levels)") if comm is not None else "single GPU",
                    "step": "amg_setup + amg_solve(x0=0, tol 1e-8) + amg_free, inputs resident in HBM"},
