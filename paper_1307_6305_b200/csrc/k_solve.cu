@@ -1028,8 +1028,10 @@ static void launch_tma_fmt(const SpOp& op, const double* xg, const Epi& e, doubl
         default:
             if (op.S.wmax <= 12) launch_tma_w<Epi, DOTS, VM, CM, 12, 1, 3>(op, xg, e, part, tk, d, s);
             else if (op.S.wmax <= 16) launch_tma_w<Epi, DOTS, VM, CM, 16, 1, 3>(op, xg, e, part, tk, d, s);
-            else if constexpr (tma_wide_fmt(VM, CM))  // fp64 values: a 2-stage ring fits the 227 KB
-                launch_tma_w<Epi, DOTS, VM, CM, 32, 1, (VM == 0 ? 2 : 3)>(op, xg, e, part, tk, d, s);
+            else if constexpr (tma_wide_fmt(VM, CM))  // 2-stage rings: 3 CTAs/SM with 1-byte value codes (C5's
+                // level 0: 149.4 -> 134.3 us per step against 3 stages; 4 stages 258 us; 2 slices/warp 1.5 ms),
+                // and the only ring of fp64 values that fits the 227 KB
+                launch_tma_w<Epi, DOTS, VM, CM, 32, 1, 2>(op, xg, e, part, tk, d, s);
     }
 }
 
