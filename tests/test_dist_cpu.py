@@ -148,3 +148,25 @@ def test_halo_plan_argument_errors():
         amg.amg_halo_plan(0, 4, np.array([0, 4, 8], np.int64), 0, np.array([2], np.int32))
     segs, nlo = amg.amg_halo_plan(4, 4, np.array([0, 4, 8, 12], np.int64), 1, np.array([1, 3, 8, 9], np.int32))
     assert nlo == 2 and segs == [(0, -2, 2), (2, 4, 2)]
+
+
+def test_bench_launcher_guards():
+    """bench.py --gpus N > 1 outside torchrun re-executes itself as N ranks; with fewer visible
+    GPUs (none here) it exits 2 with a JSON error instead of silently running one rank, and under a
+    launcher whose WORLD_SIZE differs from --gpus it exits 2 as well (the driver calls
+    python bench.py --gpus N)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2, (r.returncode, r.stdout, r.stderr)
+    assert "error" in json.loads(r.stdout.strip().splitlines()[-1])
+    env["WORLD_SIZE"] = "4"
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2"], capture_output=True,
+                       text=True, env=env, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stdout
