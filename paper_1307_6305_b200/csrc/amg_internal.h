@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -28,6 +29,15 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 void set_last_error(const std::string& msg);  // amg_last_error() text of the calling thread
 std::string validation_message(int flags);    // text of validate_input's flags
 #define CK(call) ::amg::cuda_check((call), #call, __FILE__, __LINE__)
+
+// NVTX ranges (tracing): ABI calls, setup phases per level, outer FCG iterations.  Header-only
+// NVTX v3: without a tool attached (nsys, ncu --nvtx) every push/pop is a no-op call.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- device views
 struct Csr {           // A_l: int32 row_ptr / col, fp64 values; arrays padded by >= 4 elements

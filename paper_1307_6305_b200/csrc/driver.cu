@@ -180,12 +180,14 @@ GraphReaper* reaper() {
 static void destroy_graphs(amg_hierarchy* h, bool deferred = false) {
     int dev = 0;
     if (deferred) cudaGetDevice(&dev);
-    for (auto g : h->graphs)
-        if (g) {
-            if (deferred) reaper()->push(dev, g);
-            else cudaGraphExecDestroy(g);
-        }
+    for (auto* v : {&h->graphs, &h->graphs_head})
+        for (auto g : *v)
+            if (g) {
+                if (deferred) reaper()->push(dev, g);
+                else cudaGraphExecDestroy(g);
+            }
     h->graphs.clear();
+    h->graphs_head.clear();
     h->graph_nu = 0;
 }
 
@@ -290,6 +292,7 @@ struct PhaseTimer {
         return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
     }
     void mark(const char* what, int l = -1) {
+        nvtxMarkA(what);  // phase boundary on the NVTX timeline (no-op without a tool)
         if (!on) return;
         cudaStreamSynchronize(s);
         double t = now();
@@ -463,6 +466,9 @@ void amg::build_levels(amg_hierarchy* h, int l0, int* agg0, int nc0) {
     const int m = h->m;
     int l = l0;
     for (;;) {
+        char nvname[32];
+        snprintf(nvname, sizeof(nvname), "amg setup level %d", l);
+        NvtxRange nv(nvname);
         Level& Lv = h->lev[l];
         Lv.nglob = Lv.A.n;
         Lv.nnz_glob = Lv.A.nnz;
@@ -999,6 +1005,18 @@ static void run_steps(amg_hierarchy* h, int l, const double* f, const std::vecto
     }
 }
 
+// Each outer iteration's graph is captured in two parts, split after level 0's residual and
+// restriction: the head (the m pre-smoothing steps, the residual, the restriction: ~0.5 ms of GPU
+// work on C3/C4) and the rest.  cudaGraphLaunch of the whole 134-node (C3) / 508-node (C4) graph kept
+// the GPU idle for ~0.09 / ~0.43 ms after every convergence check (tools/timeline.py); the head is
+// submitted in a few microseconds and the rest is submitted while the head runs.
+static void capture_split_point(amg_hierarchy* h) {
+    if (!h->cap_split) return;
+    h->cap_split = false;
+    CK(cudaStreamEndCapture(h->s, &h->cap_head));
+    CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+}
+
 // z = B_l(r): pre-smoothing from 0, residual, restriction, coarse correction,
 // prolongation, post-smoothing; the last smoothing step writes `out` (distinct from rin and the
 // level buffers).  `rin` must be a vector of level l's layout (it is the first step's SpMV input).
@@ -1054,6 +1072,7 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
         else launch_restrict(Lv.nc, Lv.aptr, Lv.perm, Lv.RES, C.RHO + cb, s);
     }
     if (gather) allgatherv_d(h, C.RHO, C.offs);
+    if (l == 0) capture_split_point(h);
     // coarse correction (A12: exact solve when the next level is the coarsest)
     // (global aggregation: agg holds global ids of a replicated coarse level, or coarse relative
     // indices -- remote aggregates in the coarse halo -- of a row-partitioned one)
@@ -1150,21 +1169,34 @@ static void capture_graph(amg_hierarchy* h, int pos, int nu) {
     if (h->graph_nu != nu) {
         destroy_graphs(h);
         h->graphs.assign(h->W, nullptr);
+        h->graphs_head.assign(h->W, nullptr);
         h->graph_nu = nu;
     }
     if (h->graphs[pos]) return;
     cudaGraph_t g;
     long long before = g_launches;
     CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+    h->cap_head = nullptr;
+    static const bool no_split = getenv("AMG_NO_GRAPH_SPLIT") != nullptr;  // A/B experiments
+    h->cap_split = !h->comm && !no_split;  // (row-partitioned levels fork onto the communication stream)
     try {
         outer_iteration(h, pos, nu);
     } catch (...) {
+        h->cap_split = false;
         cudaStreamEndCapture(h->s, &g);
+        if (h->cap_head) cudaGraphDestroy(h->cap_head);
+        h->cap_head = nullptr;
         throw;
     }
+    h->cap_split = false;
     CK(cudaStreamEndCapture(h->s, &g));
     h->graph_launches = g_launches - before;
     g_launches = before;
+    if (h->cap_head) {
+        CK(cudaGraphInstantiate(&h->graphs_head[pos], h->cap_head, 0));
+        CK(cudaGraphDestroy(h->cap_head));
+        h->cap_head = nullptr;
+    }
     CK(cudaGraphInstantiate(&h->graphs[pos], g, 0));
     CK(cudaGraphDestroy(g));
 }
@@ -1229,7 +1261,9 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
         for (k = 0;; ++k) {
             if (rnorm <= tol * bnorm) { status = AMG_OK; break; }
             if (k >= h->opt.max_iter) break;
+            NvtxRange nv_it("amg outer FCG iteration");
             if (graphs) {
+                if (h->graphs_head[pos]) CK(cudaGraphLaunch(h->graphs_head[pos], s));
                 CK(cudaGraphLaunch(h->graphs[pos], s));
                 ++graph_runs;
                 const int nxt = (pos + 1) % h->W;
@@ -1335,6 +1369,7 @@ static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t 
     if (o.kappa != 0.0 && !(o.kappa > 1.0)) return fail(AMG_E_ARG, "amg_setup: kappa must be 0 or > 1");
     if (o.kappa > 1.0 && !(Em_of(poly_degree, o.kappa) < 1.0))
         return fail(AMG_E_ARG, "amg_setup: E_m(kappa) >= 1: the smoother would not converge (reading A9)");
+    NvtxRange nv(comm ? "amg_setup_dist" : "amg_setup");
     amg_hierarchy* h = new amg_hierarchy();
     try {
         init_device_props();
@@ -1420,6 +1455,7 @@ int amg_setup_dist(amg_handle* out, amg_comm comm, int64_t n_global, int64_t row
 int amg_solve(amg_handle h, const double* b, double* x, double tol, int32_t k_inner, int32_t* iters, double* relres) {
     if (!h || !b || !x) return fail(AMG_E_ARG, "amg_solve: NULL argument");
     if (!(tol > 0.0) || k_inner < 1 || k_inner > kMaxWin) return fail(AMG_E_ARG, "amg_solve: bad tol or k_inner");
+    NvtxRange nv("amg_solve");
     try {
         int it = 0;
         int st = solve(h, b, x, tol, k_inner, &it, relres);
@@ -1435,6 +1471,7 @@ int amg_solve(amg_handle h, const double* b, double* x, double tol, int32_t k_in
 
 int amg_free(amg_handle h) {
     if (!h) return AMG_OK;
+    NvtxRange nv("amg_free");
     release(h);
     return AMG_OK;
 }

@@ -97,6 +97,9 @@ struct amg_hierarchy {
     int tail_smem = 0;      // doubles of shared memory the tail kernel keeps its vectors in (0 = global)
     amg::TLevel* d_tlev = nullptr;
     std::vector<cudaGraphExec_t> graphs;
+    std::vector<cudaGraphExec_t> graphs_head;  // first part of each window position's graph (split capture)
+    bool cap_split = false;                    // capture in progress, split point not reached yet
+    cudaGraph_t cap_head = nullptr;
     int graph_nu = 0;
     long long graph_launches = 0;
     std::vector<void*> allocs;
