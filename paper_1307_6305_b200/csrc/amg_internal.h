@@ -190,6 +190,10 @@ void launch_spmv_dots(const SpOp& op, const double* d, const double* rho, double
 void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, double* rH, cudaStream_t s);
 // prolongation + axpy: x[i] += eH[agg[i]]
 void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s);
+// x_i += E'[agg_i] with E' the last inner-FCG update (E' = alpha dH + eH, or alpha dH when assign;
+// alpha = *dr / *dq, 0 when *dq = 0) -- fcg_update of the coarse level fused into the prolongation
+void launch_prolong_fcg(int n, const int* agg, const double* eH, const double* dH, const double* dr, const double* dq,
+                        bool assign, double* x, cudaStream_t s);
 // dense coarse apply e = M r (M row-major n x n)
 void launch_resid_restrict(int nc, const int* aptr, const int* perm, const Csr& A, const double* x, const double* f,
                            double* rho, cudaStream_t s);

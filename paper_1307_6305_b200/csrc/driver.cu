@@ -915,10 +915,12 @@ static void spmv_dots_pass(amg_hierarchy* h, int l, double* d, const double* rho
 // FCG_inner(l, RHO_l, nu) -> E_l.  On a row-partitioned level every SpMV
 // input is halo-exchanged first and every batch of dot partials is summed over the ranks before the
 // kernels that consume it.
-static void fcg_inner(amg_hierarchy* h, int l, int nu) {
+// defer_last: the last update E (+)= alpha D_{nu-1} is left to the caller's fused prolongation
+// (launch_prolong_fcg); returns true if it was deferred.
+static bool fcg_inner(amg_hierarchy* h, int l, int nu, bool defer_last = false) {
     if (use_tail(h, l, nu)) {
         tail_call(h, 1, l, nu, nullptr, nullptr);
-        return;
+        return false;
     }
     Level& Lv = h->lev[l];
     cudaStream_t s = h->s;
@@ -947,9 +949,11 @@ static void fcg_inner(amg_hierarchy* h, int l, int nu) {
             launch_direction(n, Lv.Z, Dp, c, dq, i, Di, s);
         }
         spmv_dots_pass(h, l, Di, rho, Qi, dq + i, dr + i);  // q = A d, d.q, d.rho
+        if (defer_last && i == nu - 1) return true;
         launch_fcg_update(n, dr + i, dq + i, Di, Qi, Lv.E, i == 0, (i < nu - 1) ? rho : nullptr, nullptr, nullptr,
                           h->ds, s);
     }
+    return false;
 }
 
 // Stationary AMLI coarse correction at level l (cycle 2; reading A23):
@@ -1079,11 +1083,18 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     if (l + 1 == h->L - 1) {  // exact coarsest solve fused with the prolongation
         launch_gemv_prolong(Lv.A.n, Lv.agg, Lv.gx ? 0 : (int)cb, C.A.n, h->Minv, C.RHO, cur, s);
     } else {
+        // single-GPU levels: the inner FCG's last E update is fused into the prolongation
+        const bool fuse = h->opt.cycle != 2 && !Lv.dist && !C.dist && !Lv.gx;
+        bool deferred = false;
         if (h->opt.cycle == 2)
             amli_correction(h, l + 1, nu);
         else
-            fcg_inner(h, l + 1, nu);
-        if (Lv.gx) {
+            deferred = fcg_inner(h, l + 1, nu, fuse);
+        if (deferred) {
+            const int i = nu - 1;
+            launch_prolong_fcg(Lv.A.n, Lv.agg, C.E, C.D + (size_t)i * C.ld, C.sc + kMaxWin + i, C.sc + i, i == 0, cur,
+                               s);
+        } else if (Lv.gx) {
             if (C.dist) halo_exchange(h, l + 1, C.E);
             launch_prolong(Lv.A.n, Lv.agg, C.E, cur, s);
         } else {

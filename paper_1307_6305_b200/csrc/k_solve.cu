@@ -971,6 +971,8 @@ static bool tma_enabled() {
 
 // formats that get W = 32 instances (variable-width levels wider than 16, e.g. the RGG's level 0:
 // 1-byte value codes + int16 column offsets); the others stop at 16 to bound compile time
+// (C4's level 1 -- 1-byte value codes + int32 columns, offsets +-53k -- measured no faster on a W = 32
+// TMA instance than on the register SELL: 61.9 us per pass either way; its scattered gathers bound it)
 __host__ __device__ constexpr bool tma_wide_fmt(int vm, int cm) { return (vm == 1 && cm == 2) || (vm == 0 && cm == 2); }
 
 template <class Epi, bool DOTS, int VM, int CM, int W, int SPW, int NS>
@@ -1148,6 +1150,63 @@ __global__ void __launch_bounds__(kBlock) k_prolong(int n, const int* __restrict
     for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) x[i] += __ldg(eH + agg[i]);
 }
 
+// The last inner-FCG update fused with the prolongation (E_l is read only by the prolongation):
+// x_i += E'[agg_i], E' = alpha d + E (ASSIGN: alpha d), alpha = d.rho / d.q (0 when d.q = 0, reading
+// A13) -- the same fma as k_fcg_update's E update, then the same single add as k_prolong.  One launch
+// less per inner-FCG visit; E itself is not written.
+template <bool V, bool ASSIGN>
+__global__ void __launch_bounds__(kBlock) k_prolong_fcg(int n, const int* __restrict__ agg,
+                                                        const double* __restrict__ eH, const double* __restrict__ dH,
+                                                        const double* __restrict__ dr, const double* __restrict__ dq,
+                                                        double* __restrict__ x) {
+    const double den = *dq;
+    const double alpha = (den != 0.0) ? (*dr) / den : 0.0;
+    auto e = [&](int a) -> double {
+        const double d = __ldg(dH + a);
+        return ASSIGN ? alpha * d : fma(alpha, d, __ldg(eH + a));
+    };
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if constexpr (V) {
+        const int64_t n4 = n >> 2;
+        const int4* A4 = reinterpret_cast<const int4*>(agg);
+        double2* X2 = reinterpret_cast<double2*>(x);
+        int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; q + st < n4; q += 2 * st) {  // two quads in flight per thread (as k_prolong)
+            const int4 a0 = A4[q], a1 = A4[q + st];
+            double2 x0 = X2[2 * q], x1 = X2[2 * q + 1], x2 = X2[2 * (q + st)], x3 = X2[2 * (q + st) + 1];
+            const double e0 = e(a0.x), e1 = e(a0.y), e2 = e(a0.z), e3 = e(a0.w);
+            const double e4 = e(a1.x), e5 = e(a1.y), e6 = e(a1.z), e7 = e(a1.w);
+            x0.x += e0; x0.y += e1; x1.x += e2; x1.y += e3;
+            x2.x += e4; x2.y += e5; x3.x += e6; x3.y += e7;
+            X2[2 * q] = x0; X2[2 * q + 1] = x1; X2[2 * (q + st)] = x2; X2[2 * (q + st) + 1] = x3;
+        }
+        for (; q < n4; q += st) {
+            const int4 a0 = A4[q];
+            double2 x0 = X2[2 * q], x1 = X2[2 * q + 1];
+            x0.x += e(a0.x); x0.y += e(a0.y); x1.x += e(a0.z); x1.y += e(a0.w);
+            X2[2 * q] = x0; X2[2 * q + 1] = x1;
+        }
+        i0 = n4 << 2;
+    }
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) x[i] += e(agg[i]);
+}
+
+void launch_prolong_fcg(int n, const int* agg, const double* eH, const double* dH, const double* dr, const double* dq,
+                        bool assign, double* x, cudaStream_t s) {
+    const bool v = al16(agg) && al16(x);
+    const dim3 g(vgrid(v ? (n + 3) / 4 : n)), b(kBlock);
+    if (v) {
+        if (assign) launch_k(k_prolong_fcg<true, true>, g, b, 0, s, n, agg, eH, dH, dr, dq, x);
+        else launch_k(k_prolong_fcg<true, false>, g, b, 0, s, n, agg, eH, dH, dr, dq, x);
+    } else {
+        if (assign) launch_k(k_prolong_fcg<false, true>, g, b, 0, s, n, agg, eH, dH, dr, dq, x);
+        else launch_k(k_prolong_fcg<false, false>, g, b, 0, s, n, agg, eH, dH, dr, dq, x);
+    }
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
 void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s) {
     if (al16(agg) && al16(x)) launch_k(k_prolong<true>, dim3(vgrid((n + 3) / 4)), dim3(kBlock), 0, s, n, agg, eH, x);
     else launch_k(k_prolong<false>, dim3(vgrid(n)), dim3(kBlock), 0, s, n, agg, eH, x);
@@ -1239,8 +1298,24 @@ __global__ void __launch_bounds__(kBlock) k_resid_restrict(int nc, const int* __
             double r = 0.0;
             if (t < t1) {
                 const int i = perm[t];
+                // the row's chain in CSR order, its loads issued 8 entries at a time (one dependent
+                // column -> gather round trip per 8 entries instead of per entry)
                 double acc = 0.0;
-                for (int p = rp[i]; p < rp[i + 1]; ++p) acc = fma(v[p], ld_gather(x + ci[p]), acc);
+                const int p1 = rp[i + 1];
+                for (int p = rp[i]; p < p1; p += 8) {
+                    int c[8];
+                    double a[8], xv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        c[u] = p + u < p1 ? __ldg(ci + p + u) : -1;
+                        a[u] = p + u < p1 ? __ldg(v + p + u) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (c[u] >= 0) acc = fma(a[u], xv[u], acc);
+                }
                 r = ld_nc(f + i) - acc;
             }
             const int cnt = min(32, t1 - tb);
