@@ -190,6 +190,12 @@ void launch_spmv_dots(const SpOp& op, const double* d, const double* rho, double
 void launch_restrict(int nc, const int* aptr, const int* perm, const double* r, double* rH, cudaStream_t s);
 // prolongation + axpy: x[i] += eH[agg[i]]
 void launch_prolong(int n, const int* agg, const double* eH, double* x, cudaStream_t s);
+// nu = 2 inner FCG without d_1: the z-dots pass (out3 = z.Az, z.q0, z.rho) and the prolongation of
+// E = c0 d0 + c1 z with the coefficients formed from sc (k_solve.cu k_prolong_fcg2)
+void launch_spmv_zdots(const SpOp& op, const double* z, const double* q0, const double* rho, double* out3,
+                       const DotScratch& ds, cudaStream_t s);
+void launch_prolong_fcg2(int n, const int* agg, const double* d0, const double* z, const double* sc, double* x,
+                         cudaStream_t s);
 // x_i += E'[agg_i] with E' the last inner-FCG update (E' = alpha dH + eH, or alpha dH when assign;
 // alpha = *dr / *dq, 0 when *dq = 0) -- fcg_update of the coarse level fused into the prolongation
 void launch_prolong_fcg(int n, const int* agg, const double* eH, const double* dH, const double* dr, const double* dq,

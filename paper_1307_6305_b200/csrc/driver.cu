@@ -915,12 +915,18 @@ static void spmv_dots_pass(amg_hierarchy* h, int l, double* d, const double* rho
 // FCG_inner(l, RHO_l, nu) -> E_l.  On a row-partitioned level every SpMV
 // input is halo-exchanged first and every batch of dot partials is summed over the ranks before the
 // kernels that consume it.
-// defer_last: the last update E (+)= alpha D_{nu-1} is left to the caller's fused prolongation
-// (launch_prolong_fcg); returns true if it was deferred.
-static bool fcg_inner(amg_hierarchy* h, int l, int nu, bool defer_last = false) {
+// defer_last: the last update E (+)= alpha D_{nu-1} is left to the caller's fused prolongation.
+// Returns kFcgDone (E written), kFcgDeferred (launch_prolong_fcg with D_{nu-1} and its dots), or, for
+// nu = 2, kFcgZ: the second direction d_1 = z - beta_0 d_0 and q_1 = A d_1 are never formed -- one
+// pass over z gives z.Az, z.q_0, z.rho_1, from which beta_0, d_1.q_1 and alpha_1 follow (symmetric A;
+// see k_prolong_fcg2), and the caller prolongs E = (alpha_0 - alpha_1 beta_0) d_0 + alpha_1 z.  Two
+// launches (the multidot and the direction) and the d_1 / q_1 vectors less per visit; the same
+// iterate as the direct form up to rounding.
+enum { kFcgDone = 0, kFcgDeferred = 1, kFcgZ = 2 };
+static int fcg_inner(amg_hierarchy* h, int l, int nu, bool defer_last = false) {
     if (use_tail(h, l, nu)) {
         tail_call(h, 1, l, nu, nullptr, nullptr);
-        return false;
+        return kFcgDone;
     }
     Level& Lv = h->lev[l];
     cudaStream_t s = h->s;
@@ -938,6 +944,10 @@ static bool fcg_inner(amg_hierarchy* h, int l, int nu, bool defer_last = false) 
         Qp[i] = Qi;
         if (i == 0) {
             apply_B(h, l, nu, rho, Di);
+        } else if (defer_last && nu == 2 && !Lv.dist && !h->no_zform) {
+            apply_B(h, l, nu, rho, Lv.Z);
+            launch_spmv_zdots(Lv.op, Lv.Z, Qp[0], rho, c, h->ds, s);
+            return kFcgZ;
         } else {
             apply_B(h, l, nu, rho, Lv.Z);
             launch_multidot(n, Lv.Z, Qp, i, c, h->ds, s);
@@ -949,11 +959,11 @@ static bool fcg_inner(amg_hierarchy* h, int l, int nu, bool defer_last = false) 
             launch_direction(n, Lv.Z, Dp, c, dq, i, Di, s);
         }
         spmv_dots_pass(h, l, Di, rho, Qi, dq + i, dr + i);  // q = A d, d.q, d.rho
-        if (defer_last && i == nu - 1) return true;
+        if (defer_last && i == nu - 1) return kFcgDeferred;
         launch_fcg_update(n, dr + i, dq + i, Di, Qi, Lv.E, i == 0, (i < nu - 1) ? rho : nullptr, nullptr, nullptr,
                           h->ds, s);
     }
-    return false;
+    return kFcgDone;
 }
 
 // Stationary AMLI coarse correction at level l (cycle 2; reading A23):
@@ -1085,12 +1095,14 @@ static void apply_B(amg_hierarchy* h, int l, int nu, const double* rin, double* 
     } else {
         // single-GPU levels: the inner FCG's last E update is fused into the prolongation
         const bool fuse = h->opt.cycle != 2 && !Lv.dist && !C.dist && !Lv.gx;
-        bool deferred = false;
+        int fr = kFcgDone;
         if (h->opt.cycle == 2)
             amli_correction(h, l + 1, nu);
         else
-            deferred = fcg_inner(h, l + 1, nu, fuse);
-        if (deferred) {
+            fr = fcg_inner(h, l + 1, nu, fuse);
+        if (fr == kFcgZ) {
+            launch_prolong_fcg2(Lv.A.n, Lv.agg, C.D, C.Z, C.sc, cur, s);
+        } else if (fr == kFcgDeferred) {
             const int i = nu - 1;
             launch_prolong_fcg(Lv.A.n, Lv.agg, C.E, C.D + (size_t)i * C.ld, C.sc + kMaxWin + i, C.sc + i, i == 0, cur,
                                s);
@@ -1403,6 +1415,7 @@ static int setup_impl(amg_handle* out, amg_comm comm, int64_t n_global, int64_t 
             h->dev = dev;
             h->s = stream_acquire(dev);
         }
+        h->no_zform = getenv("AMG_NO_ZFORM") != nullptr;
         CK(cudaEventCreate(&h->e0));
         CK(cudaEventCreate(&h->e1));
         CK(cudaEventCreate(&h->pe0));

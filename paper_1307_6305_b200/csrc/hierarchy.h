@@ -98,6 +98,7 @@ struct amg_hierarchy {
     amg::TLevel* d_tlev = nullptr;
     std::vector<cudaGraphExec_t> graphs;
     std::vector<cudaGraphExec_t> graphs_head;  // first part of each window position's graph (split capture)
+    bool no_zform = false;                     // AMG_NO_ZFORM: nu = 2 inner FCG in the direct form (A/B)
     bool cap_split = false;                    // capture in progress, split point not reached yet
     cudaGraph_t cap_head = nullptr;
     int graph_nu = 0;

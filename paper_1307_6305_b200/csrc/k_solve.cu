@@ -166,6 +166,21 @@ struct EpiSpmvDots {  // q = A d; acc = (d.q, d.rho)
     }
 };
 
+// The last inner-FCG iteration for nu = 2 without materialising d_1 = z - beta_0 d_0 (driver.cu
+// fcg_inner): (A z)_i is formed and consumed, never stored; acc = (z.Az, z.q_0, z.rho_1)
+struct EpiZDots {
+    const double* q0;
+    const double* rho;
+    static constexpr int ND = 3;
+    struct Pre { double q, r; };
+    __device__ __forceinline__ Pre load(int i) const { return Pre{ld_nc(q0 + i), ld_nc(rho + i)}; }
+    __device__ __forceinline__ void store(int, double s, double zi, const Pre& p, double* acc) const {
+        acc[0] += zi * s;
+        acc[1] += zi * p.q;
+        acc[2] += zi * p.r;
+    }
+};
+
 // ------------------------------------------------------------------ tiled SpMV-class kernel
 // Shared memory per block: cap+2 doubles and cap+4 ints (16-byte aligned staging of the tile's
 // col/val run from the 16-byte-aligned chunk containing its first entry).
@@ -1099,6 +1114,11 @@ void launch_spmv_dots(const SpOp& op, const double* d, const double* rho, double
     launch_op<EpiSpmvDots, true>(op, d, e, &ds, DotOut{{dot_dq, dot_dr}}, s);
 }
 
+void launch_spmv_zdots(const SpOp& op, const double* z, const double* q0, const double* rho, double* out3,
+                       const DotScratch& ds, cudaStream_t s) {
+    launch_op<EpiZDots, true>(op, z, EpiZDots{q0, rho}, &ds, DotOut{{out3, out3 + 1, out3 + 2}}, s);
+}
+
 // ------------------------------------------------------------------ transfers
 __global__ void __launch_bounds__(kBlock) k_restrict(int nc, const int* __restrict__ aptr,
                                                      const int* __restrict__ perm, const double* __restrict__ r,
@@ -1203,6 +1223,49 @@ void launch_prolong_fcg(int n, const int* agg, const double* eH, const double* d
         if (assign) launch_k(k_prolong_fcg<false, true>, g, b, 0, s, n, agg, eH, dH, dr, dq, x);
         else launch_k(k_prolong_fcg<false, false>, g, b, 0, s, n, agg, eH, dH, dr, dq, x);
     }
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+// Prolongation of the nu = 2 inner-FCG result E = alpha_0 d_0 + alpha_1 d_1 with d_1 = z - beta_0 d_0
+// never formed: x_i += c0 d_0[I] + c1 z[I], I = agg_i, c1 = alpha_1, c0 = alpha_0 - alpha_1 beta_0, from
+// the scalars sc[0] = d_0.q_0, sc[W] = d_0.rho_0, sc[2W..2W+2] = (z.Az, z.q_0, z.rho_1) (W = kMaxWin):
+//   beta_0 = z.q_0 / d_0.q_0,  d_1.q_1 = z.Az - beta_0 z.q_0  (A symmetric: d_0.Az = q_0.z),
+//   d_1.rho_1 = z.rho_1 (d_0.rho_1 = 0: alpha_0 makes rho_1 orthogonal to d_0),
+//   alpha_i = d_i.rho_i / d_i.q_i; every quotient with a zero denominator is 0 (reading A13).
+__global__ void __launch_bounds__(kBlock) k_prolong_fcg2(int n, const int* __restrict__ agg,
+                                                         const double* __restrict__ d0, const double* __restrict__ z,
+                                                         const double* __restrict__ sc, double* __restrict__ x,
+                                                         bool vec) {
+    const double dq0 = sc[0], dr0 = sc[kMaxWin], zaz = sc[2 * kMaxWin], zq = sc[2 * kMaxWin + 1],
+                 zr = sc[2 * kMaxWin + 2];
+    const double a0 = dq0 != 0.0 ? dr0 / dq0 : 0.0;
+    const double b0 = dq0 != 0.0 ? zq / dq0 : 0.0;
+    const double dq1 = zaz - b0 * zq;
+    const double a1 = dq1 != 0.0 ? zr / dq1 : 0.0;
+    const double c0 = a0 - a1 * b0, c1 = a1;
+    auto e = [&](int a) -> double { return fma(c1, __ldg(z + a), c0 * __ldg(d0 + a)); };
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if (vec) {
+        const int64_t n4 = n >> 2;
+        const int4* A4 = reinterpret_cast<const int4*>(agg);
+        double2* X2 = reinterpret_cast<double2*>(x);
+        for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += st) {
+            const int4 a = A4[q];
+            double2 x0 = X2[2 * q], x1 = X2[2 * q + 1];
+            x0.x += e(a.x); x0.y += e(a.y); x1.x += e(a.z); x1.y += e(a.w);
+            X2[2 * q] = x0; X2[2 * q + 1] = x1;
+        }
+        i0 = n4 << 2;
+    }
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) x[i] += e(agg[i]);
+}
+
+void launch_prolong_fcg2(int n, const int* agg, const double* d0, const double* z, const double* sc, double* x,
+                         cudaStream_t s) {
+    const bool v = al16(agg) && al16(x);
+    launch_k(k_prolong_fcg2, dim3(vgrid(v ? (n + 3) / 4 : n)), dim3(kBlock), 0, s, n, agg, d0, z, sc, x, v);
     CK(cudaGetLastError());
     ++g_launches;
 }
