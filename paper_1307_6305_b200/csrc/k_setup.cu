@@ -419,12 +419,28 @@ __global__ void __launch_bounds__(kBlock) k_propose(int nv, const int* __restric
         uint64_t bh = 0;
         int bu = -1;
         if (act) {
+            // the lane's entries in batches of 4: columns and weights, then the mate gathers, are each
+            // in flight together (the max over distinct keys does not depend on the visiting order)
             const int p1 = rp[v + 1];
-            for (int p = rp[v] + t; p < p1; p += G) {
-                const int u = ci[p];
-                if (mate[u] != -1) continue;
-                const EKey k = make_key(w[p], v, u, salt, off);
-                if (bu < 0 || prop_gt(k.w, k.h, u, bw, bh, bu, v)) { bw = k.w; bh = k.h; bu = u; }
+            for (int p = rp[v] + t; p < p1; p += 4 * G) {
+                int uu[4];
+                uint32_t ww[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int q = p + k * G;
+                    uu[k] = q < p1 ? ci[q] : -1;
+                    ww[k] = q < p1 ? w[q] : 0u;
+                }
+                bool fr[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) fr[k] = uu[k] >= 0 && mate[uu[k]] == -1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!fr[k]) continue;
+                    const int u = uu[k];
+                    const EKey key = make_key(ww[k], v, u, salt, off);
+                    if (bu < 0 || prop_gt(key.w, key.h, u, bw, bh, bu, v)) { bw = key.w; bh = key.h; bu = u; }
+                }
             }
         }
 #pragma unroll
@@ -524,7 +540,10 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, in
     for (;;) {
         const int gp = std::max(1, std::min((int)(((int64_t)nv * Gl + kBlock - 1) / kBlock), 148 * 8));
         const int ga = std::max(1, std::min(grid_for(nv), 148 * 8));
-        const int nb = list ? kBatch : first;
+        // small graphs (coarse levels): rounds cost ~5 us, a read-back ~20 us of idle GPU, so the
+        // batches are longer there (C3 levels 1-3 finish a pass in one or two batches)
+        const bool small = n <= 200000;
+        const int nb = list ? (small ? 4 : kBatch) : (small ? 6 : first);
         for (int k = 0; k < nb; ++k) {
             CK(cudaMemsetAsync(any, 0, sizeof(int), s));
             switch (Gl) {

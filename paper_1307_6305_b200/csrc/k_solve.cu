@@ -414,6 +414,9 @@ __device__ __forceinline__ double sell_row_w(const SellOps<VM, CM>& ops, size_t 
     }
 }
 
+// (the generic-width instance, C4's level 1, is latency-bound on its gathers -- ncu: L1/TEX 81% busy,
+// 29% issue, 64 registers = 4 CTAs/SM -- but capping it at 48 / 40 registers for 5 / 6 CTAs/SM
+// spilled and was slower: 64.0 / 69.3 us per step against 61.9)
 template <class Epi, bool DOTS, int VM, int CM, int WMAX>
 __global__ void __launch_bounds__(kBlock) k_sell(Sell S, const double* __restrict__ xg, Epi epi, double* partials,
                                                  unsigned* ticket, DotOut dot_out) {
@@ -923,8 +926,25 @@ __global__ void __launch_bounds__(kBlock) k_vcsr(Csr A, const double* __restrict
                 pre = epi.load(i);
                 xi = ld_gather(xg + i);
             }
+            // the lane's entries p = rp[i] + sub + G*u in batches of 8: the batch's column and value
+            // loads, then its 8 gathers, are each in flight together (one dependent round trip per
+            // batch instead of per entry); the fma chain keeps the entry order
             const int p1 = rp[i + 1];
-            for (int p = rp[i] + sub; p < p1; p += G) s = fma(va[p], ld_gather(xg + ci[p]), s);
+            for (int p = rp[i] + sub; p < p1; p += 8 * G) {
+                int c[8];
+                double a[8], xv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int q = p + u * G;
+                    c[u] = q < p1 ? __ldg(ci + q) : -1;
+                    a[u] = q < p1 ? __ldg(va + q) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_gather(xg + c[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (c[u] >= 0) s = fma(a[u], xv[u], s);
+            }
         }
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
@@ -1043,6 +1063,8 @@ static void launch_tma_fmt(const SpOp& op, const double* xg, const Epi& e, doubl
         case 7: launch_tma_v<Epi, DOTS, VM, CM, 7>(op, xg, e, part, tk, d, s); break;
         case 8: launch_tma_v<Epi, DOTS, VM, CM, 8>(op, xg, e, part, tk, d, s); break;
         default:
+            // (a 2-stage ring for the L2-resident W = 16 level measured slower: C3's level 1 17.1 vs
+            // 14.7 us per step; ncu: L1/TEX 72% busy, 24% issue -- gather latency, not the ring, bounds it)
             if (op.S.wmax <= 12) launch_tma_w<Epi, DOTS, VM, CM, 12, 1, 3>(op, xg, e, part, tk, d, s);
             else if (op.S.wmax <= 16) launch_tma_w<Epi, DOTS, VM, CM, 16, 1, 3>(op, xg, e, part, tk, d, s);
             else if constexpr (tma_wide_fmt(VM, CM))  // 2-stage rings: 3 CTAs/SM with 1-byte value codes (C5's
