@@ -21,6 +21,7 @@ ap.add_argument("--max-iter", type=int, default=500)
 ap.add_argument("--json", default=None)
 ap.add_argument("--head", type=int, default=0, help="print the first K operations of each part")
 ap.add_argument("--top", type=int, default=0, help="print the K kernels with the most summed time per part")
+ap.add_argument("--host", action="store_true", help="pinned host inputs and x (the e2e path of bench.py)")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -31,9 +32,15 @@ from paper_1307_6305_b200 import amg  # noqa: E402
 p = gen.problem(a.config)
 prm = p.params
 dev = torch.device("cuda", 0)
-arrs = [torch.from_numpy(x).to(dev) if x is not None else None for x in (p.rp, p.ci, p.val, p.d)]
-b = torch.from_numpy(gen.rhs(p.n, prm["seed"])).to(dev)
-x = torch.zeros(p.n, dtype=torch.float64, device=dev)
+if a.host:
+    arrs = [torch.from_numpy(x).pin_memory() if x is not None else None for x in (p.rp, p.ci, p.val, p.d)]
+    b = torch.from_numpy(gen.rhs(p.n, prm["seed"])).pin_memory()
+    x = torch.zeros(p.n, dtype=torch.float64).pin_memory()
+else:
+    arrs = [torch.from_numpy(x).to(dev) if x is not None else None for x in (p.rp, p.ci, p.val, p.d)]
+    b = torch.from_numpy(gen.rhs(p.n, prm["seed"])).to(dev)
+    x = torch.zeros(p.n, dtype=torch.float64, device=dev)
+mark = torch.zeros(1, dtype=torch.float64, device=dev)  # its fill kernel splits setup from solve
 o = amg.amg_options_default(coarsest_size=prm["coarsest_size"], max_iter=a.max_iter)
 
 
@@ -41,6 +48,8 @@ def run():
     h = amg.amg_setup(*arrs, prm["passes"], prm["degree"], o)
     torch.cuda.synchronize()
     x.zero_()
+    if a.host:
+        mark.zero_()
     torch.cuda.synchronize()
     amg.amg_solve(h, b, x, prm["tol"], prm["k_inner"])
     info = amg.amg_get_info(h)
