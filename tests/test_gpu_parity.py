@@ -753,3 +753,29 @@ def test_zero_rhs_precond_is_zero(amg, gen_mod, oracle_mod):
                     assert not np.any(z), (tail, l, nu)
         finally:
             amg.amg_free(h)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("zform", [True, False])
+def test_inner_fcg_forms_parity(amg, gen_mod, oracle_mod, monkeypatch, zform):
+    """B_l(r) on every level of a 4-level hierarchy with nu = 2, through the z-form inner FCG (the
+    default: d_1, q_1 never formed) and through the direct form (AMG_NO_ZFORM,
+    read at setup), against the oracle's direct FCG to 1e-10 element-wise."""
+    if zform:
+        monkeypatch.delenv("AMG_NO_ZFORM", raising=False)
+    else:
+        monkeypatch.setenv("AMG_NO_ZFORM", "1")
+    p = gen_mod.problem("C2", size=128)
+    prm = p.params
+    hier = oracle_mod.Hierarchy(p.rp, p.ci, p.val, p.d, prm["passes"], prm["degree"], coarsest_size=20)
+    h = amg.amg_setup(p.rp, p.ci, p.val, p.d, prm["passes"], prm["degree"], amg.amg_options_default(coarsest_size=20))
+    try:
+        assert amg.amg_get_info(h)["levels"] == hier.nlev >= 4
+        for l in range(hier.nlev - 1):
+            n = hier.level_info(l)["n"]
+            r = np.random.default_rng(10 + l).standard_normal(n)
+            z = np.empty(n)
+            amg.amg_level_precond(h, l, 2, r, z)
+            H.assert_close(z, hier.precond(r, nu=2, level=l), 1e-10)
+    finally:
+        amg.amg_free(h)
