@@ -118,6 +118,7 @@ int validate_input(int n, int64_t nnz, int cmin, int cmax, const int64_t* rp, co
 Csr form_A0(int n, const int64_t* rp, const int32_t* ci, const double* v, const double* d, cudaStream_t s);
 // lambda_1 = max_i sum_j |a_ij|  (exact: per-row sums in CSR order, max by ordered-int atomicMax)
 double inf_norm(const Csr& A, cudaStream_t s);
+void inf_norm_launch(const Csr& A, unsigned long long* o, cudaStream_t s);
 // true if some d_i != 0
 bool any_nonzero(int n, const double* d, cudaStream_t s);
 // max |col - row| over the stored entries (0 if only a diagonal)
@@ -130,6 +131,7 @@ struct PassGraph {     // matching pass graph G_t: CSR with integer multipliciti
     int* rp = nullptr;
     int* ci = nullptr;
     uint32_t* w = nullptr;
+    bool unit = false;  // every multiplicity is 1 (G_0 of a level, reading A5): the matching kernels skip w
 };
 // off-diagonal entries with 0 <= col < n only (a row-partitioned level keeps its in-block edges: A20)
 PassGraph pass_graph0(const Csr& A, cudaStream_t s);
@@ -215,8 +217,22 @@ void launch_direction(int n, const double* z, const double* const* D, const doub
                       double* d, cudaStream_t s);
 // FCG update: alpha = dr/dq (alpha = 0 if dq == 0 and inner);  x (+)= alpha d;  r -= alpha q (if r);
 // optional rr = r.r; outer: breakdown flag if !(dq > 0).
+// x = nullptr: the x update is deferred (alpha is stored to alpha_out, *set_old = 1 if set_old;
+// launch_x_flush / launch_direction_xf apply it later)
 void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
-                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s);
+                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s,
+                       double* alpha_out = nullptr, int* set_old = nullptr);
+struct Slots {
+    int j[kMaxWin];
+};
+// x = (((x + a[j0] d_{j0}) + a[j1] d_{j1}) + ...) over the slots sl.j[0..cnt), d_j = D + j*ld: the same
+// fma sequence as cnt successive launch_fcg_update x updates, so x is bitwise the same
+void launch_x_flush(int n, double* x, const double* D, size_t ld, const double* a, const Slots& sl, int cnt,
+                    cudaStream_t s);
+// direction d = z - sum_{j<w} beta_j D[j] fused with x += a[W] d_old (if *has_old) + sum_{j<w} a[j] D[j]
+bool direction_xf_ok(int w, const double* z, const double* const* D, const double* d, const double* x);
+void launch_direction_xf(int n, const double* z, const double* const* D, const double* c, const double* dq, int w,
+                         double* d, double* x, const double* alph, const int* has_old, cudaStream_t s);
 // v -= mean(v) (two kernels: sum then subtract); tmp = one device double
 void launch_mean_project(int n, double* v, double* tmp, const DotScratch& ds, cudaStream_t s);
 // v -= (*sum) / ntot  (the second half of a mean projection whose sum was allreduced)

@@ -465,6 +465,15 @@ void amg::build_levels(amg_hierarchy* h, int l0, int* agg0, int nc0) {
     PhaseTimer pt(s);
     const int m = h->m;
     int l = l0;
+    // lambda_1 of every level goes to a device slot; one read-back after the loop (a8 needs it only
+    // for the solve and finish_build)
+    unsigned long long* lam = dalloc<unsigned long long>(kMaxLevels, s);
+    CK(cudaMemsetAsync(lam, 0, sizeof(unsigned long long) * kMaxLevels, s));
+    struct LamGuard {
+        unsigned long long* p;
+        cudaStream_t s;
+        ~LamGuard() { dfree(p, s); }
+    } lam_guard{lam, s};
     for (;;) {
         char nvname[32];
         snprintf(nvname, sizeof(nvname), "amg setup level %d", l);
@@ -472,9 +481,7 @@ void amg::build_levels(amg_hierarchy* h, int l0, int* agg0, int nc0) {
         Level& Lv = h->lev[l];
         Lv.nglob = Lv.A.n;
         Lv.nnz_glob = Lv.A.nnz;
-        Lv.lambda1 = inf_norm(Lv.A, s);
-        Lv.kappa = h->opt.kappa > 1.0 ? h->opt.kappa : kappa_rule(m);
-        poly_coeffs(Lv.lambda1, Lv.kappa, m, Lv.alpha, Lv.beta);
+        inf_norm_launch(Lv.A, lam + l, s);
         pt.mark("lambda1", l);
         if (Lv.A.n <= h->opt.coarsest_size) break;
         if (l + 1 >= kMaxLevels) throw Error(AMG_E_SETUP, "too many levels");
@@ -506,6 +513,15 @@ void amg::build_levels(amg_hierarchy* h, int l0, int* agg0, int nc0) {
         ++l;
     }
     h->L = l + 1;
+    std::vector<unsigned long long> lh((size_t)(l - l0 + 1));
+    CK(cudaMemcpyAsync(lh.data(), lam + l0, sizeof(unsigned long long) * lh.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = l0; k <= l; ++k) {
+        Level& Lv = h->lev[k];
+        memcpy(&Lv.lambda1, &lh[k - l0], sizeof(double));
+        Lv.kappa = h->opt.kappa > 1.0 ? h->opt.kappa : kappa_rule(m);
+        poly_coeffs(Lv.lambda1, Lv.kappa, m, Lv.alpha, Lv.beta);
+    }
 }
 
 double* amg::valloc(amg_hierarchy* h, Level& Lv, int slots, bool ws) {
@@ -652,6 +668,8 @@ void amg::finish_build(amg_hierarchy* h) {
     h->D = valloc(h, L0, h->W, false);
     h->Q = valloc(h, L0, h->W, false);
     h->osc = halloc<double>(h, 2 * kMaxWin + 8);
+    h->alph = halloc<double>(h, kMaxWin);
+    h->xold = halloc<int>(h, 4);
     h->flag = halloc<int>(h, 4);
     h->ds.partials = halloc<double>(h, (size_t)(kMaxWin + 2) * 4096);
     h->ds.ticket = halloc<unsigned>(h, 4);
@@ -1178,10 +1196,23 @@ static void outer_iteration(amg_hierarchy* h, int pos, int nu) {
             for (int j = 0; j < pos; ++j) cs.push_back(c + j);
             dot_allreduce(h, cs);
         }
-        launch_direction(n, h->Z, Ds, c, dq, pos, Dp, s);
+        if (h->xf && pos == h->W - 1)  // the window's deferred x updates ride along (k_direction_xf)
+            launch_direction_xf(n, h->Z, Ds, c, dq, pos, Dp, h->x, h->alph, h->xold, s);
+        else
+            launch_direction(n, h->Z, Ds, c, dq, pos, Dp, s);
     }
     spmv_dots_pass(h, 0, Dp, h->r, Qp, dq + pos, dr);
-    launch_fcg_update(n, dr, dq + pos, Dp, Qp, h->x, false, h->r, rr, h->flag, h->ds, s);
+    // x += alpha d is deferred: the window keeps every d_j, and nothing reads x before the solve ends.
+    // With xf the last position's direction applies positions 0..W-2 and the previous window's W-1;
+    // otherwise one flush at the end of every window.
+    const bool last = pos == h->W - 1;
+    launch_fcg_update(n, dr, dq + pos, Dp, Qp, nullptr, false, h->r, rr, h->flag, h->ds, s, h->alph + pos,
+                      h->xf && last ? h->xold : nullptr);
+    if (!h->xf && last) {
+        Slots sl{};
+        for (int j = 0; j < h->W; ++j) sl.j[j] = j;
+        launch_x_flush(n, h->x, h->D, ld, h->alph, sl, h->W, s);
+    }
     if (dist) dot_allreduce(h, {rr});
 }
 
@@ -1241,6 +1272,16 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     // distributed handle whose whole hierarchy is replicated (g = 0): gather the caller's blocks
     const bool gather_in = h->comm && !dist;
     ensure_inner_ws(h, nu);
+    {   // deferred outer x updates: fused into the last window position's direction when it can be
+        const double* Ds[kMaxWin];
+        for (int j = 0; j < h->W; ++j) Ds[j] = h->D + (size_t)j * h->lev[0].ld;
+        const bool xf = h->W >= 2 && direction_xf_ok(h->W - 1, h->Z, Ds, Ds[h->W - 1], h->x);
+        if (xf != h->xf) {  // the captured graphs depend on it
+            destroy_graphs(h);
+            h->xf = xf;
+        }
+        CK(cudaMemsetAsync(h->xold, 0, sizeof(int), s));
+    }
     long long launches0 = g_launches;
     CK(cudaEventRecord(h->e0, s));
     // inputs
@@ -1280,7 +1321,10 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
         status = AMG_OK;
         rnorm = 0.0;
     } else {
-        int pos = 0;
+        // deferred x updates (outer_iteration): pending = this window's positions not yet applied,
+        // oldp = the previous window's last position not yet applied (xf mode)
+        int pos = 0, pending = 0;
+        bool oldp = false;
         for (k = 0;; ++k) {
             if (rnorm <= tol * bnorm) { status = AMG_OK; break; }
             if (k >= h->opt.max_iter) break;
@@ -1297,6 +1341,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
             CK(cudaMemcpyAsync(h->hsc, rr, sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(h->hsc + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
+            if (pos == h->W - 1) { pending = 0; oldp = h->xf; } else { pending = pos + 1; }
             int fl;
             memcpy(&fl, h->hsc + 2, sizeof(int));
             if (h->L > 1) {
@@ -1310,6 +1355,11 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
             rnorm = std::sqrt(h->hsc[0]);
             pos = (pos + 1) % h->W;
         }
+        Slots sl{};
+        int cnt = 0;
+        if (oldp) sl.j[cnt++] = h->W - 1;  // in iteration order: the previous window's last, then this one's
+        for (int j = 0; j < pending; ++j) sl.j[cnt++] = j;
+        launch_x_flush(n, h->x, h->D, h->lev[0].ld, h->alph, sl, cnt, s);
     }
     // true residual ||b - A x|| (reported) and the solution back to the caller
     double* rt = h->osc + 2 * kMaxWin + 6;

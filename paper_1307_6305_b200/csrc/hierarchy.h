@@ -89,6 +89,9 @@ struct amg_hierarchy {
     int n = 0, W = 5;
     double *b = nullptr, *x = nullptr, *r = nullptr, *Z = nullptr, *D = nullptr, *Q = nullptr;
     double* osc = nullptr;  // dq[kMaxWin], c[kMaxWin], dr, rr, bb, tmp, rr_true
+    double* alph = nullptr;  // alpha_j of the window positions whose x update is still pending (deferred)
+    int* xold = nullptr;     // device flag: the last window slot's x update is pending (fused flush)
+    bool xf = false;         // x updates flushed inside the last position's direction kernel
     int* flag = nullptr;
     double* hsc = nullptr;  // pinned host mirror: rr, flag
     amg::DotScratch ds;

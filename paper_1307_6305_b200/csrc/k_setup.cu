@@ -11,6 +11,7 @@
 //    coarse entry in (row, CSR position) order.
 //  * Dense coarsest (pseudo-)inverse by Gauss-Jordan steps (SPD, no pivoting).
 // CUB (header-only, CUDA 12.9) supplies the radix sorts and scans.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -298,6 +299,14 @@ __global__ void k_rowabs_max(int n, const int* __restrict__ rp, const double* __
     if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// lambda_1 into a device slot (zeroed by the caller; the bit pattern of a double >= 0 orders as an
+// unsigned integer), read back later together with the other levels' (no host synchronisation)
+void inf_norm_launch(const Csr& A, unsigned long long* o, cudaStream_t s) {
+    k_rowabs_max<<<grid_red(A.n), kBlock, 0, s>>>(A.n, A.rp, A.v, o);
+    ++g_launches;
+    CK(cudaGetLastError());
+}
+
 double inf_norm(const Csr& A, cudaStream_t s) {
     unsigned long long* o = dalloc<unsigned long long>(1, s);
     CK(cudaMemsetAsync(o, 0, sizeof(unsigned long long), s));
@@ -345,6 +354,7 @@ PassGraph pass_graph0(const Csr& A, cudaStream_t s) {
     k_g0_fill<<<grid_for(A.n), kBlock, 0, s>>>(A.n, A.rp, A.ci, G.rp, G.ci, G.w);
     ++g_launches;
     CK(cudaGetLastError());
+    G.unit = true;  // multiplicities start at 1 on every level (A5)
     return G;
 }
 
@@ -400,10 +410,11 @@ __device__ __forceinline__ bool prop_gt(uint32_t w1, uint64_t h1, int u1, uint32
 }
 
 template <int G>
-__global__ void __launch_bounds__(kBlock) k_propose(int nv, const int* __restrict__ list, const int* __restrict__ rp,
-                                                    const int* __restrict__ ci, const uint32_t* __restrict__ w,
-                                                    int* __restrict__ mate, int* __restrict__ prop, uint64_t salt,
-                                                    int off, int* any) {
+__global__ void __launch_bounds__(kBlock) k_propose(int nv, const int* __restrict__ nvp, const int* __restrict__ list,
+                                                    const int* __restrict__ rp, const int* __restrict__ ci,
+                                                    const uint32_t* __restrict__ w, int* __restrict__ mate,
+                                                    int* __restrict__ prop, uint64_t salt, int off, int* any) {
+    if (nvp) nv = *nvp;  // list length produced on the device (no host read-back)
     __shared__ int bany;
     if (threadIdx.x == 0) bany = 0;
     __syncthreads();
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(kBlock) k_propose(int nv, const int* __restric
                 for (int k = 0; k < 4; ++k) {
                     const int q = p + k * G;
                     uu[k] = q < p1 ? ci[q] : -1;
-                    ww[k] = q < p1 ? w[q] : 0u;
+                    ww[k] = q < p1 ? (w ? w[q] : 1u) : 0u;
                 }
                 bool fr[4];
 #pragma unroll
@@ -463,7 +474,9 @@ __global__ void __launch_bounds__(kBlock) k_propose(int nv, const int* __restric
 
 // handshake round, step 2: mutual proposals match.  A free vertex's proposal target u was free when
 // the batch started, so u is on the list and prop[u] is this round's.
-__global__ void k_accept(int nv, const int* __restrict__ list, int* __restrict__ mate, const int* __restrict__ prop) {
+__global__ void k_accept(int nv, const int* __restrict__ nvp, const int* __restrict__ list, int* __restrict__ mate,
+                         const int* __restrict__ prop) {
+    if (nvp) nv = *nvp;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nv; idx += gridDim.x * blockDim.x) {
         const int v = list ? list[idx] : idx;
         if (mate[v] != -1) continue;
@@ -472,10 +485,52 @@ __global__ void k_accept(int nv, const int* __restrict__ list, int* __restrict__
     }
 }
 
-struct IsFree {
-    const int* mate;
-    __device__ bool operator()(int v) const { return mate[v] == -1; }
-};
+// free-list compaction: the vertices of list (or of 0..n-1) still free, appended tile by tile (tiles of
+// kBlock * 16 entries, one atomic per tile, so the atomics never serialise at one L2 slice).  The
+// order of the list changes no result: every round's proposal and acceptance is a function of the
+// vertex and of mate[] alone.
+__global__ void __launch_bounds__(kBlock) k_compact_free(int n, const int* __restrict__ nvp, const int* __restrict__ list,
+                                                         const int* __restrict__ mate, int* __restrict__ out,
+                                                         int* __restrict__ cnt) {
+    constexpr int IT = 16, TILE = kBlock * IT, NW = kBlock / 32;
+    const int nv = nvp ? *nvp : n;
+    __shared__ int wsum[NW];
+    __shared__ int base;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t0 = (int64_t)blockIdx.x * TILE; t0 < nv; t0 += (int64_t)gridDim.x * TILE) {
+        int v[IT];
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int64_t idx = t0 + k * kBlock + threadIdx.x;
+            v[k] = idx < nv ? (list ? list[idx] : (int)idx) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            if (v[k] >= 0 && mate[v[k]] != -1) v[k] = -1;
+            c += v[k] >= 0;
+        }
+        int inc = c;  // inclusive warp scan of the per-thread counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int k = 0; k < NW; ++k) { const int x = wsum[k]; wsum[k] = t; t += x; }
+            base = t ? atomicAdd(cnt, t) : 0;
+        }
+        __syncthreads();
+        int pos = base + wsum[wid] + inc - c;
+#pragma unroll
+        for (int k = 0; k < IT; ++k)
+            if (v[k] >= 0) out[pos++] = v[k];
+        __syncthreads();  // wsum / base are rewritten by the next tile
+    }
+}
 
 // attach (A3) + leader (A4)
 __global__ void k_leader(int n, const int* __restrict__ rp, const int* __restrict__ ci,
@@ -490,7 +545,7 @@ __global__ void k_leader(int n, const int* __restrict__ rp, const int* __restric
             EKey bk{};
             int bu = -1;
             for (int p = rp[v]; p < rp[v + 1]; ++p) {
-                EKey k = make_key(w[p], v, ci[p], salt, off);
+                EKey k = make_key(w ? w[p] : 1u, v, ci[p], salt, off);
                 if (bu < 0 || key_gt(k, bk)) { bk = k; bu = ci[p]; }
             }
             const int mu = mate[bu];  // matched by maximality
@@ -507,17 +562,164 @@ __global__ void k_assign(int n, const int* __restrict__ leader, const int* __res
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) agg[v] = id[leader[v]];
 }
 
+// One matching pass of a small pass graph in ONE cooperative launch (a2 + a3): the handshake rounds
+// of k_propose / k_accept, the attach and leader rule of k_leader, the leader numbering (exclusive
+// scan in vertex order) and k_assign, with grid barriers in place of kernel boundaries and of the
+// host's per-batch read-backs.  The rounds stop after the first round in which no free vertex found
+// a free neighbour: that round settles every vertex still free, and any later round is a no-op, so
+// the matching is the launch path's.  mate / prop / leader are written inside the launch, so they are
+// read with ld.global.cg (L2), never through the incoherent L1.  ctl: [0..1] round flags (double
+// buffered), [2] n_c, [3] rounds.
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_match_coop(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                       const uint32_t* __restrict__ w, int* mate, int* prop,
+                                                       int* leader, int* bcnt, int* ctl, uint64_t salt, int off,
+                                                       int* __restrict__ agg_t) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int wsh[kBlock / 32];
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31, t = lane & (G - 1), gi = lane / G, wl = threadIdx.x >> 5;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gth = gridDim.x * blockDim.x;
+    auto block_sum = [&](int x) {  // every thread gets the block's sum
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) wsh[wl] = x;
+        __syncthreads();
+        int tot = 0;
+#pragma unroll
+        for (int k = 0; k < kBlock / 32; ++k) tot += wsh[k];
+        __syncthreads();
+        return tot;
+    };
+    for (int v = gtid; v < n; v += gth) mate[v] = -1;
+    if (gtid == 0) { ctl[0] = 0; ctl[1] = 0; }
+    grid.sync();
+    int r = 0;
+    for (;; ++r) {
+        bool found = false;
+        for (int base = wid * GPW; base < n; base += nw * GPW) {  // k_propose's body, list = all vertices
+            const int v = base + gi < n ? base + gi : -1;
+            const bool act = v >= 0 && __ldcg(&mate[v]) == -1;
+            uint32_t bw = 0;
+            uint64_t bh = 0;
+            int bu = -1;
+            if (act) {
+                const int p1 = rp[v + 1];
+                for (int p = rp[v] + t; p < p1; p += 4 * G) {
+                    int uu[4];
+                    uint32_t ww[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int q = p + k * G;
+                        uu[k] = q < p1 ? ci[q] : -1;
+                        ww[k] = q < p1 ? (w ? w[q] : 1u) : 0u;
+                    }
+                    bool fr[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) fr[k] = uu[k] >= 0 && __ldcg(&mate[uu[k]]) == -1;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (!fr[k]) continue;
+                        const int u = uu[k];
+                        const EKey key = make_key(ww[k], v, u, salt, off);
+                        if (bu < 0 || prop_gt(key.w, key.h, u, bw, bh, bu, v)) { bw = key.w; bh = key.h; bu = u; }
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                const uint32_t ow = __shfl_xor_sync(0xffffffffu, bw, o, G);
+                const uint64_t oh = __shfl_xor_sync(0xffffffffu, bh, o, G);
+                const int ou = __shfl_xor_sync(0xffffffffu, bu, o, G);
+                if (ou >= 0 && (bu < 0 || prop_gt(ow, oh, ou, bw, bh, bu, v))) { bw = ow; bh = oh; bu = ou; }
+            }
+            if (act && t == 0) {
+                if (bu < 0) mate[v] = -2;
+                prop[v] = bu;
+                found |= bu >= 0;
+            }
+        }
+        if (__syncthreads_or(found) && threadIdx.x == 0) atomicExch(&ctl[r & 1], 1);
+        grid.sync();
+        const bool go = __ldcg(&ctl[r & 1]) != 0;
+        if (!go) break;  // uniform: every thread read the flag after the barrier
+        if (gtid == 0) ctl[(r + 1) & 1] = 0;  // next round's flag (its writers start after the next barrier)
+        for (int v = gtid; v < n; v += gth) {  // k_accept
+            if (__ldcg(&mate[v]) != -1) continue;
+            const int u = __ldcg(&prop[v]);
+            if (u >= 0 && __ldcg(&prop[u]) == v) mate[v] = u;
+        }
+        grid.sync();
+    }
+    // attach (A3) + leader (A4) over a contiguous chunk per block, so ids can be numbered in vertex order
+    const int chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int v0 = min(n, blockIdx.x * chunk), v1 = min(n, v0 + chunk);
+    int cnt = 0;
+    for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+        const int m = __ldcg(&mate[v]);
+        int ld;
+        if (m >= 0) {
+            ld = v < m ? v : m;
+        } else if (rp[v + 1] > rp[v]) {
+            EKey bk{};
+            int bu = -1;
+            for (int p = rp[v]; p < rp[v + 1]; ++p) {
+                EKey k = make_key(w ? w[p] : 1u, v, ci[p], salt, off);
+                if (bu < 0 || key_gt(k, bk)) { bk = k; bu = ci[p]; }
+            }
+            const int mu = __ldcg(&mate[bu]);  // matched by maximality
+            ld = bu < mu ? bu : mu;
+        } else {
+            ld = v;
+        }
+        leader[v] = ld;
+        cnt += ld == v;  // leader flag: the smaller end of a pair, or an isolated vertex
+    }
+    cnt = block_sum(cnt);
+    if (threadIdx.x == 0) bcnt[blockIdx.x] = cnt;
+    grid.sync();
+    int pre = 0;
+    for (int k = threadIdx.x; k < (int)blockIdx.x; k += blockDim.x) pre += __ldcg(&bcnt[k]);
+    pre = block_sum(pre);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        ctl[2] = pre + cnt;
+        ctl[3] = r + 1;
+    }
+    // ids: exclusive scan of the leader flags in vertex order (prop reused as the id array)
+    for (int b0 = v0; b0 < v1; b0 += blockDim.x) {
+        const int v = b0 + threadIdx.x;
+        const bool fl = v < v1 && __ldcg(&leader[v]) == v;
+        const unsigned bal = __ballot_sync(0xffffffffu, fl);
+        if (lane == 0) wsh[wl] = __popc(bal);
+        __syncthreads();
+        int wpre = 0, tot = 0;
+        for (int k = 0; k < kBlock / 32; ++k) {
+            const int x = wsh[k];
+            if (k < wl) wpre += x;
+            tot += x;
+        }
+        if (fl) prop[v] = pre + wpre + __popc(bal & ((1u << lane) - 1u));
+        pre += tot;
+        __syncthreads();
+    }
+    grid.sync();
+    for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) agg_t[v] = __ldcg(&prop[__ldcg(&leader[v])]);
+}
+
 int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, int* nc, int* rounds, cudaStream_t s) {
     const int n = G.n;
+    const uint32_t* Gw = G.unit ? nullptr : G.w;  // unit multiplicities: not read
     int* mate = dalloc<int>(n, s);
     int* prop = dalloc<int>(n, s);
     int* any = dalloc<int>(4, s);
-    CK(cudaMemsetAsync(mate, 0xff, sizeof(int) * (size_t)n, s));
     int r = 0;
     const int g = grid_for(n);
-    // Rounds are issued in batches of 3 and only the last round's "some vertex proposed" flag is
-    // read back: a round without proposals means the matching is maximal, and further rounds are
-    // no-ops, so the result does not depend on the batch size.
+    // Rounds are issued in batches of 3, each batch followed by the compaction of the free list; the
+    // matching is maximal once no vertex is left free (a vertex with no free neighbour settles at
+    // mate -2 in its next proposal), and further rounds are no-ops, so the result does not depend
+    // on the batch size.
     constexpr int kBatch = 3;
     static int gsel = -1;
     if (gsel < 0) gsel = getenv("AMG_PROPOSE_G") ? atoi(getenv("AMG_PROPOSE_G")) : 0;
@@ -527,67 +729,118 @@ int aggregate_pass(const PassGraph& G, uint64_t salt, int id_off, int* agg_t, in
         Gl = 2;
         while (Gl < 16 && 4.0 * Gl < dg) Gl <<= 1;
     }
-    // after the first batch the rounds run over the vertices still free (a shrinking list)
-    int* list = nullptr;
-    int* list2 = nullptr;
-    int* nsel = dalloc<int>(2, s);
-    int* hsel = static_cast<int*>(pinned_scratch()) + 20;
-    int nv = n;
-    void* tmp = nullptr;
-    size_t tb = 0;
+    // small pass graphs: the whole pass in one cooperative launch (AMG_COOP_MATCH = largest n; 0 = off)
+    static int coop_max = -1;
+    if (coop_max < 0) coop_max = getenv("AMG_COOP_MATCH") ? atoi(getenv("AMG_COOP_MATCH")) : (1 << 20);
+    if (n > 0 && n <= coop_max) {
+        void (*fn)(int, const int*, const int*, const uint32_t*, int*, int*, int*, int*, int*, uint64_t, int, int*);
+        switch (Gl) {
+            case 1: fn = k_match_coop<1>; break;
+            case 2: fn = k_match_coop<2>; break;
+            case 4: fn = k_match_coop<4>; break;
+            case 8: fn = k_match_coop<8>; break;
+            default: fn = k_match_coop<16>; break;
+        }
+        int bpsm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, fn, kBlock, 0));
+        int dev = 0, nsm = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const int want = (int)std::max<int64_t>(1, ((int64_t)n * Gl + kBlock - 1) / kBlock);
+        const int nb = std::min(want, bpsm * nsm);
+        if (nb >= 1 && bpsm >= 1) {
+            int* leader = dalloc<int>((size_t)n + 1, s);
+            int* bcnt = dalloc<int>((size_t)nb + 1, s);
+            int* ctl = dalloc<int>(4, s);
+            int n_ = n, off_ = id_off;
+            uint64_t salt_ = salt;
+            const int* rp_ = G.rp;
+            const int* ci_ = G.ci;
+            const uint32_t* w_ = Gw;
+            void* args[] = {&n_, &rp_, &ci_, &w_, &mate, &prop, &leader, &bcnt, &ctl, &salt_, &off_, &agg_t};
+            CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(nb), dim3(kBlock), args, 0, s));
+            ++g_launches;
+            int* h = static_cast<int*>(pinned_scratch()) + 28;
+            CK(cudaMemcpyAsync(h, ctl + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            *nc = h[0];
+            *rounds = h[1];
+            dfree(leader, s);
+            dfree(bcnt, s);
+            dfree(ctl, s);
+            dfree(mate, s);
+            dfree(prop, s);
+            dfree(any, s);
+            return 0;
+        }
+    }
+    CK(cudaMemsetAsync(mate, 0xff, sizeof(int) * (size_t)n, s));
+    // After the first batch the rounds run over the vertices still free (a shrinking list).  The list
+    // and its length stay on the device: batch b+1 is issued before batch b's length is known on the
+    // host (its kernels read the length from device memory), so the host's read-back of batch b
+    // overlaps batch b+1 and the GPU never waits on it.  When batch b leaves no free vertex the
+    // matching is maximal and batch b+1 runs on an empty list (a no-op); the result does not depend
+    // on the batching.
+    int* lists = dalloc<int>(2 * ((size_t)n + 8), s);
+    constexpr int R = 4;  // ring of device counts / pinned mirrors / events
+    int* dcnt = dalloc<int>(R, s);
+    volatile int* hcnt = static_cast<int*>(pinned_scratch()) + 20;
+    cudaEvent_t ev[R];
+    for (int k = 0; k < R; ++k) CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
     static int first = -1;  // rounds before the first free-list compaction (AMG_MATCH_FIRST; 2 measured best)
     if (first < 0) first = getenv("AMG_MATCH_FIRST") ? std::max(1, atoi(getenv("AMG_MATCH_FIRST"))) : 2;
-    for (;;) {
-        const int gp = std::max(1, std::min((int)(((int64_t)nv * Gl + kBlock - 1) / kBlock), 148 * 8));
-        const int ga = std::max(1, std::min(grid_for(nv), 148 * 8));
-        // small graphs (coarse levels): rounds cost ~5 us, a read-back ~20 us of idle GPU, so the
-        // batches are longer there (C3 levels 1-3 finish a pass in one or two batches)
-        const bool small = n <= 200000;
-        const int nb = list ? (small ? 4 : kBatch) : (small ? 6 : first);
+    // small graphs (coarse levels): rounds cost ~5 us, so the batches are longer there
+    const bool small = n <= 200000;
+    auto issue = [&](int b, int nv_ub) {  // batch b: rounds over list b, then list b+1 and its length
+        const int* list = b ? lists + (size_t)(b & 1) * (n + 8) : nullptr;
+        const int* nvp = b ? dcnt + (b - 1) % R : nullptr;
+        int* out = lists + (size_t)((b + 1) & 1) * (n + 8);
+        const int nb = b ? (small ? 4 : kBatch) : (small ? 6 : first);
+        const int gp = std::max(1, std::min((int)(((int64_t)nv_ub * Gl + kBlock - 1) / kBlock), 148 * 8));
+        const int ga = std::max(1, std::min(grid_for(nv_ub), 148 * 8));
         for (int k = 0; k < nb; ++k) {
-            CK(cudaMemsetAsync(any, 0, sizeof(int), s));
             switch (Gl) {
-                case 1: k_propose<1><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
-                case 2: k_propose<2><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
-                case 4: k_propose<4><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
-                case 8: k_propose<8><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
-                default: k_propose<16><<<gp, kBlock, 0, s>>>(nv, list, G.rp, G.ci, G.w, mate, prop, salt, id_off, any); break;
+                case 1: k_propose<1><<<gp, kBlock, 0, s>>>(nv_ub, nvp, list, G.rp, G.ci, Gw, mate, prop, salt, id_off, any); break;
+                case 2: k_propose<2><<<gp, kBlock, 0, s>>>(nv_ub, nvp, list, G.rp, G.ci, Gw, mate, prop, salt, id_off, any); break;
+                case 4: k_propose<4><<<gp, kBlock, 0, s>>>(nv_ub, nvp, list, G.rp, G.ci, Gw, mate, prop, salt, id_off, any); break;
+                case 8: k_propose<8><<<gp, kBlock, 0, s>>>(nv_ub, nvp, list, G.rp, G.ci, Gw, mate, prop, salt, id_off, any); break;
+                default: k_propose<16><<<gp, kBlock, 0, s>>>(nv_ub, nvp, list, G.rp, G.ci, Gw, mate, prop, salt, id_off, any); break;
             }
-            ++g_launches;
-            k_accept<<<ga, kBlock, 0, s>>>(nv, list, mate, prop);
-            ++g_launches;
+            k_accept<<<ga, kBlock, 0, s>>>(nv_ub, nvp, list, mate, prop);
+            g_launches += 2;
         }
+        CK(cudaMemsetAsync(dcnt + b % R, 0, sizeof(int), s));
+        const int gc = std::max(1, std::min((int)((nv_ub + kBlock * 16 - 1) / (kBlock * 16)), 148 * 8));
+        k_compact_free<<<gc, kBlock, 0, s>>>(nv_ub, nvp, list, mate, out, dcnt + b % R);
+        ++g_launches;
         CK(cudaGetLastError());
-        // next batch's list: the vertices still free
-        if (!list) {
-            list = dalloc<int>((size_t)n + 1, s);
-            list2 = dalloc<int>((size_t)n + 1, s);
-            size_t tb2 = 0;
-            CK(cub::DeviceSelect::If(nullptr, tb, thrust::counting_iterator<int>(0), list, nsel, n, IsFree{mate}, s));
-            CK(cub::DeviceSelect::If(nullptr, tb2, list, list2, nsel, n, IsFree{mate}, s));
-            tb = std::max(tb, tb2);
-            tmp = dalloc<char>(tb, s);
-            CK(cub::DeviceSelect::If(tmp, tb, thrust::counting_iterator<int>(0), list, nsel, n, IsFree{mate}, s));
-        } else {
-            CK(cub::DeviceSelect::If(tmp, tb, list, list2, nsel, nv, IsFree{mate}, s));
-            std::swap(list, list2);
-        }
-        CK(cudaMemcpyAsync(nsel + 1, any, sizeof(int), cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(hsel, nsel, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpyAsync((void*)(hcnt + b % R), dcnt + b % R, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ev[b % R], s));
+        return nb;
+    };
+    int nv_ub = n;
+    int nb = issue(0, nv_ub);
+    for (int b = 0;; ++b) {
+        const int nb_next = issue(b + 1, nv_ub);  // speculative: a no-op if batch b ends the matching
+        CK(cudaEventSynchronize(ev[b % R]));
         r += nb;
-        if (!hsel[1] || hsel[0] == 0) break;
-        nv = hsel[0];
-        if (r > 30000) throw Error(-7, "matching did not terminate");
+        const int left = hcnt[b % R];
+        if (left == 0) break;
+        nv_ub = left;
+        nb = nb_next;
+        if (r > 30000) {
+            CK(cudaStreamSynchronize(s));
+            for (int k = 0; k < R; ++k) cudaEventDestroy(ev[k]);
+            throw Error(-7, "matching did not terminate");
+        }
     }
-    dfree(list, s);
-    dfree(list2, s);
-    dfree(tmp, s);
-    dfree(nsel, s);
+    for (int k = 0; k < R; ++k) CK(cudaEventDestroy(ev[k]));
+    dfree(lists, s);
+    dfree(dcnt, s);
     int* leader = prop;  // reuse
     int* isl = dalloc<int>((size_t)n + 1, s);
     CK(cudaMemsetAsync(isl + n, 0, sizeof(int), s));
-    k_leader<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, G.w, mate, salt, id_off, leader, isl);
+    k_leader<<<g, kBlock, 0, s>>>(n, G.rp, G.ci, Gw, mate, salt, id_off, leader, isl);
     ++g_launches;
     CK(cudaGetLastError());
     int* id = dalloc<int>((size_t)n + 1, s);

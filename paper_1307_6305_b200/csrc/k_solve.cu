@@ -1625,13 +1625,89 @@ void launch_direction(int n, const double* z, const double* const* D, const doub
     ++g_launches;
 }
 
+// Outer FCG at the last window position p = W (W >= 1 earlier directions): the direction
+// d_p = z - sum_j beta_j d_j of k_direction, fused with the deferred x updates of the window.  The
+// d_j it loads anyway are reused for x += a_j d_j (j < p), and before d_p overwrites its slot the
+// slot's old content -- the previous window's last direction, pending if *has_old -- is applied
+// first.  The fma sequence is the one of the per-iteration updates (previous window's last, then
+// this window's in order), so x is bitwise the same.
+template <int W>
+__global__ void __launch_bounds__(kBlock) k_direction_xf(int n, const double* __restrict__ z, PtrArr D,
+                                                         const double* __restrict__ c, const double* __restrict__ dq,
+                                                         double* __restrict__ d, double* __restrict__ x,
+                                                         const double* __restrict__ alph, const int* __restrict__ has_old) {
+    double beta[W], al[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        beta[j] = dq[j] != 0.0 ? c[j] / dq[j] : 0.0;  // d_j = 0: no term (A13)
+        al[j] = alph[j];
+    }
+    const bool ho = *has_old != 0;
+    const double aold = alph[W];  // the slot d_p overwrites: the previous window's last alpha
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n2 = n >> 1;
+    const double2* Z2 = reinterpret_cast<const double2*>(z);
+    double2* O2 = reinterpret_cast<double2*>(d);
+    double2* X2 = reinterpret_cast<double2*>(x);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += st) {
+        double2 va = Z2[i], xi = X2[i], od = make_double2(0.0, 0.0);
+        if (ho) od = O2[i];
+        double2 pj[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) pj[j] = reinterpret_cast<const double2*>(D.p[j])[i];
+        if (ho) { xi.x += aold * od.x; xi.y += aold * od.y; }
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            xi.x += al[j] * pj[j].x;
+            xi.y += al[j] * pj[j].y;
+            va.x -= beta[j] * pj[j].x;
+            va.y -= beta[j] * pj[j].y;
+        }
+        X2[i] = xi;
+        O2[i] = va;
+    }
+    for (int64_t i = (n2 << 1) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) {
+        double v = z[i], xi = x[i];
+        if (ho) xi += aold * d[i];
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const double p = D.p[j][i];
+            xi += al[j] * p;
+            v -= beta[j] * p;
+        }
+        x[i] = xi;
+        d[i] = v;
+    }
+}
+
+bool direction_xf_ok(int w, const double* z, const double* const* D, const double* d, const double* x) {
+    return w >= 1 && w <= 4 && al16(z) && al16(d) && al16(x) && all_al16(D, w);
+}
+
+void launch_direction_xf(int n, const double* z, const double* const* D, const double* c, const double* dq, int w,
+                         double* d, double* x, const double* alph, const int* has_old, cudaStream_t s) {
+    if (!direction_xf_ok(w, z, D, d, x)) throw Error(-1, "launch_direction_xf: unsupported window");
+    PtrArr a{};
+    for (int j = 0; j < w; ++j) a.p[j] = D[j];
+    const dim3 g(vgrid((n + 1) / 2)), b(kBlock);
+    switch (w) {
+        case 1: launch_k(k_direction_xf<1>, g, b, 0, s, n, z, a, c, dq, d, x, alph, has_old); break;
+        case 2: launch_k(k_direction_xf<2>, g, b, 0, s, n, z, a, c, dq, d, x, alph, has_old); break;
+        case 3: launch_k(k_direction_xf<3>, g, b, 0, s, n, z, a, c, dq, d, x, alph, has_old); break;
+        default: launch_k(k_direction_xf<4>, g, b, 0, s, n, z, a, c, dq, d, x, alph, has_old); break;
+    }
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
 // x (+)= alpha d; r -= alpha q; rr = r.r;  alpha = d.r / d.q (outer: d.q <= 0 or NaN is a breakdown)
-template <bool ASSIGN, bool UPD_R, bool RR, bool V>
+// NOX: the x update is deferred (launch_x_flush); alpha goes to alpha_out, and d and x are not touched
+template <bool ASSIGN, bool UPD_R, bool RR, bool V, bool NOX = false>
 __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __restrict__ dr,
                                                        const double* __restrict__ dq, const double* __restrict__ d,
                                                        const double* __restrict__ q, double* __restrict__ x,
                                                        double* __restrict__ r, int* breakdown, double* partials,
-                                                       unsigned* ticket, double* rr) {
+                                                       unsigned* ticket, double* rr, double* alpha_out, int* set_old) {
     const double den = *dq;
     double alpha;
     if (breakdown) {  // outer FCG: d.q <= 0 or NaN is a breakdown
@@ -1639,6 +1715,10 @@ __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __re
         if (!(den > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) *breakdown = 1;
     } else {          // inner: rho = 0 => d = 0 => 0/0, take alpha = 0 (DESIGN.md readings)
         alpha = (den != 0.0) ? (*dr) / den : 0.0;
+    }
+    if (NOX && blockIdx.x == 0 && threadIdx.x == 0) {
+        *alpha_out = alpha;
+        if (set_old) *set_old = 1;  // this slot's update is now pending (k_direction_xf applies it)
     }
     double acc[1] = {0.0};
     const int64_t st = (int64_t)gridDim.x * blockDim.x;
@@ -1651,13 +1731,15 @@ __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __re
         double2* R2 = reinterpret_cast<double2*>(r);
         int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
         for (; i < n2; i += st) {
-            const double2 di = D2[i];
-            double2 xi;
-            if (!ASSIGN) xi = X2[i];
             double2 ri, qi;
             if (UPD_R) { ri = R2[i]; qi = Q2[i]; }
-            if (ASSIGN) { xi.x = alpha * di.x; xi.y = alpha * di.y; } else { xi.x += alpha * di.x; xi.y += alpha * di.y; }
-            X2[i] = xi;
+            if (!NOX) {
+                const double2 di = D2[i];
+                double2 xi;
+                if (!ASSIGN) xi = X2[i];
+                if (ASSIGN) { xi.x = alpha * di.x; xi.y = alpha * di.y; } else { xi.x += alpha * di.x; xi.y += alpha * di.y; }
+                X2[i] = xi;
+            }
             if (UPD_R) {
                 ri.x = ri.x - alpha * qi.x;
                 ri.y = ri.y - alpha * qi.y;
@@ -1668,8 +1750,10 @@ __global__ void __launch_bounds__(kBlock) k_fcg_update(int n, const double* __re
         i0 = n2 << 1;
     }
     for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) {
-        double di = d[i];
-        if (ASSIGN) x[i] = alpha * di; else x[i] += alpha * di;
+        if (!NOX) {
+            double di = d[i];
+            if (ASSIGN) x[i] = alpha * di; else x[i] += alpha * di;
+        }
         if (UPD_R) {
             double ri = r[i] - alpha * q[i];
             r[i] = ri;
@@ -1686,25 +1770,100 @@ static void fcg_update_v(dim3 g, dim3 b, cudaStream_t s, int n, const double* dr
     double* np = nullptr;
     unsigned* nt = nullptr;
     if (assign_x) {
-        if (r) launch_k(k_fcg_update<true, true, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
-        else   launch_k(k_fcg_update<true, false, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        if (r) launch_k(k_fcg_update<true, true, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np, np, nullptr);
+        else   launch_k(k_fcg_update<true, false, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np, np, nullptr);
     } else if (r && rr) {
-        launch_k(k_fcg_update<false, true, true, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, ds.partials, ds.ticket, rr);
+        launch_k(k_fcg_update<false, true, true, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, ds.partials, ds.ticket, rr, np, nullptr);
     } else if (r) {
-        launch_k(k_fcg_update<false, true, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        launch_k(k_fcg_update<false, true, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np, np, nullptr);
     } else {
-        launch_k(k_fcg_update<false, false, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np);
+        launch_k(k_fcg_update<false, false, false, V>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown, np, nt, np, np, nullptr);
     }
 }
 
 void launch_fcg_update(int n, const double* dr, const double* dq, const double* d, const double* q, double* x,
-                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s) {
+                       bool assign_x, double* r, double* rr, int* breakdown, const DotScratch& ds, cudaStream_t s,
+                       double* alpha_out, int* set_old) {
     const bool v = al16(d) && al16(x) && (!r || (al16(r) && al16(q)));
     const dim3 g(vgrid(v ? (n + 1) / 2 : n)), b(kBlock);
+    if (!x) {  // deferred x update (outer FCG): r -= alpha q, rr = r.r, alpha stored
+        if (!r || !rr || !alpha_out || assign_x) throw Error(-1, "launch_fcg_update: bad deferred update");
+        if (v) launch_k(k_fcg_update<false, true, true, true, true>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown,
+                        ds.partials, ds.ticket, rr, alpha_out, set_old);
+        else   launch_k(k_fcg_update<false, true, true, false, true>, g, b, 0, s, n, dr, dq, d, q, x, r, breakdown,
+                        ds.partials, ds.ticket, rr, alpha_out, set_old);
+        CK(cudaGetLastError());
+        ++g_launches;
+        return;
+    }
     if (v)
         fcg_update_v<true>(g, b, s, n, dr, dq, d, q, x, assign_x, r, rr, breakdown, ds);
     else
         fcg_update_v<false>(g, b, s, n, dr, dq, d, q, x, assign_x, r, rr, breakdown, ds);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+// deferred outer-FCG x update: x = (((x + a_{j0} d_{j0}) + a_{j1} d_{j1}) + ...) over the window
+// slots sl.j[0..cnt) in that order (the order of the iterations they belong to).  One pass over x and
+// the directions instead of one x read-modify-write per iteration.  C > 0: compile-time count (the C
+// direction loads of a step in flight together); C = 0: runtime cnt.
+template <int C, bool V>
+__global__ void __launch_bounds__(kBlock) k_x_flush(int n, double* __restrict__ x, const double* __restrict__ D,
+                                                    size_t ld, const double* __restrict__ a, Slots sl, int cnt) {
+    constexpr int M = C > 0 ? C : kMaxWin;
+    if (C > 0) cnt = C;
+    double al[M];
+    const double* dp[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        al[j] = j < cnt ? a[sl.j[j]] : 0.0;
+        dp[j] = D + (size_t)(j < cnt ? sl.j[j] : 0) * ld;
+    }
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int64_t i0 = 0;
+    if constexpr (V && C > 0) {
+        const int64_t n2 = n >> 1;
+        double2* X2 = reinterpret_cast<double2*>(x);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += st) {
+            double2 dj[C];
+#pragma unroll
+            for (int j = 0; j < C; ++j) dj[j] = __ldcs(reinterpret_cast<const double2*>(dp[j]) + i);
+            double2 xi = X2[i];
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+                xi.x += al[j] * dj[j].x;
+                xi.y += al[j] * dj[j].y;
+            }
+            X2[i] = xi;
+        }
+        i0 = n2 << 1;
+    }
+    for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += st) {
+        double xi = x[i];
+        for (int j = 0; j < cnt; ++j) xi += al[j] * dp[j][i];
+        x[i] = xi;
+    }
+}
+
+void launch_x_flush(int n, double* x, const double* D, size_t ld, const double* a, const Slots& sl, int cnt,
+                    cudaStream_t s) {
+    if (cnt <= 0) return;
+    if (cnt > kMaxWin) throw Error(-1, "launch_x_flush: cnt > kMaxWin");
+    const bool v = al16(x) && al16(D) && (ld % 2) == 0;
+    const dim3 g(vgrid(v ? (n + 1) / 2 : n)), b(kBlock);
+    if (v) {
+        switch (cnt) {
+            case 1: launch_k(k_x_flush<1, true>, g, b, 0, s, n, x, D, ld, a, sl, cnt); break;
+            case 2: launch_k(k_x_flush<2, true>, g, b, 0, s, n, x, D, ld, a, sl, cnt); break;
+            case 3: launch_k(k_x_flush<3, true>, g, b, 0, s, n, x, D, ld, a, sl, cnt); break;
+            case 4: launch_k(k_x_flush<4, true>, g, b, 0, s, n, x, D, ld, a, sl, cnt); break;
+            case 5: launch_k(k_x_flush<5, true>, g, b, 0, s, n, x, D, ld, a, sl, cnt); break;
+            default: launch_k(k_x_flush<0, false>, dim3(vgrid(n)), b, 0, s, n, x, D, ld, a, sl, cnt); break;
+        }
+    } else {
+        launch_k(k_x_flush<0, false>, g, b, 0, s, n, x, D, ld, a, sl, cnt);
+    }
     CK(cudaGetLastError());
     ++g_launches;
 }

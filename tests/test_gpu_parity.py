@@ -779,3 +779,37 @@ def test_inner_fcg_forms_parity(amg, gen_mod, oracle_mod, monkeypatch, zform):
             H.assert_close(z, hier.precond(r, nu=2, level=l), 1e-10)
     finally:
         amg.amg_free(h)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("restart", [1, 2, 3, 5, 7])
+def test_deferred_x_updates_any_window(amg, gen_mod, oracle_mod, restart):
+    """The outer FCG defers x += alpha_k d_k (flushed at the window end, or inside the last window
+    position's direction kernel for restart 2..5, and at the end of the solve).  Stopping after any
+    number of iterations -- mid-window, at a window end, or right after one -- the returned x must
+    carry every update exactly once: its true residual equals the recursive one, and at convergence
+    x equals the oracle's with the same restart."""
+    p = gen_mod.problem("C2", size=200)
+    b = gen_mod.rhs(p.n, 3)
+    for K in (1, 2, 3, 4, 5, 6, 7, 8, 11):
+        o = amg.amg_options_default(coarsest_size=p.params.get("coarsest_size", 100), restart=restart, max_iter=K)
+        h = amg.amg_setup(p.rp, p.ci, p.val, p.d, p.params["passes"], p.params["degree"], o)
+        try:
+            x = np.zeros(p.n)
+            st, it, rr = amg.amg_solve(h, b, x, 1e-14, 2)
+            info = amg.amg_get_info(h)
+            assert it == K and st != 0
+            # ||b - A x|| / ||b|| (x from the deferred updates) vs the FCG's recursive ||r_K|| / ||b||
+            assert abs(info["last_true_relres"] - rr) <= 1e-9 * max(1.0, rr), (K, info["last_true_relres"], rr)
+        finally:
+            amg.amg_free(h)
+    hier = oracle_mod.setup_problem(p, restart=restart)
+    ref = hier.solve(b, tol=1e-8, nu=2)
+    h = gpu_setup(amg, p, restart=restart)
+    try:
+        x = np.zeros(p.n)
+        st, it, rr = amg.amg_solve(h, b, x, 1e-8, 2)
+        assert st == 0 and abs(it - ref["iters"]) <= 1, (it, ref["iters"])
+        H.assert_close(x, ref["x"], 1e-6)
+    finally:
+        amg.amg_free(h)
