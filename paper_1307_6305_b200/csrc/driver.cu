@@ -17,9 +17,6 @@
 #include <cstdlib>
 #include <string>
 #include <condition_variable>
-#include <deque>
-#include <functional>
-#include <future>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -179,66 +176,7 @@ GraphReaper* reaper() {
     return g_reaper;
 }
 
-// One background host thread that builds level formats during setup (see amg_hierarchy::fs).  It is
-// persistent so that its thread-local pinned read-back scratch is allocated once per process.
-struct FormatWorker {
-    std::mutex mu;
-    std::condition_variable cv;
-    std::deque<std::packaged_task<void()>> q;
-    bool stop = false;
-    std::thread th;
-    FormatWorker() : th([this] { run(); }) {}
-    void run() {
-        std::unique_lock<std::mutex> lk(mu);
-        for (;;) {
-            cv.wait(lk, [this] { return stop || !q.empty(); });
-            if (q.empty()) return;  // stop requested and nothing pending
-            auto job = std::move(q.front());
-            q.pop_front();
-            lk.unlock();
-            job();  // exceptions land in the job's future
-            lk.lock();
-        }
-    }
-    std::future<void> submit(std::function<void()> fn) {
-        std::packaged_task<void()> t(std::move(fn));
-        std::future<void> f = t.get_future();
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            q.push_back(std::move(t));
-        }
-        cv.notify_one();
-        return f;
-    }
-    void shutdown() {
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            stop = true;
-        }
-        cv.notify_one();
-        if (th.joinable()) th.join();
-    }
-};
-FormatWorker* g_fmt_worker = nullptr;
-std::mutex g_fmt_mu;
-FormatWorker* fmt_worker() {
-    std::lock_guard<std::mutex> lk(g_fmt_mu);
-    if (!g_fmt_worker) {
-        g_fmt_worker = new FormatWorker();
-        std::atexit([] { if (g_fmt_worker) g_fmt_worker->shutdown(); });
-    }
-    return g_fmt_worker;
-}
 }  // namespace
-
-// waits for the handle's format jobs (errors swallowed: used on teardown paths)
-static void drain_format_jobs(amg_hierarchy* h) {
-    for (auto& f : h->fmt_jobs)
-        if (f.valid()) {
-            try { f.get(); } catch (...) {}
-        }
-    h->fmt_jobs.clear();
-}
 
 static void destroy_graphs(amg_hierarchy* h, bool deferred = false) {
     int dev = 0;
@@ -315,8 +253,6 @@ static void release(amg_hierarchy* h) {
     static const bool trace = getenv("AMG_FREE_TRACE") != nullptr;
     const double t0 = trace ? now_ms() : 0.0;
     destroy_graphs(h, true);
-    drain_format_jobs(h);
-    if (h->fs) cudaStreamSynchronize(h->fs);
     const double t1 = trace ? now_ms() : 0.0;
     if (h->s) {
         for (int l = 0; l < h->L; ++l) {
@@ -341,7 +277,6 @@ static void release(amg_hierarchy* h) {
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
     if (h->ev_halo) cudaEventDestroy(h->ev_halo);
     if (h->cs) cudaStreamDestroy(h->cs);
-    if (h->fs) stream_release(h->dev, h->fs);
     if (h->s) stream_release(h->dev, h->s);
     delete h;
 }
@@ -474,8 +409,6 @@ static void build(amg_hierarchy* h, int64_t n64, const int64_t* rp_in, const int
     free_inputs();
     h->L = 1;
     pt.mark("form A0");
-    static const bool fmt_overlap = getenv("AMG_FORMAT_OVERLAP") != nullptr && getenv("AMG_SETUP_TRACE") == nullptr;
-    if (fmt_overlap && n > h->opt.coarsest_size) h->fs = stream_acquire(h->dev);
     build_levels(h, 0, agg0, nc0);
     finish_build(h);
 }
@@ -529,36 +462,6 @@ int* amg::aggregate_level(amg_hierarchy* h, int l, PassGraph& G, int* nc_out) {
     return agg;
 }
 
-// SpMV formats of level k (SELL, or CSR row tiles when too irregular; lossless compression)
-static void build_formats(amg_hierarchy* h, int k, cudaStream_t s) {
-    Level& Lv = h->lev[k];
-    if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
-    if (!Lv.S.sptr) Lv.T = build_tiles(Lv.A, 0, s);  // only the levels too irregular for SELL use them
-    if (Lv.S.sptr && h->opt.compress) compress_sell(Lv.S, Lv.A, s);
-}
-
-// Level l will be coarsened, so the solve runs SpMV-class kernels on it: hand its formats to the
-// worker thread (side stream fs, ordered after A_l on s).  They depend on A_l only, and their
-// bandwidth-bound kernels fill the device while the matching passes of level l run their small
-// latency-bound rounds on s.  C3: setup 17.0 -> see DESIGN 7 (AMG_NO_FORMAT_OVERLAP=1 for A/B).
-static void submit_formats(amg_hierarchy* h, int l) {
-    if (!h->fs) return;
-    cudaEvent_t ev;
-    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CK(cudaEventRecord(ev, h->s));
-    CK(cudaStreamWaitEvent(h->fs, ev, 0));
-    CK(cudaEventDestroy(ev));
-    if ((int)h->fmt_jobs.size() <= l) h->fmt_jobs.resize(l + 1);
-    const int dev = h->dev;
-    cudaStream_t fs = h->fs;
-    h->fmt_jobs[l] = fmt_worker()->submit([h, l, dev, fs] {
-        CK(cudaSetDevice(dev));
-        const long long before = g_launches;
-        build_formats(h, l, fs);
-        h->fmt_launches[l] = g_launches - before;  // this thread's counter; added to the caller's at the join
-    });
-}
-
 void amg::build_levels(amg_hierarchy* h, int l0, int* agg0, int nc0) {
     cudaStream_t s = h->s;
     PhaseTimer pt(s);
@@ -584,7 +487,6 @@ void amg::build_levels(amg_hierarchy* h, int l0, int* agg0, int nc0) {
         pt.mark("lambda1", l);
         if (Lv.A.n <= h->opt.coarsest_size) break;
         if (l + 1 >= kMaxLevels) throw Error(AMG_E_SETUP, "too many levels");
-        submit_formats(h, l);
         int* agg = nullptr;
         int nc = Lv.A.n;
         if (l == l0 && agg0) {  // level 0's aggregation already ran (overlapped with the value copies)
@@ -705,26 +607,18 @@ void amg::finish_build(amg_hierarchy* h) {
     h->allocs.push_back(h->Minv);
     pt.mark("coarse inverse", h->L - 1);
     // SpMV formats of every level the SpMV-class kernels run on (all but the coarsest; level 0 always)
-    bool fmt_joined = false;
     for (int k = 0; k < h->L; ++k) {
         Level& Lv = h->lev[k];
         if (k < h->L - 1 || k == 0) {
-            if (k < (int)h->fmt_jobs.size() && h->fmt_jobs[k].valid()) {
-                h->fmt_jobs[k].get();  // built on the side stream by the worker; rethrows its error
-                g_launches += h->fmt_launches[k];
-                fmt_joined = true;
-                pt.mark("formats (joined)", k);
-            } else {
-                if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
-                if (Lv.S.sptr) Lv.S.chi = Lv.A.n + Lv.H.nhi - 1;
-                pt.mark("sell", k);
-                if (!Lv.S.sptr) {  // CSR row tiles: only the levels too irregular for SELL use them
-                    Lv.T = build_tiles(Lv.A, 0, s);
-                    pt.mark("tiles", k);
-                }
-                if (Lv.S.sptr && h->opt.compress) compress_sell(Lv.S, Lv.A, s);
-                pt.mark("compress", k);
+            if (!getenv("AMG_NO_SELL")) Lv.S = build_sell(Lv.A, 1.6, s);
+            if (Lv.S.sptr) Lv.S.chi = Lv.A.n + Lv.H.nhi - 1;
+            pt.mark("sell", k);
+            if (!Lv.S.sptr) {  // CSR row tiles: only the levels too irregular for SELL use them
+                Lv.T = build_tiles(Lv.A, 0, s);
+                pt.mark("tiles", k);
             }
+            if (Lv.S.sptr && h->opt.compress) compress_sell(Lv.S, Lv.A, s);
+            pt.mark("compress", k);
         }
         Lv.op.A = Lv.A;
         Lv.op.T = Lv.T;
@@ -748,13 +642,6 @@ void amg::finish_build(amg_hierarchy* h) {
         // vector layout [pad | lower halo | own | upper halo]
         Lv.lo_pad = (Lv.H.nlo + 3) & ~3;
         Lv.ld = Lv.dist ? ((Lv.lo_pad + Lv.A.n + Lv.H.nhi + 3) & ~3) : ((Lv.A.n + 3) & ~3);  // 32-byte aligned slots
-    }
-    if (fmt_joined) {  // the solve's stream sees the side stream's formats
-        cudaEvent_t ev;
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev, h->fs));
-        CK(cudaStreamWaitEvent(s, ev, 0));
-        CK(cudaEventDestroy(ev));
     }
     pt.mark("formats");
     // level workspaces

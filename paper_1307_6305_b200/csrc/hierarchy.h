@@ -6,7 +6,6 @@
 
 #include <cuda_runtime.h>
 
-#include <future>
 #include <vector>
 
 #include "../../include/amg.h"
@@ -110,12 +109,6 @@ struct amg_hierarchy {
     std::vector<long long> graph_launches_pos;  // per restart-window position
     std::vector<void*> allocs;
     std::vector<void*> ws_allocs;
-    // single-GPU setup: the SpMV formats (SELL, compression, tiles) of level l are built by the
-    // library's worker thread on the side stream fs as soon as A_l exists, while the level loop
-    // aggregates level l on s (finish_build joins)
-    cudaStream_t fs = nullptr;
-    std::vector<std::future<void>> fmt_jobs;  // index = level
-    long long fmt_launches[amg::kMaxLevels] = {};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaEvent_t pe0 = nullptr, pe1 = nullptr;  // live profile of the level-0 smoother steps
     bool prof_on = false;
