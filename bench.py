@@ -253,7 +253,7 @@ CEILING = {"C3": 6.2e9, "C4": 4.8e9, "C5": 4.3e9}  # SURVEY 8(d) unknowns*iter/s
 
 
 def run_config(amg, torch, dev, stream, cfg, steps, **opt_over):
-    """One BASELINE config at full size on this GPU: 1 warm-up + `steps` timed steps (setup + solve
+    """One BASELINE config at full size on this GPU: 3 warm-up + `steps` timed steps (setup + solve
     + free, inputs resident in HBM, CUDA events on the caller's stream); the library's own device
     timings split setup / solve."""
     from inputs import gen
@@ -274,7 +274,8 @@ def run_config(amg, torch, dev, stream, cfg, steps, **opt_over):
         amg.amg_free(h)
         return st, it, rr, info
 
-    step()
+    for _ in range(3):  # W >= 3 warm-up steps (the GPU idles through the CPU baseline before these runs)
+        step()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)

@@ -672,7 +672,7 @@ void amg::finish_build(amg_hierarchy* h) {
     h->osc = halloc<double>(h, 2 * kMaxWin + 8);
     h->alph = halloc<double>(h, kMaxWin);
     h->xold = halloc<int>(h, 4);
-    h->flag = halloc<int>(h, 4);
+    h->flag = reinterpret_cast<int*>(h->osc + 2 * kMaxWin + 4);  // next to rr: one read-back per outer iteration
     h->ds.partials = halloc<double>(h, (size_t)(kMaxWin + 2) * 4096);
     h->ds.ticket = halloc<unsigned>(h, 4);
     CK(cudaMemsetAsync(h->ds.ticket, 0, 4 * sizeof(unsigned), s));
@@ -1306,7 +1306,7 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
     halo_exchange(h, 0, h->x);
     launch_resid(h->lev[0].op, h->x, h->b, h->r, rr, h->ds, s);
     if (dist) dot_allreduce(h, {rr, bb});
-    CK(cudaMemsetAsync(h->flag, 0, sizeof(int), s));
+    CK(cudaMemsetAsync(h->flag, 0, sizeof(double), s));
     CK(cudaMemcpyAsync(h->hsc, rr, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const double bnorm = std::sqrt(h->hsc[1]);
@@ -1348,12 +1348,12 @@ static int solve(amg_hierarchy* h, const double* b_in, double* x_out, double tol
             } else {
                 outer_iteration(h, pos, nu);
             }
-            CK(cudaMemcpyAsync(h->hsc, rr, sizeof(double), cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(h->hsc + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+            // rr and the breakdown flag in one 32-byte copy: osc slots +1..+4 = rr, bb, (mean scratch), flag
+            CK(cudaMemcpyAsync(h->hsc, rr, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (pos == h->W - 1) { pending = 0; oldp = h->xf; } else { pending = pos + 1; }
             int fl;
-            memcpy(&fl, h->hsc + 2, sizeof(int));
+            memcpy(&fl, h->hsc + 3, sizeof(int));
             if (h->L > 1) {
                 float pm = 0.f;
                 CK(cudaEventElapsedTime(&pm, h->pe0, h->pe1));
